@@ -1,0 +1,418 @@
+#!/usr/bin/env python3
+"""DynamiQ all-reduce benchmark (B200).  Prints ONE JSON line on rank 0.
+
+Workloads (BASELINE.json configs):
+  N = 1 : configs[1] — one B200 runs the full round of n_sim = 4 simulated
+          workers (stats, allocation, permuted ring reduce-scatter with leaf
+          compress + fused DAR per hop + sink, compressed gather decode) on
+          64M-entry synthetic Llama-like (per-super-group log-normal scale,
+          sigma_log = 4) fp32 gradients, 4-bit budget.
+  N > 1 : configs[2] — one rank per GPU (torchrun), 256M-entry (1 GiB fp32)
+          gradient per rank, ring, 4-bit budget; NCCL bf16 all-reduce timed
+          beside it.
+
+metric "effective GB/s": fp32 gradient bytes all-reduced per second summed
+over workers, (workers x 4 d) / t — whole-job, so weak scaling keeps per-GPU
+work fixed.  ``value`` is device-resident (inputs already in HBM); ``e2e`` runs
+the same round through the C-ABI from pinned host buffers (H2D of every input
+and D2H of the sum inside the timed region).
+
+``--impl reference`` times the reference's own CPU implementation of the path
+(oracle/_ref: the reference library compiled from its sources) on this box's
+host cores, on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "DynamiQ all-reduce effective GB/s (4-bit budget, fp32-equivalent bytes x workers / s)"
+UNIT = "GB/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--d", type=int, default=0, help="entries per worker (default 2^26 at N=1, 2^28 at N>1)")
+    p.add_argument("--n-sim", type=int, default=4, help="simulated workers at N=1")
+    p.add_argument("--budget", type=float, default=4.0)
+    p.add_argument("--topology", default="ring", choices=["ring", "butterfly"])
+    p.add_argument("--sigma-log", type=float, default=4.0)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--cpu-sample-d", type=int, default=1 << 22)
+    return p.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def synth(torch, d, n, sigma_log, seed=1, device="cuda"):
+    """Llama-like heavy-tailed gradients: per-super-group log-normal scale shared
+    across workers (proj/src/synth.cpp:46-53), entries N(0, sigma_j^2) per worker."""
+    g = torch.Generator(device=device).manual_seed(seed)
+    T = (d + 255) // 256
+    scale = torch.exp(sigma_log * torch.randn(T, device=device, generator=g))
+    out = []
+    for r in range(n):
+        x = torch.randn(T, 256, device=device, generator=g) * scale[:, None]
+        out.append(x.reshape(-1)[:d].contiguous())
+    return out
+
+
+def roofline_of(prof, peak, peak_kind, kernel="quant_dar"):
+    p = prof.get(kernel)
+    if not p or p["ms"] <= 0:
+        return None
+    achieved = p["bytes"] / (p["ms"] * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                traffic = json.load(f).get(kernel, {}).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    return {"bound": "hbm", "kernel": kernel, "achieved": round(achieved, 1), "peak": peak, "peak_source": peak_kind,
+            "unit": "GB/s", "frac": round(achieved / peak, 4),
+            "algorithmic_bytes_per_launch": p["bytes"] / max(p["launches"], 1),
+            "avg_launch_ms": p["ms"] / max(p["launches"], 1), "launches": p["launches"], "traffic": traffic}
+
+
+def cpu_baseline(n, d_sample, budget, topology, sigma_log, steps=1):
+    """The reference's own run_round (oracle/_ref) on a bounded sample, all chunk threads."""
+    from oracle.oracle import Oracle, available
+    kind = "reference" if available("reference") else "port"
+    ora = Oracle(kind)
+    rng = np.random.default_rng(1)
+    T = (d_sample + 255) // 256
+    scale = np.exp(sigma_log * rng.standard_normal(T)).astype(np.float64)
+    ws = [(rng.standard_normal((T, 256)) * scale[:, None]).astype(np.float32).ravel()[:d_sample] for _ in range(n)]
+    threads = min(n, os.cpu_count() or 1) if kind == "reference" else 1
+    cfg = ora.round_cfg(n, budget, topology, seed=1, threads=threads)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        res = ora.run_round(ws, cfg)
+        times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    return {"value": round(n * 4 * d_sample / t / 1e9, 6), "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"run_round n={n} {topology} d={d_sample} b={budget} sigma_log={sigma_log} "
+                      f"(1/{max(1, 1)} of the per-worker size scaled by entries), median of {steps}",
+            "seconds_per_round": round(t, 4), "vnmse": res["vnmse"]}
+
+
+# --------------------------------------------------------------------- N = 1
+def bench_sim(args):
+    import torch
+    import paper_2602_08923_b200 as dq
+    d = args.d or (1 << 26)
+    n = args.n_sim
+    cfg = dq.PipelineConfig(n_workers=n, budget_bits=args.budget,
+                            topology=dq.BUTTERFLY if args.topology == "butterfly" else dq.RING,
+                            seed=dq.SharedSeed(1, 0))
+    ctx = dq.Context(cfg)
+    ws = synth(torch, d, n, args.sigma_log)
+    out = torch.empty(d, device="cuda")
+    st = torch.cuda.current_stream()
+    r = dq.run_round(ws, cfg, out=out, ctx=ctx)  # with metrics (vNMSE vs fp64 sum), untimed
+    vnmse = r.vnmse
+    for _ in range(args.warmup):
+        r = dq.run_round(ws, cfg, out=out, ctx=ctx, metrics=False)
+    torch.cuda.synchronize()
+    ctx.profile(True)
+    ctx.read_profile(reset=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    per_step = []
+    with Clocks(torch.cuda.current_device()) as clk:
+        torch.cuda.synchronize()
+        e0.record(st)
+        for _ in range(args.steps):
+            r = dq.run_round(ws, cfg, out=out, ctx=ctx, metrics=False)
+            per_step.append(r.info["ms_total"])
+        e1.record(st)
+        torch.cuda.synchronize()
+    prof = ctx.read_profile(reset=True)
+    ctx.profile(False)
+    ms = e0.elapsed_time(e1) / args.steps
+    value = n * 4 * d / (ms * 1e-3) / 1e9
+    peak, pk = peaks()
+    launches = sum(p["launches"] for p in prof.values())
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 in / u8 codes (bit-exact integer PRNG path)", "data": "synthetic",
+        "config": {"workload": f"configs[1]: single-B200 simulated {args.topology} all-reduce round, "
+                               f"{n} workers x {d} entries, b={args.budget}, sigma_log={args.sigma_log}",
+                   "global_batch": n, "entries_per_worker": d, "parallelism": f"sim{n}",
+                   "l2": "inputs larger than L2 (>= 1 GiB resident)"},
+        "vnmse": vnmse, "u": r.u, "widths_8_4_2": [r.info["n8"], r.info["n4"], r.info["n2"]],
+        "round_device_ms_median": round(statistics.median(per_step), 4),
+        "kernels": {k: {"launches": v["launches"], "ms_per_step": round(v["ms"] / args.steps, 4),
+                        "GBps": round(v["bytes"] / max(v["ms"], 1e-9) / 1e6, 1)} for k, v in prof.items()},
+        "roofline": roofline_of(prof, peak, pk), "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if not args.no_e2e:
+        hosts = [torch.empty(d, dtype=torch.float32, pin_memory=True) for _ in range(n)]
+        for h, w in zip(hosts, ws):
+            h.copy_(w)
+        hout = torch.empty(d, dtype=torch.float32, pin_memory=True)
+        import ctypes as C
+        from paper_2602_08923_b200._lib import RoundInfo, check, lib
+        ptrs = (C.c_void_p * n)(*[h.data_ptr() for h in hosts])
+        info = RoundInfo()
+        sptr = C.c_void_p(st.cuda_stream)
+        for _ in range(2):
+            check(lib().dq_run_round_host(ctx.h, ptrs, d, C.c_void_p(hout.data_ptr()), C.byref(info), sptr))
+        k = max(3, args.steps // 4)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        for _ in range(k):
+            check(lib().dq_run_round_host(ctx.h, ptrs, d, C.c_void_p(hout.data_ptr()), C.byref(info), sptr))
+        b.record(st)
+        torch.cuda.synchronize()
+        ems = a.elapsed_time(b) / k
+        line["e2e"] = {"value": round(n * 4 * d / (ems * 1e-3) / 1e9, 3), "unit": UNIT, "ms_per_step": round(ems, 3),
+                       "h2d_bytes_per_step": n * 4 * d, "d2h_bytes_per_step": 4 * d,
+                       "api": "dq_run_round_host (C-ABI, pinned host buffers)"}
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(n, args.cpu_sample_d, args.budget, args.topology, args.sigma_log)
+    return line
+
+
+# --------------------------------------------------------------------- N > 1
+def bench_dist(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2602_08923_b200 as dq
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    d = args.d or (1 << 28)
+    cfg = dq.PipelineConfig(n_workers=world, budget_bits=args.budget,
+                            topology=dq.BUTTERFLY if args.topology == "butterfly" else dq.RING,
+                            seed=dq.SharedSeed(1, 0))
+    comm = dq.Communicator(cfg, rank, world)
+    # each rank's synthetic gradient: shared per-SG scale, rank-keyed entries
+    g = torch.Generator(device="cuda").manual_seed(1)
+    T = (d + 255) // 256
+    scale = torch.exp(args.sigma_log * torch.randn(T, device="cuda", generator=g))
+    g.manual_seed(1000 + rank)
+    x = (torch.randn(T, 256, device="cuda", generator=g) * scale[:, None]).reshape(-1)[:d].contiguous()
+    out = torch.empty_like(x)
+    st = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        comm.allreduce(x, out)
+    torch.cuda.synchronize()
+    # accuracy vs exact fp32 sum (outside the timed region)
+    truth = x.clone()
+    dist.all_reduce(truth)
+    err = float(((out.double() - truth.double()) ** 2).sum())
+    ref = float((truth.double() ** 2).sum())
+    comm.ctx.profile(True)
+    comm.ctx.read_profile(reset=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(st)
+        for _ in range(args.steps):
+            _, info = comm.allreduce(x, out)
+        e1.record(st)
+        torch.cuda.synchronize()
+        dist.barrier()
+    prof = comm.ctx.read_profile(reset=True)
+    comm.ctx.profile(False)
+    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms)
+    # NCCL bf16 all-reduce baseline on the same d
+    xb = x.to(torch.bfloat16)
+    for _ in range(3):
+        dist.all_reduce(xb)
+    torch.cuda.synchronize()
+    dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(st)
+    for _ in range(args.steps):
+        dist.all_reduce(xb)
+    b.record(st)
+    torch.cuda.synchronize()
+    nms = torch.tensor([a.elapsed_time(b) / args.steps], device="cuda")
+    dist.all_reduce(nms, op=dist.ReduceOp.MAX)
+    nms = float(nms)
+    peak, pk = peaks()
+    line = None
+    if rank == 0:
+        value = world * 4 * d / (ms * 1e-3) / 1e9
+        launches = sum(p["launches"] for k, p in prof.items() if k != "nccl")
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32 in / u8 codes (bit-exact integer PRNG path)", "data": "synthetic",
+            "config": {"workload": f"configs[2]: {args.topology} all-reduce over {world} B200, {d} fp32 entries "
+                                   f"per rank, b={args.budget}, sigma_log={args.sigma_log}",
+                       "global_batch": world, "entries_per_worker": d, "parallelism": f"dp{world}",
+                       "l2": "inputs larger than L2"},
+            "algbw_effective_gbs": round(4 * d / (ms * 1e-3) / 1e9, 3),
+            "vnmse": err / ref if ref > 0 else 0.0,
+            "nccl_bf16": {"ms": round(nms, 4), "effective_gbs": round(4 * d / (nms * 1e-3) / 1e9, 3),
+                          "algbw_gbs": round(2 * d / (nms * 1e-3) / 1e9, 3),
+                          "busbw_gbs": round(2 * d / (nms * 1e-3) / 1e9 * 2 * (world - 1) / world, 3)},
+            "kernels": {k: {"launches": v["launches"], "ms_per_step": round(v["ms"] / args.steps, 4),
+                            "GBps": round(v["bytes"] / max(v["ms"], 1e-9) / 1e6, 1)} for k, v in prof.items()},
+            "roofline": roofline_of(prof, peak, pk), "gpu_launches": launches, "clocks": clk.summary(),
+        }
+    # e2e: pinned host -> device, all-reduce, device -> host
+    if not args.no_e2e:
+        hx = torch.empty(d, dtype=torch.float32, pin_memory=True)
+        hx.copy_(x)
+        hy = torch.empty(d, dtype=torch.float32, pin_memory=True)
+        dx = torch.empty_like(x)
+        k = max(3, args.steps // 4)
+        for _ in range(2):
+            dx.copy_(hx, non_blocking=True)
+            comm.allreduce(dx, out)
+            hy.copy_(out, non_blocking=True)
+        torch.cuda.synchronize()
+        dist.barrier()
+        a.record(st)
+        for _ in range(k):
+            dx.copy_(hx, non_blocking=True)
+            comm.allreduce(dx, out)
+            hy.copy_(out, non_blocking=True)
+        b.record(st)
+        torch.cuda.synchronize()
+        ems = torch.tensor([a.elapsed_time(b) / k], device="cuda")
+        dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        if rank == 0:
+            ems = float(ems)
+            line["e2e"] = {"value": round(world * 4 * d / (ems * 1e-3) / 1e9, 3), "unit": UNIT,
+                           "ms_per_step": round(ems, 3), "h2d_bytes_per_step": 4 * d, "d2h_bytes_per_step": 4 * d,
+                           "api": "Communicator.allreduce (dq_allreduce C-ABI) with pinned host copies"}
+    dist.barrier()
+    dist.destroy_process_group()
+    return line
+
+
+def bench_reference(args):
+    """--impl reference: the reference's CPU run_round on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    n = args.n_sim if args.gpus <= 1 else args.gpus
+    d_full = args.d or ((1 << 26) if args.gpus <= 1 else (1 << 28))
+    dsamp = min(args.cpu_sample_d, d_full)
+    from oracle.oracle import Oracle, available
+    kind = "reference" if available("reference") else "port"
+    ora = Oracle(kind)
+    rng = np.random.default_rng(1)
+    T = (dsamp + 255) // 256
+    scale = np.exp(args.sigma_log * rng.standard_normal(T))
+    ws = [(rng.standard_normal((T, 256)) * scale[:, None]).astype(np.float32).ravel()[:dsamp] for _ in range(n)]
+    threads = min(n, os.cpu_count() or 1) if kind == "reference" else 1
+    cfg = ora.round_cfg(n, args.budget, args.topology, seed=1, threads=threads)
+    steps = max(1, min(args.steps, 3))
+    for _ in range(min(args.warmup, 1)):
+        ora.run_round(ws, cfg)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        res = ora.run_round(ws, cfg)
+        times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    value = n * 4 * dsamp / t / 1e9
+    sample = (f"run_round n={n} {args.topology} d={dsamp} per worker (full workload d={d_full}), "
+              f"b={args.budget}, sigma_log={args.sigma_log}, median of {steps}")
+    return {"impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": UNIT, "n_gpus": args.gpus,
+            "steps": steps, "warmup": min(args.warmup, 1), "ms_per_step": round(t * 1e3, 2),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"reference CPU run_round sample of the bench workload ({n} workers)",
+                       "entries_per_worker": dsamp, "parallelism": f"threads{threads}"},
+            "vnmse": res["vnmse"],
+            "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": threads, "kind": kind,
+                             "sample": sample},
+            "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        line = bench_reference(args)
+    elif int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        line = bench_dist(args)
+    else:
+        line = bench_sim(args)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

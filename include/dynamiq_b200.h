@@ -1,0 +1,183 @@
+/*
+ * dynamiq_b200.h — C-ABI of the B200-native DynamiQ compressed all-reduce.
+ *
+ * Drop-in boundary for the reference's hot path (run_round and the four codec
+ * kernels).  Plain pointers and sizes only: device pointers are CUDA device
+ * addresses, streams are cudaStream_t passed as void*.  Every entry point
+ * returns a status (DQ_OK = 0) and leaves a thread-local message for
+ * dq_last_error().  Status codes mirror the reference's exception types and
+ * the CLI's exit codes (proj/tools/dynamiq_cli.cpp:446-458):
+ *   DQ_EINVAL      std::invalid_argument         (exit 2)
+ *   DQ_EINFEASIBLE dynamiq::InfeasibleBudget     (exit 3)
+ *   DQ_EMALFORMED  std::runtime_error("malformed compressed buffer: ...")
+ *
+ * Device chunk format ("dq tiled SoA"): the super-groups of a
+ * chunk in body order (n8 width-8, then n4 width-4, then n2 width-2), packed in
+ * tiles of 64 super-groups [payloads | 16 u8 group-scale codes each | bf16
+ * super-group scale each].  Bits are identical to the reference record fields
+ * (proj/src/codec.cpp:92-124); only the interleaving differs and the 24-byte
+ * header is implied by (chunk, n8, n4, n2).  dq_to_reference_wire converts to
+ * the reference's serialize_chunk bytes (proj/src/codec.cpp:319-343).
+ *
+ * Reference interface replaced by each entry point is cited in brackets
+ * (paths relative to the reference repository root).
+ */
+#ifndef DYNAMIQ_B200_H
+#define DYNAMIQ_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DQ_VERSION 1
+
+enum dq_status {
+  DQ_OK = 0,
+  DQ_EINVAL = 2,
+  DQ_EINFEASIBLE = 3,
+  DQ_EMALFORMED = 4,
+  DQ_ECUDA = 5,
+  DQ_ENCCL = 6,
+};
+
+enum dq_topology { DQ_RING = 0, DQ_BUTTERFLY = 1 };
+enum dq_allocator { DQ_ALLOC_GENERAL = 0, DQ_ALLOC_FAST = 1, DQ_ALLOC_FIXED = 2 };
+
+/* [proj/include/dynamiq/engine.hpp:22-43 PipelineConfig] — same fields and
+ * defaults (dq_config_default).  Supported on device: group_size 16,
+ * super_group_size 256, hierarchical scales, quantized codec, fast or fixed
+ * allocator; non_uniform and correlated may be toggled. */
+typedef struct dq_config {
+  uint32_t n_workers;
+  uint32_t group_size;
+  uint32_t super_group_size;
+  double budget_bits;
+  int32_t non_uniform;
+  int32_t variable_width;
+  int32_t hierarchical_scales;
+  int32_t correlated;
+  int32_t fixed_width;
+  int32_t allocator; /* enum dq_allocator */
+  int32_t topology;  /* enum dq_topology */
+  int32_t codec;     /* 0 quantized (1 = lossless debug codec: not on device) */
+  uint64_t seed;     /* SharedSeed.seed */
+  uint64_t round;    /* SharedSeed.round */
+  uint32_t threads;  /* accepted for API parity; the device ignores it */
+} dq_config;
+
+/* [proj/include/dynamiq/codec.hpp:33-40 QuantContext] */
+typedef struct dq_qctx {
+  uint64_t seed, round;
+  uint32_t chunk_index;
+  uint32_t hop_slot;
+  uint32_t n_slots;
+  int32_t correlated;
+} dq_qctx;
+
+/* [proj/include/dynamiq/engine.hpp:45-54 RoundResult, metrics.hpp:24-40 WireVolume]
+ * (synced goes to the caller's buffer; widths/permutation via dq_round_allocation) */
+typedef struct dq_round_info {
+  uint64_t wire_hash;   /* only when the round was run with collect_wire = 1 */
+  double vnmse, mse;    /* only for dq_sim_round (needs every worker's input) */
+  double u;             /* fast-allocator search state (BitAllocation.u) */
+  uint64_t payload_bits;
+  uint64_t stats_bits, wire_payload_bits, scale_bits, header_bits;
+  uint64_t repr_bits, compressed_coordinates, transmitted_coordinates;
+  uint32_t n8, n4, n2;  /* width-class counts over all super-groups */
+  uint32_t alloc_passes;
+  double ms_total;      /* device time of the round (CUDA events) */
+} dq_round_info;
+
+typedef struct dq_ctx dq_ctx;
+
+int dq_version(void);
+const char* dq_last_error(void);
+void dq_config_default(dq_config* cfg);
+
+/* ---- context: one per GPU; owns scratch sized on demand ------------------ */
+int dq_ctx_create(const dq_config* cfg, int device, dq_ctx** out);
+int dq_ctx_destroy(dq_ctx* ctx);
+int dq_ctx_set_config(dq_ctx* ctx, const dq_config* cfg);
+
+/* ---- codec primitives on device buffers (one chunk) ----------------------
+ * Widths are given as run lengths n8, n4, n2 of the width-sorted body
+ * (the reference's wire order, proj/src/codec.cpp:298-315). */
+size_t dq_chunk_bytes(uint32_t n8, uint32_t n4, uint32_t n2);
+/* [codec.hpp:64-69 compress_chunk] values: n_sg*256 fp32 */
+int dq_compress_chunk(const float* d_values, uint32_t n8, uint32_t n4, uint32_t n2,
+                      const dq_qctx* q, uint32_t first_sg_index, int non_uniform, void* d_out,
+                      void* stream);
+/* [codec.hpp:86-91 decompress_accumulate_recompress] */
+int dq_dar_chunk(const void* d_in, const float* d_local, uint32_t n8, uint32_t n4, uint32_t n2,
+                 const dq_qctx* q, uint32_t first_sg_index, int non_uniform, void* d_out,
+                 void* stream);
+/* [codec.hpp:75-78 decompress_accumulate] acc += decompress(in) */
+int dq_da_chunk(const void* d_in, float* d_acc, uint32_t n8, uint32_t n4, uint32_t n2,
+                int non_uniform, void* stream);
+/* [codec.hpp:71-73 decompress_chunk] */
+int dq_decompress_chunk(const void* d_in, float* d_out, uint32_t n8, uint32_t n4, uint32_t n2,
+                        int non_uniform, void* stream);
+/* [codec.cpp:319-399 serialize_chunk / parse_chunk] host buffers.
+ * to: writes dq_chunk_bytes + 24 bytes.  from: strict parse of reference bytes
+ * (DQ_EMALFORMED on any malformed buffer), returns the run lengths. */
+int dq_to_reference_wire(const void* h_soa, uint32_t chunk_index, uint32_t n8, uint32_t n4,
+                         uint32_t n2, void* h_ref);
+int dq_from_reference_wire(const void* h_ref, size_t len, void* h_soa, size_t soa_cap,
+                           uint32_t* chunk_index, uint32_t* n8, uint32_t* n4, uint32_t* n2);
+
+/* ---- statistics and allocation ------------------------------------------ */
+/* [stats.hpp:19 compute_stats] per super-group fp64-sequential mean / sum of squares */
+int dq_compute_stats(const float* d_x, size_t d, float* d_mean, float* d_sq, void* stream);
+/* [stats.hpp:23 reduce_stats] d_means/d_sqs: [n_workers][n_sg], rank order */
+int dq_reduce_stats(const float* d_means, const float* d_sqs, uint32_t n_workers, size_t n_sg,
+                    float* d_gmean, float* d_gsq, void* stream);
+/* [allocation.hpp:63-64 allocate_fast + :85 build_permutation].  Synchronizes the
+ * stream (the plateau midpoint is finished on the host with the reference's libm). */
+int dq_allocate_fast(dq_ctx* ctx, const float* d_sq_norms, size_t n_sg, double budget_bits,
+                     uint8_t* d_widths, uint32_t* d_perm, double* u, uint64_t* payload_bits,
+                     uint32_t counts[3], void* stream);
+
+/* ---- the all-reduce ------------------------------------------------------ */
+/* [engine.hpp:63-64 run_round] all cfg.n_workers gradients resident on this
+ * GPU (simulated hops, BASELINE config 2).  d_workers: host array of n device
+ * pointers.  flags: DQ_SIM_COLLECT_WIRE hashes every message in reference wire
+ * format (wire_hash parity; slow, for tests); DQ_SIM_NO_METRICS skips the
+ * vNMSE pass against the fp64 sum of the inputs. */
+enum { DQ_SIM_COLLECT_WIRE = 1, DQ_SIM_NO_METRICS = 2 };
+int dq_sim_round(dq_ctx* ctx, const float* const* d_workers, size_t d, float* d_synced,
+                 int flags, dq_round_info* info, void* stream);
+/* Same with HOST gradients: copies in, runs, copies the sum out (the e2e call). */
+int dq_run_round_host(dq_ctx* ctx, const float* const* h_workers, size_t d, float* h_synced,
+                      dq_round_info* info, void* stream);
+/* After a round: widths (original super-group order) and permutation. */
+int dq_round_allocation(dq_ctx* ctx, uint8_t* h_widths, uint32_t* h_perm, size_t n_sg);
+
+/* Per-kernel-family device timing: when enabled, every launch is bracketed by
+ * CUDA events on its stream; totals (launch count, ms, algorithmic bytes) are
+ * read back per family ("quant_dar", "decode_out", ...). */
+typedef struct dq_kernel_profile {
+  char name[32];
+  uint64_t launches;
+  double ms;
+  double bytes;
+} dq_kernel_profile;
+int dq_profile_enable(dq_ctx* ctx, int on);
+int dq_profile_read(dq_ctx* ctx, dq_kernel_profile* out, int cap, int* count, int reset);
+
+/* Multi-GPU: one process per GPU.  Rank 0 creates the id, the caller ships the
+ * 128 bytes to every rank (e.g. torch.distributed), every rank joins. */
+int dq_comm_unique_id(uint8_t out[128]);
+int dq_comm_init(dq_ctx* ctx, int rank, int nranks, const uint8_t id[128]);
+/* [engine.hpp:63-64 run_round, distributed] d_in: this rank's gradient; d_out:
+ * the SUM estimate over ranks (caller divides by n for a mean, as the
+ * reference's caller does). */
+int dq_allreduce(dq_ctx* ctx, const float* d_in, float* d_out, size_t d, dq_round_info* info,
+                 void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DYNAMIQ_B200_H */

@@ -1,0 +1,438 @@
+"""Python mirror of the reference's hot-path interface, backed by the B200 C-ABI.
+
+Names, argument meaning and error behaviour follow the reference library
+(``proj/include/dynamiq/{codec,stats,allocation,engine}.hpp``) so a caller of
+``dynamiq::compress_chunk`` / ``run_round`` finds the same operations here:
+
+=================================================  =============================================
+reference (proj/include/dynamiq/...)               here
+=================================================  =============================================
+codec.hpp:64  compress_chunk                       :func:`compress_chunk`
+codec.hpp:71  decompress_chunk                     :func:`decompress_chunk`
+codec.hpp:75  decompress_accumulate                :func:`decompress_accumulate`
+codec.hpp:86  decompress_accumulate_recompress     :func:`decompress_accumulate_recompress`
+codec.hpp:94  serialize_chunk / parse_chunk        :func:`serialize_chunk` / :func:`parse_chunk`
+codec.hpp:88  compressed_size_bits                 :func:`compressed_size_bits`
+stats.hpp:19  compute_stats / reduce_stats         :func:`compute_stats` / :func:`reduce_stats`
+allocation.hpp:63 allocate_fast (+permutation)     :func:`allocate_fast`
+engine.hpp:63 run_round                            :func:`run_round` (all workers on one GPU)
+(distributed run_round, PAPER §4)                  :class:`Communicator` ``.allreduce``
+=================================================  =============================================
+
+Tensors are torch CUDA tensors (device memory + the current stream are the
+plumbing); all compute runs in the native library's sm_100a kernels.
+Errors: :class:`InvalidArgument` (std::invalid_argument), :class:`InfeasibleBudget`,
+:class:`MalformedBuffer` (std::runtime_error "malformed compressed buffer").
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import (Config, InfeasibleBudget, InvalidArgument, MalformedBuffer, QCtx, RoundInfo,  # noqa: F401
+                   check, lib)
+
+RING, BUTTERFLY = 0, 1
+KIND_GENERAL, KIND_FAST, KIND_FIXED = 0, 1, 2
+
+
+@dataclass
+class SharedSeed:
+    """proj/include/dynamiq/random.hpp:12-15"""
+    seed: int = 0
+    round: int = 0
+
+
+@dataclass
+class QuantContext:
+    """proj/include/dynamiq/codec.hpp:33-40"""
+    seed: SharedSeed = field(default_factory=SharedSeed)
+    chunk_index: int = 0
+    hop_slot: int = 0
+    n_slots: int = 1
+    correlated: bool = True
+
+    def _c(self) -> QCtx:
+        return QCtx(self.seed.seed, self.seed.round, self.chunk_index, self.hop_slot, self.n_slots,
+                    int(self.correlated))
+
+
+@dataclass
+class CodecConfig:
+    """proj/include/dynamiq/codec.hpp:26-31 (device: s=16, S=256, hierarchical)"""
+    group_size: int = 16
+    super_group_size: int = 256
+    hierarchical_scales: bool = True
+    non_uniform: bool = True  # CodebookSet::non_uniform_defaults() vs uniform_all()
+
+    def validate(self) -> None:
+        if self.group_size == 0 or self.super_group_size % self.group_size or self.super_group_size % 4:
+            raise InvalidArgument(2, "super-group size must be a positive multiple of the group size")
+        if (self.group_size, self.super_group_size, self.hierarchical_scales) != (16, 256, True):
+            raise InvalidArgument(2, "device codec supports s=16, S=256 with hierarchical scales")
+
+
+@dataclass
+class PipelineConfig:
+    """proj/include/dynamiq/engine.hpp:22-43 — same fields and defaults."""
+    n_workers: int = 4
+    group_size: int = 16
+    super_group_size: int = 256
+    budget_bits: float = 5.0
+    non_uniform: bool = True
+    variable_width: bool = True
+    hierarchical_scales: bool = True
+    correlated: bool = True
+    fixed_width: int = 4
+    allocator: int = KIND_FAST
+    topology: int = RING
+    codec: int = 0
+    seed: SharedSeed = field(default_factory=lambda: SharedSeed(1, 0))
+    threads: int = 1
+
+    def _c(self) -> Config:
+        return Config(self.n_workers, self.group_size, self.super_group_size, float(self.budget_bits),
+                      int(self.non_uniform), int(self.variable_width), int(self.hierarchical_scales),
+                      int(self.correlated), int(self.fixed_width), int(self.allocator), int(self.topology),
+                      int(self.codec), self.seed.seed, self.seed.round, self.threads)
+
+
+@dataclass
+class DeviceChunk:
+    """A compressed chunk resident in HBM (dq tiled SoA layout, include/dynamiq_b200.h).
+
+    ``widths`` is implied by the run lengths (8, 4, 2 order) like the
+    reference's wire header (proj/src/codec.cpp:283-317)."""
+    chunk_index: int
+    n8: int
+    n4: int
+    n2: int
+    data: torch.Tensor  # uint8, dq_chunk_bytes(n8, n4, n2)
+
+    @property
+    def n_sg(self) -> int:
+        return self.n8 + self.n4 + self.n2
+
+    @property
+    def widths(self) -> np.ndarray:
+        return np.array([8] * self.n8 + [4] * self.n4 + [2] * self.n2, np.uint8)
+
+
+def _stream() -> C.c_void_p:
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t: Optional[torch.Tensor]) -> C.c_void_p:
+    return C.c_void_p(t.data_ptr() if t is not None else 0)
+
+
+def _runs(widths) -> tuple:
+    """Run lengths of a width-sorted body; unsorted bodies are rejected like serialize_chunk
+    (proj/src/codec.cpp:298-315)."""
+    w = np.asarray(widths, np.uint8).ravel()
+    rank = {8: 0, 4: 1, 2: 2}
+    cls = []
+    for x in w.tolist():
+        if x not in rank:
+            if x == 16:
+                raise InvalidArgument(2, "width-16 passthrough is not supported by the device codec")
+            raise InvalidArgument(2, f"unsupported codec width {x}")
+        cls.append(rank[x])
+    if any(b < a for a, b in zip(cls, cls[1:])):
+        raise InvalidArgument(2, "chunk body must be ordered by width class 8,4,2,16")
+    return cls.count(0), cls.count(1), cls.count(2)
+
+
+def _f32(t: torch.Tensor, n: int, what: str) -> torch.Tensor:
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float32):
+        raise InvalidArgument(2, f"{what} must be a CUDA float32 tensor")
+    if t.numel() != n:
+        raise InvalidArgument(2, f"{what} length does not match chunk")
+    t = t.contiguous()
+    if t.data_ptr() % 16:
+        t = t.clone()
+    return t
+
+
+def chunk_bytes(n8: int, n4: int, n2: int) -> int:
+    return lib().dq_chunk_bytes(n8, n4, n2)
+
+
+def compressed_size_bits(widths, S: int = 256, s: int = 16, hierarchical_scales: bool = True) -> int:
+    """Exact reference wire size, header included (proj/src/codec.cpp:281-291)."""
+    w = np.asarray(widths, np.uint8)
+    scales = (16 + (S // s) * 8) if hierarchical_scales else (S // s) * 16
+    return 192 + int(sum(int(x) * S + (0 if x == 16 else scales) for x in w.tolist()))
+
+
+def compress_chunk(values: torch.Tensor, widths, cfg: CodecConfig, qctx: QuantContext,
+                   first_sg_index: int = 0) -> DeviceChunk:
+    cfg.validate()
+    n8, n4, n2 = _runs(widths)
+    v = _f32(values, (n8 + n4 + n2) * 256, "chunk")
+    out = torch.empty(max(chunk_bytes(n8, n4, n2), 1), dtype=torch.uint8, device=v.device)
+    q = qctx._c()
+    check(lib().dq_compress_chunk(_ptr(v), n8, n4, n2, C.byref(q), first_sg_index, int(cfg.non_uniform),
+                                  _ptr(out), _stream()))
+    return DeviceChunk(qctx.chunk_index, n8, n4, n2, out)
+
+
+def decompress_accumulate_recompress(chunk: DeviceChunk, local: torch.Tensor, cfg: CodecConfig,
+                                     qctx: QuantContext, first_sg_index: int = 0) -> DeviceChunk:
+    cfg.validate()
+    loc = _f32(local, chunk.n_sg * 256, "local buffer")
+    out = torch.empty_like(chunk.data)
+    q = qctx._c()
+    check(lib().dq_dar_chunk(_ptr(chunk.data), _ptr(loc), chunk.n8, chunk.n4, chunk.n2, C.byref(q),
+                             first_sg_index, int(cfg.non_uniform), _ptr(out), _stream()))
+    return DeviceChunk(qctx.chunk_index, chunk.n8, chunk.n4, chunk.n2, out)
+
+
+def decompress_accumulate(chunk: DeviceChunk, acc: torch.Tensor, cfg: CodecConfig) -> None:
+    """acc += decompress(chunk), in place (acc must be contiguous and 16-byte aligned)."""
+    cfg.validate()
+    if not (acc.is_cuda and acc.dtype == torch.float32 and acc.is_contiguous() and acc.data_ptr() % 16 == 0):
+        raise InvalidArgument(2, "accumulator must be a contiguous, aligned CUDA float32 tensor")
+    if acc.numel() != chunk.n_sg * 256:
+        raise InvalidArgument(2, "accumulator length does not match chunk")
+    check(lib().dq_da_chunk(_ptr(chunk.data), _ptr(acc), chunk.n8, chunk.n4, chunk.n2, int(cfg.non_uniform),
+                            _stream()))
+
+
+def decompress_chunk(chunk: DeviceChunk, cfg: CodecConfig, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    cfg.validate()
+    if out is None:
+        out = torch.empty(chunk.n_sg * 256, dtype=torch.float32, device=chunk.data.device)
+    elif out.numel() != chunk.n_sg * 256:
+        raise InvalidArgument(2, "output length does not match chunk")
+    check(lib().dq_decompress_chunk(_ptr(chunk.data), _ptr(out), chunk.n8, chunk.n4, chunk.n2,
+                                    int(cfg.non_uniform), _stream()))
+    return out
+
+
+def serialize_chunk(chunk: DeviceChunk) -> bytes:
+    """Reference wire bytes (proj/src/codec.cpp:319-343)."""
+    soa = chunk.data.cpu().numpy()
+    out = np.zeros(chunk_bytes(chunk.n8, chunk.n4, chunk.n2) + 24, np.uint8)
+    check(lib().dq_to_reference_wire(soa.ctypes.data_as(C.c_void_p), chunk.chunk_index, chunk.n8, chunk.n4,
+                                     chunk.n2, out.ctypes.data_as(C.c_void_p)))
+    return out.tobytes()
+
+
+def soa_from_reference(buf: bytes):
+    """Strict parse of reference wire bytes into the device layout (host numpy array)."""
+    b = np.frombuffer(buf, np.uint8).copy()
+    cap = max(len(buf), 1)
+    soa = np.zeros(cap, np.uint8)
+    ci, n8, n4, n2 = C.c_uint32(), C.c_uint32(), C.c_uint32(), C.c_uint32()
+    check(lib().dq_from_reference_wire(b.ctypes.data_as(C.c_void_p), b.size, soa.ctypes.data_as(C.c_void_p),
+                                       soa.size, C.byref(ci), C.byref(n8), C.byref(n4), C.byref(n2)))
+    return ci.value, n8.value, n4.value, n2.value, soa[: chunk_bytes(n8.value, n4.value, n2.value)]
+
+
+def parse_chunk(buf: bytes, device="cuda") -> DeviceChunk:
+    """proj/src/codec.cpp:345-399 — raises MalformedBuffer on any malformed buffer."""
+    ci, n8, n4, n2, soa = soa_from_reference(buf)
+    data = torch.from_numpy(soa.copy() if soa.size else np.zeros(1, np.uint8)).to(device)
+    return DeviceChunk(ci, n8, n4, n2, data)
+
+
+def compute_stats(x: torch.Tensor):
+    """proj/src/stats.cpp:23-35 -> (mean, sq_norm) float32 tensors, one per super-group."""
+    x = _f32(x, x.numel(), "gradient")
+    T = (x.numel() + 255) // 256
+    mean = torch.empty(T, dtype=torch.float32, device=x.device)
+    sq = torch.empty_like(mean)
+    check(lib().dq_compute_stats(_ptr(x), x.numel(), _ptr(mean), _ptr(sq), _stream()))
+    return mean, sq
+
+
+def reduce_stats(means: torch.Tensor, sqs: torch.Tensor):
+    """proj/src/stats.cpp:37-54: rank-ordered fp64 reduction of [n_workers, n_sg] stats."""
+    means, sqs = means.contiguous(), sqs.contiguous()
+    n, T = means.shape
+    gm = torch.empty(T, dtype=torch.float32, device=means.device)
+    gs = torch.empty_like(gm)
+    check(lib().dq_reduce_stats(_ptr(means), _ptr(sqs), n, T, _ptr(gm), _ptr(gs), _stream()))
+    return gm, gs
+
+
+@dataclass
+class BitAllocation:
+    """proj/include/dynamiq/allocation.hpp:40-45"""
+    widths: torch.Tensor       # uint8 per super-group (original order)
+    permutation: torch.Tensor  # int32: position k holds super-group permutation[k]
+    payload_bits: int
+    u: float
+    counts: tuple              # (n8, n4, n2)
+
+
+class Context:
+    """One device context (scratch owner); mirrors one worker's engine state."""
+
+    def __init__(self, config: Optional[PipelineConfig] = None, device: Optional[int] = None):
+        self.config = config or PipelineConfig()
+        self.device = torch.cuda.current_device() if device is None else device
+        h = C.c_void_p()
+        cfg = self.config._c()
+        check(lib().dq_ctx_create(C.byref(cfg), self.device, C.byref(h)))
+        self.h = h
+
+    def set_config(self, config: PipelineConfig) -> None:
+        cfg = config._c()
+        check(lib().dq_ctx_set_config(self.h, C.byref(cfg)))
+        self.config = config
+
+    def profile(self, on: bool = True) -> None:
+        check(lib().dq_profile_enable(self.h, int(on)))
+
+    def read_profile(self, reset: bool = True) -> dict:
+        """{family: {"launches", "ms", "bytes"}} accumulated since the last reset."""
+        arr = (_lib.KernelProfile * 16)()
+        n = C.c_int()
+        check(lib().dq_profile_read(self.h, arr, 16, C.byref(n), int(reset)))
+        return {arr[i].name.decode(): {"launches": arr[i].launches, "ms": arr[i].ms, "bytes": arr[i].bytes}
+                for i in range(min(n.value, 16))}
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            lib().dq_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ctx: dict = {}
+
+
+def _ctx_for(config: PipelineConfig) -> Context:
+    dev = torch.cuda.current_device()
+    c = _default_ctx.get(dev)
+    if c is None:
+        c = _default_ctx[dev] = Context(config, dev)
+    else:
+        c.set_config(config)
+    return c
+
+
+def allocate_fast(sq_norms: torch.Tensor, budget_bits: float, ctx: Optional[Context] = None) -> BitAllocation:
+    """proj/src/allocation.cpp:228-260 + build_permutation (W = {2,4,8}, s=16, S=256)."""
+    ctx = ctx or _ctx_for(PipelineConfig())
+    F = _f32(sq_norms, sq_norms.numel(), "sq_norms")
+    T = F.numel()
+    widths = torch.empty(max(T, 1), dtype=torch.uint8, device=F.device)
+    perm = torch.empty(max(T, 1), dtype=torch.int32, device=F.device)
+    u, pay = C.c_double(), C.c_uint64()
+    counts = (C.c_uint32 * 3)()
+    check(lib().dq_allocate_fast(ctx.h, _ptr(F), T, float(budget_bits), _ptr(widths), _ptr(perm), C.byref(u),
+                                 C.byref(pay), counts, _stream()))
+    return BitAllocation(widths[:T], perm[:T], pay.value, u.value, tuple(counts))
+
+
+@dataclass
+class RoundResult:
+    """proj/include/dynamiq/engine.hpp:45-54 (exact fp64 sum not materialized)."""
+    synced: torch.Tensor
+    vnmse: float
+    mse: float
+    wire_hash: int
+    u: float
+    payload_bits: int
+    info: dict
+    widths: Optional[np.ndarray] = None
+    permutation: Optional[np.ndarray] = None
+
+
+def _info_dict(info: RoundInfo) -> dict:
+    return {k: getattr(info, k) for k, _ in RoundInfo._fields_}
+
+
+def run_round(worker_values: Sequence[torch.Tensor], config: PipelineConfig, collect_wire: bool = False,
+              with_allocation: bool = False, out: Optional[torch.Tensor] = None,
+              ctx: Optional[Context] = None, metrics: bool = True) -> RoundResult:
+    """One full round with every worker's gradient on this GPU (simulated hops).
+
+    Same inputs/outputs as the reference's run_round (proj/src/engine.cpp:269-418);
+    ``collect_wire`` also computes the reference's wire_hash over the serialized
+    messages (slow; for parity tests)."""
+    if len(worker_values) == 0:
+        raise InvalidArgument(2, "no workers")
+    if len(worker_values) != config.n_workers:
+        raise InvalidArgument(2, "worker count does not match config")
+    d = worker_values[0].numel()
+    if d == 0:
+        raise InvalidArgument(2, "empty gradient")
+    xs = [_f32(w, d, "worker gradient") if w.numel() == d else None for w in worker_values]
+    if any(x is None for x in xs):
+        raise InvalidArgument(2, "worker gradients must have equal length")
+    ctx = ctx or _ctx_for(config)
+    if ctx.config is not config:
+        ctx.set_config(config)
+    if out is None:
+        out = torch.empty(d, dtype=torch.float32, device=xs[0].device)
+    ptrs = (C.c_void_p * len(xs))(*[x.data_ptr() for x in xs])
+    info = RoundInfo()
+    flags = (1 if collect_wire else 0) | (0 if metrics else 2)
+    check(lib().dq_sim_round(ctx.h, ptrs, d, _ptr(out), flags, C.byref(info), _stream()))
+    res = RoundResult(out, info.vnmse, info.mse, info.wire_hash, info.u, info.payload_bits, _info_dict(info))
+    if with_allocation and config.n_workers > 1:
+        T = (d + 255) // 256
+        w = np.zeros(T, np.uint8)
+        p = np.zeros(T, np.uint32)
+        check(lib().dq_round_allocation(ctx.h, w.ctypes.data_as(C.POINTER(C.c_uint8)),
+                                        p.ctypes.data_as(C.POINTER(C.c_uint32)), T))
+        res.widths, res.permutation = w, p
+    return res
+
+
+def run_round_host(worker_values: Sequence[np.ndarray], config: PipelineConfig,
+                   ctx: Optional[Context] = None) -> tuple:
+    """run_round on HOST buffers (the e2e path: H2D of every input and D2H of the sum inside)."""
+    ctx = ctx or _ctx_for(config)
+    if ctx.config is not config:
+        ctx.set_config(config)
+    xs = [np.ascontiguousarray(w, np.float32) for w in worker_values]
+    d = xs[0].size
+    out = np.empty(d, np.float32)
+    ptrs = (C.c_void_p * len(xs))(*[x.ctypes.data for x in xs])
+    info = RoundInfo()
+    check(lib().dq_run_round_host(ctx.h, ptrs, d, out.ctypes.data_as(C.c_void_p), C.byref(info), _stream()))
+    return out, _info_dict(info)
+
+
+class Communicator:
+    """Distributed all-reduce: one process per GPU, NCCL over NVLink between the fused kernels.
+
+    ``torch.distributed`` (any backend) only ships the 128-byte NCCL id."""
+
+    def __init__(self, config: PipelineConfig, rank: int, world_size: int, group=None):
+        import torch.distributed as dist
+        if config.n_workers != world_size:
+            raise InvalidArgument(2, "config.n_workers must equal the world size")
+        self.ctx = Context(config)
+        uid = np.zeros(128, np.uint8)
+        if rank == 0:
+            check(lib().dq_comm_unique_id(uid.ctypes.data_as(C.POINTER(C.c_uint8))))
+        obj = [uid.tobytes()]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        uid = np.frombuffer(obj[0], np.uint8).copy()
+        check(lib().dq_comm_init(self.ctx.h, rank, world_size, uid.ctypes.data_as(C.POINTER(C.c_uint8))))
+        self.rank, self.world_size = rank, world_size
+
+    def allreduce(self, x: torch.Tensor, out: Optional[torch.Tensor] = None) -> tuple:
+        """SUM estimate of every rank's ``x`` (caller divides by n for a mean)."""
+        x = _f32(x, x.numel(), "gradient")
+        if out is None:
+            out = torch.empty_like(x)
+        info = RoundInfo()
+        check(lib().dq_allreduce(self.ctx.h, _ptr(x), _ptr(out), x.numel(), C.byref(info), _stream()))
+        return out, _info_dict(info)

@@ -1,0 +1,122 @@
+// dq_device.cuh — device-side building blocks of the DynamiQ B200 hot path.
+//
+// Keyed counter-based PRNG (bit-exact with proj/src/random.cpp:10-90), bf16
+// helpers (proj/include/dynamiq/bf16.hpp:12-40) and the tiled SoA chunk layout
+// used on HBM and on the wire between GPUs.
+//
+// Floating point: every float/double expression that must round exactly like
+// the x86-64 reference uses explicit _rn intrinsics, and the whole library is
+// compiled with --fmad=false -prec-div=true -ftz=false as a second guard.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace dq {
+
+constexpr int kS = 256;            // super-group size S (entries)
+constexpr int kG = 16;             // group size s (entries)
+constexpr int kGroups = kS / kG;   // groups per super-group
+constexpr int kTileSG = 64;        // super-groups per layout tile
+constexpr int kMetaBytes = 18;     // per-SG scale bytes: 16 u8 codes + bf16 sg_scale
+constexpr uint64_t kGolden = 0x9e3779b97f4a7c15ULL;
+constexpr uint64_t kSeedSalt = 0x6a09e667f3bcc909ULL;
+
+enum Purpose : uint32_t { kEntryQuant = 1, kScaleQuant = 2, kPermutation = 3 };
+
+// ---------------------------------------------------------------- PRNG
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 33)) * 0xff51afd7ed558ccdULL;
+  z = (z ^ (z >> 33)) * 0xc4ceb9fe1a85ec53ULL;
+  return z ^ (z >> 33);
+}
+// h' = mix64(h ^ (w + golden + (h << 6) + (h >> 2)))   (proj/src/random.cpp:19-21)
+__host__ __device__ __forceinline__ uint64_t absorb(uint64_t h, uint64_t w) {
+  return mix64(h ^ (w + kGolden + (h << 6) + (h >> 2)));
+}
+// The absorb of a counter into a fixed h: the (h-dependent) addend is shared by
+// every counter, so a Fisher-Yates draw costs one add + xor + mix64.
+__host__ __device__ __forceinline__ uint64_t absorb_base(uint64_t h) {
+  return kGolden + (h << 6) + (h >> 2);
+}
+__host__ __device__ __forceinline__ double unit53(uint64_t b) {
+  return static_cast<double>(b >> 11) * 0x1.0p-53;
+}
+// Prefix of keyed_bits up to and including the purpose word
+// (proj/src/random.cpp:25-34): the per-round constant of each purpose.
+__host__ __device__ inline uint64_t purpose_prefix(uint64_t seed, uint64_t round, uint32_t purpose) {
+  uint64_t h = mix64(seed ^ kSeedSalt);
+  h = absorb(h, round);
+  return absorb(h, purpose);
+}
+
+// r % k for the Fisher-Yates draw, k = i+1 <= 64.  Compile-time k lets nvcc
+// strength-reduce; the runtime path handles arbitrary worker counts.
+template <int K>
+__device__ __forceinline__ uint32_t mod_const(uint64_t r) {
+  if constexpr ((K & (K - 1)) == 0) return static_cast<uint32_t>(r) & (K - 1);
+  else return static_cast<uint32_t>(r % K);
+}
+
+// ---------------------------------------------------------------- bf16
+__host__ __device__ __forceinline__ float bf16_to_float(uint16_t b) {
+#ifdef __CUDA_ARCH__
+  return __uint_as_float(static_cast<uint32_t>(b) << 16);
+#else
+  union { uint32_t u; float f; } c{static_cast<uint32_t>(b) << 16};
+  return c.f;
+#endif
+}
+// Round toward +inf onto bf16 with clamp below +inf (bf16.hpp:30-40).
+__device__ __forceinline__ uint16_t bf16_round_up(float v) {
+  const uint32_t u = __float_as_uint(v);
+  const uint16_t hi = static_cast<uint16_t>(u >> 16);
+  if ((u & 0xffffu) == 0) return hi;
+  const uint16_t up = static_cast<uint16_t>(hi + 1);
+  return (up & 0x7f80u) == 0x7f80u ? 0x7f7fu : up;
+}
+
+// ---------------------------------------------------------------- layout
+// A chunk of nsg super-groups in body order: n8 width-8, then n4 width-4, then
+// n2 width-2 super-groups (the reference's wire run order 8,4,2).  Super-groups
+// are packed in tiles of 64: [payloads][16 u8 codes x cnt][bf16 sg_scale x cnt].
+// Every tile starts 64-byte aligned (payloads are 64/128/256 B, metadata is
+// 18 x 64 = 1152 B for full tiles) and a run of whole tiles is one contiguous
+// byte range, which is what the transport pipelines on.
+struct Layout {
+  uint32_t nsg, n8, n4;
+  __host__ __device__ uint32_t n2() const { return nsg - n8 - n4; }
+  __host__ __device__ uint32_t width(uint32_t i) const { return i < n8 ? 8 : (i < n8 + n4 ? 4 : 2); }
+  // payload bytes of super-groups [0, k)
+  __host__ __device__ uint64_t pay_prefix(uint32_t k) const {
+    const uint32_t a = k < n8 ? k : n8;
+    const uint32_t r = k - a;
+    const uint32_t b = r < n4 ? r : n4;
+    const uint32_t c = r - b;
+    return 256ull * a + 128ull * b + 64ull * c;
+  }
+  __host__ __device__ uint64_t tile_offset(uint32_t t) const {
+    const uint32_t k = t * kTileSG < nsg ? t * kTileSG : nsg;
+    return pay_prefix(k) + static_cast<uint64_t>(kMetaBytes) * k;
+  }
+  __host__ __device__ uint32_t tiles() const { return (nsg + kTileSG - 1) / kTileSG; }
+  __host__ __device__ uint64_t bytes() const { return tile_offset(tiles()); }
+  struct SG {
+    uint64_t payload, codes, scale;
+    uint32_t width;
+  };
+  __host__ __device__ SG locate(uint32_t i) const {
+    const uint32_t t = i / kTileSG, first = t * kTileSG;
+    const uint32_t last = first + kTileSG < nsg ? first + kTileSG : nsg;
+    const uint32_t cnt = last - first;
+    const uint64_t base = tile_offset(t);
+    const uint64_t tp = pay_prefix(last) - pay_prefix(first);
+    SG s;
+    s.payload = base + (pay_prefix(i) - pay_prefix(first));
+    s.codes = base + tp + 16ull * (i - first);
+    s.scale = base + tp + 16ull * cnt + 2ull * (i - first);
+    s.width = width(i);
+    return s;
+  }
+};
+
+}  // namespace dq

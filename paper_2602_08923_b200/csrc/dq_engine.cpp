@@ -1,0 +1,1133 @@
+// dq_engine.cpp — host runtime of the DynamiQ B200 all-reduce and its C-ABI.
+//
+// Mirrors the reference's round orchestration (proj/src/engine.cpp:94-418):
+// stats -> exact stats reduction -> fast allocation -> width-sorted chunks ->
+// per-chunk reduce events (leaf compress / fused DAR / DA, last-parent rule) ->
+// sink compression -> all-gather -> decode with unpermute + denormalize.  All
+// data stays on the device; every kernel is stream-ordered on the caller's
+// stream.  Two executors share the plan: dq_sim_round runs every worker of a
+// chunk on one GPU (BASELINE config 2), dq_allreduce runs one rank per GPU and
+// moves the compressed chunks over NVLink with NCCL point-to-point.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include "../../include/dynamiq_b200.h"
+#include "dq_internal.h"
+
+namespace dq {
+namespace {
+
+thread_local std::string g_err;
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+#define DQ_CUDA(x)                                                                      \
+  do {                                                                                  \
+    cudaError_t e_ = (x);                                                               \
+    if (e_ != cudaSuccess)                                                              \
+      throw Error(DQ_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_));           \
+  } while (0)
+#define DQ_NCCL(x)                                                                      \
+  do {                                                                                  \
+    ncclResult_t r_ = (x);                                                              \
+    if (r_ != ncclSuccess) throw Error(DQ_ENCCL, std::string(#x) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+[[noreturn]] void invalid(const std::string& m) { throw Error(DQ_EINVAL, m); }
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return DQ_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return DQ_EINVAL;
+  }
+}
+
+// ------------------------------------------------------------ codebooks
+// f(eps, r) in double, stored as float, strictly increasing (proj/src/codebook.cpp:20-60);
+// default eps 0.05 / 0.25 / 0.05 for widths 2 / 4 / 8 (codebook.cpp:63-75).
+void fill_book(float* q, int width, bool uniform) {
+  const int count = 1 << (width - 1), top = count - 1;
+  if (uniform) {
+    for (int r = 0; r < count; ++r) q[r] = static_cast<float>(static_cast<double>(r) / top);
+    return;
+  }
+  const double eps = width == 4 ? 0.25 : 0.05;
+  const double base = 1.0 + 2.0 * eps * eps;
+  for (int r = 0; r < count; ++r)
+    q[r] = static_cast<float>(r == 0 ? 0.0 : r == top ? 1.0 : (std::pow(base, r) - 1.0) / (std::pow(base, top) - 1.0));
+  for (int r = 1; r < count; ++r)
+    if (q[r] <= q[r - 1]) q[r] = std::nextafter(q[r - 1], 2.0f);
+}
+
+std::once_flag g_books_once;
+void ensure_books() {
+  static int status = 0;
+  std::call_once(g_books_once, [] {
+    float books[2][138];
+    for (int u = 0; u < 2; ++u) {
+      fill_book(books[u], 2, u);
+      fill_book(books[u] + 2, 4, u);
+      fill_book(books[u] + 10, 8, u);
+    }
+    status = upload_codebooks(&books[0][0]) == cudaSuccess ? 0 : 1;
+  });
+  if (status) throw Error(DQ_ECUDA, "codebook upload failed");
+}
+
+// alpha = 4 / log2(512/17)  (allocation.cpp:34-35)
+const double kAlpha = 4.0 / std::log2(512.0 / 17.0);
+
+double key_to_double(uint64_t k) {
+  const uint64_t b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  double d;
+  std::memcpy(&d, &b, 8);
+  return d;
+}
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  void reserve(size_t want) {
+    if (want <= n) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    DQ_CUDA(cudaMalloc(&p, sizeof(T) * (want ? want : 1)));
+    n = want;
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+struct Event {
+  uint32_t snd, rcv, slot;
+};
+struct Plan {  // proj/src/topology.cpp:8-70
+  uint32_t sink, sink_slot, n_slots, n_gat;
+  std::vector<Event> red;
+};
+Plan make_plan(uint32_t n, uint32_t c, int topology) {
+  Plan p;
+  p.sink = c;
+  p.n_gat = n - 1;
+  if (topology == DQ_RING) {
+    for (uint32_t h = 0; h + 1 < n; ++h) p.red.push_back({(c + 1 + h) % n, (c + 2 + h) % n, h});
+  } else {
+    int stages = 0;
+    while ((1u << stages) < n) ++stages;
+    uint32_t slot = 0;
+    for (int l = 0; l < stages; ++l) {
+      const uint32_t bit = 1u << (stages - 1 - l), high = ~(2 * bit - 1);
+      for (uint32_t w = 0; w < n; ++w) {
+        if ((w & high) != (c & high) || (w & bit) == (c & bit)) continue;
+        p.red.push_back({w, w ^ bit, slot++});
+      }
+    }
+  }
+  p.sink_slot = static_cast<uint32_t>(p.red.size());
+  p.n_slots = p.sink_slot + 1;
+  return p;
+}
+
+uint64_t fnv1a(const uint8_t* b, size_t n, uint64_t h) {
+  for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 0x100000001b3ULL;
+  return h;
+}
+
+}  // namespace
+}  // namespace dq
+
+using namespace dq;
+
+struct dq_ctx {
+  dq_config cfg{};
+  int device = 0;
+  // round scratch
+  DevBuf<float> mean_all, sq_all, gmean, gsq;
+  DevBuf<uint8_t> widths;
+  DevBuf<uint32_t> perm;
+  DevBuf<double> level;
+  DevBuf<AllocState> astate;
+  DevBuf<uint64_t> bins;
+  DevBuf<uint32_t> blockcnt, counts;
+  DevBuf<const float*> xptrs;
+  DevBuf<double> vn;
+  DevBuf<uint8_t> msgs;   // message pool
+  DevBuf<float> accs;     // per-worker chunk accumulators (butterfly)
+  DevBuf<float> stage;    // host-round staging of inputs / output
+  AllocState* h_state = nullptr;
+  uint32_t* h_counts = nullptr;
+  double* h_vn = nullptr;
+  uint32_t last_T = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // per-kernel-family device timing (CUDA events bracketing each launch)
+  struct Prof {
+    int kind;
+    double bytes;
+    cudaEvent_t a, b;
+  };
+  int profile = 0;
+  std::vector<Prof> pending;
+  std::vector<cudaEvent_t> ev_pool;
+  double prof_ms[16] = {}, prof_bytes[16] = {};
+  uint64_t prof_launches[16] = {};
+  // distributed
+  ncclComm_t comm = nullptr;
+  int rank = 0, nranks = 1;
+  ~dq_ctx() {
+    if (h_state) cudaFreeHost(h_state);
+    if (h_counts) cudaFreeHost(h_counts);
+    if (h_vn) cudaFreeHost(h_vn);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (comm) ncclCommDestroy(comm);
+    for (auto& p : pending) {
+      cudaEventDestroy(p.a);
+      cudaEventDestroy(p.b);
+    }
+    for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
+  }
+};
+
+namespace dq {
+namespace {
+
+cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+enum Kind { K_STATS, K_REDUCE, K_ALLOC_SEARCH, K_ALLOC_ASSIGN, K_LEAF, K_DAR, K_DA, K_DECODE, K_NCCL, K_NKINDS };
+const char* const kKindName[K_NKINDS] = {"stats", "reduce_stats", "alloc_search", "alloc_assign", "quant_leaf",
+                                         "quant_dar", "decompress_accumulate", "decode_out", "nccl"};
+const int kKindLaunches[K_NKINDS] = {1, 1, 3 + 2 * kAllocMaxPasses, 3, 1, 1, 1, 1, 0};
+
+cudaEvent_t pool_event(dq_ctx* ctx) {
+  if (!ctx->ev_pool.empty()) {
+    cudaEvent_t e = ctx->ev_pool.back();
+    ctx->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  DQ_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+// run `launch` on st; when profiling, bracket it with events and book its algorithmic bytes
+template <class F>
+void timed(dq_ctx* ctx, int kind, double bytes, cudaStream_t st, F&& launch) {
+  if (!ctx || !ctx->profile) {
+    launch();
+    if (ctx) ctx->prof_launches[kind] += kKindLaunches[kind];
+    return;
+  }
+  dq_ctx::Prof p{kind, bytes, pool_event(ctx), pool_event(ctx)};
+  DQ_CUDA(cudaEventRecord(p.a, st));
+  launch();
+  DQ_CUDA(cudaEventRecord(p.b, st));
+  ctx->pending.push_back(p);
+  ctx->prof_launches[kind] += kKindLaunches[kind];
+}
+
+// after a stream sync: fold the pending event pairs into the per-kind totals
+void harvest(dq_ctx* ctx) {
+  for (auto& p : ctx->pending) {
+    float ms = 0.f;
+    DQ_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+    ctx->prof_ms[p.kind] += ms;
+    ctx->prof_bytes[p.kind] += p.bytes;
+    ctx->ev_pool.push_back(p.a);
+    ctx->ev_pool.push_back(p.b);
+  }
+  ctx->pending.clear();
+}
+
+double quant_bytes(const Layout& L, bool dar) {  // local fp32 + mean/perm + in (DAR) + out
+  const double chunk = static_cast<double>(L.bytes());
+  return 1024.0 * L.nsg + 8.0 * L.nsg + chunk * (dar ? 2.0 : 1.0);
+}
+
+void validate(const dq_config& c) {  // engine.cpp:243-255 + device coverage
+  if (c.n_workers == 0 || c.n_workers > 64) invalid("n_workers must be in 1..64");
+  if (c.group_size == 0 || c.super_group_size % c.group_size != 0 || c.super_group_size % 4 != 0)
+    invalid("super-group size must be a multiple of the group size and of 4");
+  if (!c.variable_width && c.fixed_width != 2 && c.fixed_width != 4 && c.fixed_width != 8)
+    invalid("fixed width must be one of {2,4,8}");
+  if ((c.allocator == DQ_ALLOC_FIXED) != !c.variable_width)
+    invalid("fixed-width allocator requires variable_width off and vice versa");
+  if (c.threads == 0) invalid("threads must be >= 1");
+  if (c.topology == DQ_BUTTERFLY && (c.n_workers & (c.n_workers - 1)) != 0)
+    invalid("butterfly topology requires a power-of-two worker count");
+  if (c.topology != DQ_RING && c.topology != DQ_BUTTERFLY) invalid("unknown topology");
+  if (c.group_size != 16 || c.super_group_size != 256)
+    invalid("device codec supports group_size 16 and super_group_size 256");
+  if (!c.hierarchical_scales) invalid("device codec supports hierarchical scales only");
+  if (c.codec != 0) invalid("device codec supports the quantized codec only");
+  if (c.variable_width && c.allocator != DQ_ALLOC_FAST) invalid("device supports the fast allocator");
+}
+
+double payload_budget(const dq_config& c) {  // allocation.cpp:45-58
+  const double bbar = c.budget_bits - (8.0 / c.group_size + 16.0 / c.super_group_size);
+  if (!(bbar > 2.0)) {
+    char m[160];
+    std::snprintf(m, sizeof m, "payload budget %f does not exceed the minimum width 2", bbar);
+    throw Error(DQ_EINFEASIBLE, m);
+  }
+  return bbar;
+}
+
+AllocWork work_of(dq_ctx* ctx, uint32_t T) {
+  ctx->level.reserve(T);
+  ctx->astate.reserve(1);
+  ctx->bins.reserve(4 * kAllocBins);
+  ctx->blockcnt.reserve(4 * (alloc_blocks(T) + 1));
+  ctx->counts.reserve(4);
+  if (!ctx->h_state) DQ_CUDA(cudaMallocHost(&ctx->h_state, sizeof(AllocState)));
+  if (!ctx->h_counts) DQ_CUDA(cudaMallocHost(&ctx->h_counts, 4 * sizeof(uint32_t)));
+  return AllocWork{ctx->level.p, ctx->astate.p, ctx->bins.p, ctx->blockcnt.p, ctx->counts.p};
+}
+
+struct AllocResult {
+  double u = 0.0;
+  uint64_t payload = 0;
+  uint32_t n8 = 0, n4 = 0, n2 = 0, passes = 0;
+};
+
+// allocate_fast (allocation.cpp:228-260) + build_permutation; see dq_stats_alloc.cu
+AllocResult allocate(dq_ctx* ctx, const dq_config& c, const float* dF, uint32_t T, uint8_t* dW,
+                     uint32_t* dP, cudaStream_t st) {
+  AllocResult r;
+  const uint32_t S = c.super_group_size;
+  AllocWork w = work_of(ctx, T);
+  const double bbar = payload_budget(c);
+  if (!c.variable_width) {
+    if (c.fixed_width > bbar)
+      throw Error(DQ_EINFEASIBLE, "fixed width " + std::to_string(c.fixed_width) + " exceeds the payload budget");
+    launch_fixed_assign(T, c.fixed_width, w, dW, dP, st);
+    DQ_CUDA(cudaGetLastError());
+    r.n8 = c.fixed_width == 8 ? T : 0;
+    r.n4 = c.fixed_width == 4 ? T : 0;
+    r.n2 = c.fixed_width == 2 ? T : 0;
+    r.payload = static_cast<uint64_t>(T) * S * c.fixed_width;
+    return r;
+  }
+  const double budget = static_cast<double>(T) * S * bbar;
+  // largest cumulative flip weight W with S * (2T + W) <= budget, compared in double
+  auto fits = [&](int64_t W) { return static_cast<double>(static_cast<uint64_t>(S) * (2ull * T + W)) <= budget; };
+  int64_t W = static_cast<int64_t>(std::floor(budget / S)) - 2 * static_cast<int64_t>(T);
+  if (W < -1) W = -1;
+  while (fits(W + 1)) ++W;
+  while (W >= 0 && !fits(W)) --W;
+  if (W < 0) throw Error(DQ_EINFEASIBLE, "bit allocation infeasible within budget");
+  timed(ctx, K_ALLOC_SEARCH, 8.0 * T, st, [&] { launch_alloc_search(dF, T, kAlpha, static_cast<uint64_t>(W), w, st); });
+  DQ_CUDA(cudaGetLastError());
+  DQ_CUDA(cudaMemcpyAsync(ctx->h_state, w.state, sizeof(AllocState), cudaMemcpyDeviceToHost, st));
+  DQ_CUDA(cudaStreamSynchronize(st));
+  const AllocState s = *ctx->h_state;
+  double u;
+  switch (s.status) {
+    case 3: u = 0.0; break;                                  // no positive F (allocation.cpp:212-215)
+    case 2: u = key_to_double(s.kmax) + 1.0; break;          // every flip fits: flips.back() + 1
+    case 1:
+      u = s.has_pred ? 0.5 * (key_to_double(s.pred_key) + key_to_double(s.cross_key))
+                     : key_to_double(s.cross_key) - 1.0;     // plateau midpoint / flips.front() - 1
+      break;
+    default: throw Error(DQ_ECUDA, "allocation search did not converge (status " + std::to_string(s.status) + ")");
+  }
+  u = u < -1e6 ? -1e6 : (u > 1e6 ? 1e6 : u);
+  const float t24 = static_cast<float>(std::exp2((4.0 - u) / kAlpha));
+  const float t48 = static_cast<float>(std::exp2((8.0 - u) / kAlpha));
+  timed(ctx, K_ALLOC_ASSIGN, 13.0 * T, st, [&] { launch_alloc_assign(dF, T, t24, t48, w, dW, dP, st); });
+  DQ_CUDA(cudaGetLastError());
+  DQ_CUDA(cudaMemcpyAsync(ctx->h_counts, w.counts, 3 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  DQ_CUDA(cudaStreamSynchronize(st));
+  r.u = u;
+  r.n8 = ctx->h_counts[0];
+  r.n4 = ctx->h_counts[1];
+  r.n2 = ctx->h_counts[2];
+  r.passes = s.passes;
+  r.payload = static_cast<uint64_t>(S) * (8ull * r.n8 + 4ull * r.n4 + 2ull * r.n2);
+  if (static_cast<double>(r.payload) > budget) throw Error(DQ_EINFEASIBLE, "bit allocation infeasible within budget");
+  return r;
+}
+
+Layout chunk_layout(const AllocResult& a, uint32_t lo, uint32_t hi) {
+  auto overlap = [](uint32_t a0, uint32_t a1, uint32_t b0, uint32_t b1) {
+    const uint32_t l = a0 > b0 ? a0 : b0, h = a1 < b1 ? a1 : b1;
+    return h > l ? h - l : 0u;
+  };
+  Layout L;
+  L.nsg = hi - lo;
+  L.n8 = overlap(lo, hi, 0, a.n8);
+  L.n4 = overlap(lo, hi, a.n8, a.n8 + a.n4);
+  return L;
+}
+
+CodecArgs base_args(const dq_config& c, uint32_t chunk) {
+  CodecArgs a{};
+  a.h3_eq = absorb(purpose_prefix(c.seed, c.round, kEntryQuant), chunk);
+  a.h3_sc = absorb(purpose_prefix(c.seed, c.round, kScaleQuant), chunk);
+  a.h3_pm = absorb(purpose_prefix(c.seed, c.round, kPermutation), chunk);
+  a.correlated = c.correlated;
+  a.uniform_books = c.non_uniform ? 0 : 1;
+  a.n_workers_f = static_cast<float>(c.n_workers);
+  return a;
+}
+
+// reference-format bytes of a device chunk (serialize_chunk, codec.cpp:319-343)
+void to_reference(const uint8_t* soa, uint32_t chunk, const Layout& L, uint8_t* out) {
+  auto put32 = [&](size_t at, uint32_t v) {
+    for (int i = 0; i < 4; ++i) out[at + i] = static_cast<uint8_t>(v >> (8 * i));
+  };
+  put32(0, chunk);
+  put32(4, L.nsg);
+  put32(8, L.n8);
+  put32(12, L.n4);
+  put32(16, L.n2());
+  put32(20, 0);
+  size_t at = 24;
+  for (uint32_t i = 0; i < L.nsg; ++i) {
+    const Layout::SG g = L.locate(i);
+    std::memcpy(out + at, soa + g.scale, 2);
+    std::memcpy(out + at + 2, soa + g.codes, 16);
+    std::memcpy(out + at + 18, soa + g.payload, 32 * g.width);
+    at += 18 + 32 * g.width;
+  }
+}
+
+// wire accounting of one message of a chunk (engine.cpp:135-160)
+void account(dq_round_info* info, const Layout& L, bool fresh) {
+  const uint64_t coords = static_cast<uint64_t>(L.nsg) * 256;
+  const uint64_t pay = 256ull * (8ull * L.n8 + 4ull * L.n4 + 2ull * L.n2());
+  const uint64_t scl = static_cast<uint64_t>(L.nsg) * (16 + 16 * 8);
+  info->transmitted_coordinates += coords;
+  info->header_bits += 192;
+  info->wire_payload_bits += pay;
+  info->scale_bits += scl;
+  if (fresh) {
+    info->repr_bits += pay + scl;
+    info->compressed_coordinates += coords;
+  }
+}
+
+struct Prepared {
+  uint32_t T;
+  AllocResult a;
+  std::vector<uint32_t> lo;  // chunk boundaries (engine.cpp:52-62)
+  size_t max_chunk_bytes;
+};
+
+// stats (already reduced into ctx->gsq / gmean) -> allocation -> chunk plan
+Prepared prepare(dq_ctx* ctx, uint32_t T, cudaStream_t st) {
+  Prepared p;
+  p.T = T;
+  const dq_config& c = ctx->cfg;
+  p.a = allocate(ctx, c, ctx->gsq.p, T, ctx->widths.p, ctx->perm.p, st);
+  const uint32_t n = c.n_workers;
+  p.lo.resize(n + 1);
+  for (uint32_t i = 0; i <= n; ++i) p.lo[i] = static_cast<uint32_t>(static_cast<uint64_t>(T) * i / n);
+  p.max_chunk_bytes = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    const size_t b = chunk_layout(p.a, p.lo[i], p.lo[i + 1]).bytes();
+    p.max_chunk_bytes = b > p.max_chunk_bytes ? b : p.max_chunk_bytes;
+  }
+  p.max_chunk_bytes = (p.max_chunk_bytes + 255) / 256 * 256;
+  ctx->last_T = T;
+  return p;
+}
+
+void reserve_round(dq_ctx* ctx, uint32_t T, uint32_t n) {
+  ctx->mean_all.reserve(static_cast<size_t>(n) * T);
+  ctx->sq_all.reserve(static_cast<size_t>(n) * T);
+  ctx->gmean.reserve(T);
+  ctx->gsq.reserve(T);
+  ctx->widths.reserve(T);
+  ctx->perm.reserve(T);
+}
+
+void fill_info_alloc(dq_round_info* info, const Prepared& p) {
+  info->u = p.a.u;
+  info->payload_bits = p.a.payload;
+  info->n8 = p.a.n8;
+  info->n4 = p.a.n4;
+  info->n2 = p.a.n2;
+  info->alloc_passes = p.a.passes;
+}
+
+// ---------------------------------------------------------- simulation
+void sim_round(dq_ctx* ctx, const float* const* xs, size_t d, float* out, int flags,
+               dq_round_info* info, cudaStream_t st) {
+  const int collect_wire = flags & DQ_SIM_COLLECT_WIRE;
+  const dq_config& c = ctx->cfg;
+  const uint32_t n = c.n_workers;
+  *info = dq_round_info{};
+  if (d == 0) invalid("empty gradient");
+  if (n == 1) {  // engine.cpp:280-286: nothing to synchronize
+    DQ_CUDA(cudaMemcpyAsync(out, xs[0], d * sizeof(float), cudaMemcpyDeviceToDevice, st));
+    return;
+  }
+  for (uint32_t r = 0; r < n; ++r)
+    if (reinterpret_cast<uintptr_t>(xs[r]) % 16) invalid("gradients must be 16-byte aligned");
+  if (reinterpret_cast<uintptr_t>(out) % 16) invalid("output must be 16-byte aligned");
+  const uint64_t T64 = (d + 255) / 256;
+  if (T64 > 0xffffffffull / 2) invalid("gradient too large");
+  const uint32_t T = static_cast<uint32_t>(T64);
+  ensure_books();
+  if (!ctx->ev0) {
+    DQ_CUDA(cudaEventCreate(&ctx->ev0));
+    DQ_CUDA(cudaEventCreate(&ctx->ev1));
+  }
+  DQ_CUDA(cudaEventRecord(ctx->ev0, st));
+  reserve_round(ctx, T, n);
+  ctx->xptrs.reserve(n);
+  DQ_CUDA(cudaMemcpyAsync(ctx->xptrs.p, xs, n * sizeof(float*), cudaMemcpyHostToDevice, st));
+  timed(ctx, K_STATS, 4.0 * n * d + 8.0 * n * T, st,
+        [&] { launch_stats(ctx->xptrs.p, n, d, T, ctx->mean_all.p, ctx->sq_all.p, st); });
+  timed(ctx, K_REDUCE, 8.0 * (n + 1) * T, st,
+        [&] { launch_reduce_stats(ctx->mean_all.p, ctx->sq_all.p, n, T, ctx->gmean.p, ctx->gsq.p, st); });
+  DQ_CUDA(cudaGetLastError());
+  Prepared p = prepare(ctx, T, st);
+  fill_info_alloc(info, p);
+
+  // message pool: per-worker pending slot + one scratch; per-worker accumulators
+  const size_t mb = p.max_chunk_bytes;
+  ctx->msgs.reserve((n + 2) * mb);
+  uint32_t max_nsg = 0;
+  for (uint32_t i = 0; i < n; ++i) max_nsg = std::max(max_nsg, p.lo[i + 1] - p.lo[i]);
+  const bool need_acc = c.topology == DQ_BUTTERFLY;
+  if (need_acc) ctx->accs.reserve(static_cast<size_t>(n) * max_nsg * 256);
+  std::vector<uint8_t> host_soa, host_ref;
+  uint64_t H = 0xcbf29ce484222325ULL;
+
+  for (uint32_t ch = 0; ch < n; ++ch) {
+    const Plan plan = make_plan(n, ch, c.topology);
+    const Layout L = chunk_layout(p.a, p.lo[ch], p.lo[ch + 1]);
+    CodecArgs base = base_args(c, ch);
+    base.L = L;
+    base.first_sg = p.lo[ch];
+    base.perm = ctx->perm.p;
+    base.gmean = ctx->gmean.p;
+    base.d = d;
+    base.n_slots = plan.n_slots;
+    std::vector<int> pend_slot(n, -1), last_in(n, -1);
+    std::vector<char> has_acc(n, 0);
+    for (size_t e = 0; e < plan.red.size(); ++e) last_in[plan.red[e].rcv] = static_cast<int>(e);
+    std::vector<int> free_slots;
+    for (int k = static_cast<int>(n) + 1; k >= 0; --k) free_slots.push_back(k);
+    auto slot_ptr = [&](int k) { return ctx->msgs.p + static_cast<size_t>(k) * mb; };
+    auto acc_ptr = [&](uint32_t w) { return ctx->accs.p + static_cast<size_t>(w) * max_nsg * 256; };
+    uint64_t hsh = 0xcbf29ce484222325ULL;
+    auto hash_msg = [&](const uint8_t* dmsg, int times_fresh_first) {
+      if (!collect_wire) return;
+      const size_t sb = L.bytes();
+      host_soa.resize(sb);
+      host_ref.resize(sb + 24);
+      DQ_CUDA(cudaMemcpyAsync(host_soa.data(), dmsg, sb, cudaMemcpyDeviceToHost, st));
+      DQ_CUDA(cudaStreamSynchronize(st));
+      to_reference(host_soa.data(), ch, L, host_ref.data());
+      for (int t = 0; t < times_fresh_first; ++t) hsh = fnv1a(host_ref.data(), host_ref.size(), hsh);
+    };
+    auto operand = [&](uint32_t w, CodecArgs& a) -> int {  // 0 gather raw, 1 accumulator
+      if (has_acc[w]) {
+        a.acc_in = acc_ptr(w);
+        return 1;
+      }
+      a.x = xs[w];
+      return 0;
+    };
+    int gather_slot = -1;
+    for (size_t e = 0; e < plan.red.size(); ++e) {
+      const Event ev = plan.red[e];
+      const int os = free_slots.back();
+      free_slots.pop_back();
+      CodecArgs a = base;
+      a.slot = ev.slot;
+      a.out = slot_ptr(os);
+      const int src = operand(ev.snd, a);
+      const bool dar = pend_slot[ev.snd] >= 0;
+      if (dar) a.in = slot_ptr(pend_slot[ev.snd]);
+      timed(ctx, dar ? K_DAR : K_LEAF, quant_bytes(L, dar), st, [&] { launch_quant(a, src, dar, st); });
+      if (dar) {
+        free_slots.push_back(pend_slot[ev.snd]);
+        pend_slot[ev.snd] = -1;
+      }
+      account(info, L, true);
+      hash_msg(slot_ptr(os), 1);
+      const uint32_t r = ev.rcv;
+      if (static_cast<int>(e) == last_in[r] && r != plan.sink) {
+        pend_slot[r] = os;
+      } else if (static_cast<int>(e) == last_in[r] && r == plan.sink) {
+        // fused sink: compress(dec(last) + buf[sink]) at the sink slot (== DA then compress)
+        const int gs = free_slots.back();
+        free_slots.pop_back();
+        CodecArgs g = base;
+        g.slot = plan.sink_slot;
+        g.out = slot_ptr(gs);
+        g.in = slot_ptr(os);
+        const int gsrc = operand(r, g);
+        timed(ctx, K_DAR, quant_bytes(L, true), st, [&] { launch_quant(g, gsrc, true, st); });
+        free_slots.push_back(os);
+        gather_slot = gs;
+      } else {
+        CodecArgs g = base;
+        g.in = slot_ptr(os);
+        const int gsrc = operand(r, g);
+        g.acc_out = acc_ptr(r);
+        timed(ctx, K_DA, 2048.0 * L.nsg + L.bytes(), st, [&] { launch_da(g, gsrc, st); });
+        has_acc[r] = 1;
+        free_slots.push_back(os);
+      }
+    }
+    DQ_CUDA(cudaGetLastError());
+    // all-gather of the sink's bytes: hashed once per forward (engine.cpp:219-229)
+    if (collect_wire) hash_msg(slot_ptr(gather_slot), static_cast<int>(plan.n_gat));
+    for (uint32_t g = 0; g < plan.n_gat; ++g) account(info, L, g == 0);
+    info->stats_bits += static_cast<uint64_t>(plan.red.size() + plan.n_gat) * 64ull * L.nsg;
+    CodecArgs dec = base;
+    dec.in = slot_ptr(gather_slot);
+    dec.acc_out = out;
+    timed(ctx, K_DECODE, 1032.0 * L.nsg + L.bytes(), st, [&] { launch_decode(dec, 1, st); });
+    DQ_CUDA(cudaGetLastError());
+    H ^= hsh + 0x9e3779b97f4a7c15ULL + (H << 6) + (H >> 2);
+  }
+  if (collect_wire) info->wire_hash = H;
+  DQ_CUDA(cudaEventRecord(ctx->ev1, st));
+  if (flags & DQ_SIM_NO_METRICS) {
+    DQ_CUDA(cudaStreamSynchronize(st));
+    harvest(ctx);
+    float ms = 0.f;
+    DQ_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    info->ms_total = ms;
+    return;
+  }
+  // vNMSE against the fp64 sum of the inputs (metrics, not part of the timed path)
+  ctx->vn.reserve(2);
+  if (!ctx->h_vn) DQ_CUDA(cudaMallocHost(&ctx->h_vn, 2 * sizeof(double)));
+  DQ_CUDA(cudaMemsetAsync(ctx->vn.p, 0, 2 * sizeof(double), st));
+  launch_vnmse(ctx->xptrs.p, n, out, d, ctx->vn.p, st);
+  DQ_CUDA(cudaMemcpyAsync(ctx->h_vn, ctx->vn.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  DQ_CUDA(cudaStreamSynchronize(st));
+  harvest(ctx);
+  info->mse = ctx->h_vn[0] / static_cast<double>(d);
+  info->vnmse = ctx->h_vn[1] > 0 ? ctx->h_vn[0] / ctx->h_vn[1] : 0.0;
+  float ms = 0.f;
+  DQ_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+  info->ms_total = ms;
+}
+
+// ---------------------------------------------------------- distributed
+// One rank per GPU.  Events of every chunk are grouped into stages (ring: the
+// hop index; butterfly: the halving stage) and each stage is one NCCL group of
+// point-to-point sends/receives of compressed chunks over NVLink, bracketed by
+// the fused codec kernels: outgoing = leaf compress or DAR of the held last
+// parent, incoming = held (last parent), DA'd (earlier parents) or, at the
+// chunk's sink, fused DAR at the sink slot.  The all-gather forwards the sink
+// bytes verbatim (engine.cpp:219-229) as one group of n-1 sends and receives.
+void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info* info, cudaStream_t st) {
+  const dq_config& c = ctx->cfg;
+  const uint32_t n = c.n_workers, me = static_cast<uint32_t>(ctx->rank);
+  *info = dq_round_info{};
+  if (d == 0) invalid("empty gradient");
+  if (n == 1) {
+    if (out != x) DQ_CUDA(cudaMemcpyAsync(out, x, d * sizeof(float), cudaMemcpyDeviceToDevice, st));
+    return;
+  }
+  if (!ctx->comm) invalid("dq_comm_init has not been called");
+  if (reinterpret_cast<uintptr_t>(x) % 16 || reinterpret_cast<uintptr_t>(out) % 16)
+    invalid("buffers must be 16-byte aligned");
+  const uint32_t T = static_cast<uint32_t>((d + 255) / 256);
+  ensure_books();
+  if (!ctx->ev0) {
+    DQ_CUDA(cudaEventCreate(&ctx->ev0));
+    DQ_CUDA(cudaEventCreate(&ctx->ev1));
+  }
+  DQ_CUDA(cudaEventRecord(ctx->ev0, st));
+  reserve_round(ctx, T, n);
+  ctx->xptrs.reserve(1);
+  DQ_CUDA(cudaMemcpyAsync(ctx->xptrs.p, &x, sizeof(float*), cudaMemcpyHostToDevice, st));
+  // (a) local stats into this rank's row, (b) all-gather rows, fixed-order fp64 reduce (H4)
+  float* my_mean = ctx->mean_all.p + static_cast<size_t>(me) * T;
+  float* my_sq = ctx->sq_all.p + static_cast<size_t>(me) * T;
+  timed(ctx, K_STATS, 4.0 * d + 8.0 * T, st, [&] { launch_stats(ctx->xptrs.p, 1, d, T, my_mean, my_sq, st); });
+  timed(ctx, K_NCCL, 8.0 * T * n, st, [&] {
+    DQ_NCCL(ncclGroupStart());
+    DQ_NCCL(ncclAllGather(my_mean, ctx->mean_all.p, T, ncclFloat, ctx->comm, st));
+    DQ_NCCL(ncclAllGather(my_sq, ctx->sq_all.p, T, ncclFloat, ctx->comm, st));
+    DQ_NCCL(ncclGroupEnd());
+  });
+  timed(ctx, K_REDUCE, 8.0 * (n + 1) * T, st,
+        [&] { launch_reduce_stats(ctx->mean_all.p, ctx->sq_all.p, n, T, ctx->gmean.p, ctx->gsq.p, st); });
+  DQ_CUDA(cudaGetLastError());
+  Prepared p = prepare(ctx, T, st);
+  fill_info_alloc(info, p);
+
+  const size_t mb = p.max_chunk_bytes;
+  uint32_t max_nsg = 0;
+  for (uint32_t i = 0; i < n; ++i) max_nsg = std::max(max_nsg, p.lo[i + 1] - p.lo[i]);
+  // per chunk: outgoing, incoming, held, gather; accumulators for butterfly receivers
+  ctx->msgs.reserve(4ull * n * mb);
+  auto buf = [&](int kind, uint32_t ch) { return ctx->msgs.p + (static_cast<size_t>(kind) * n + ch) * mb; };
+  const bool need_acc = c.topology == DQ_BUTTERFLY;
+  if (need_acc) ctx->accs.reserve(static_cast<size_t>(n) * max_nsg * 256);
+  auto acc_ptr = [&](uint32_t ch) { return ctx->accs.p + static_cast<size_t>(ch) * max_nsg * 256; };
+
+  std::vector<Plan> plans(n);
+  std::vector<Layout> lays(n);
+  std::vector<CodecArgs> bases(n);
+  for (uint32_t ch = 0; ch < n; ++ch) {
+    plans[ch] = make_plan(n, ch, c.topology);
+    lays[ch] = chunk_layout(p.a, p.lo[ch], p.lo[ch + 1]);
+    CodecArgs b = base_args(c, ch);
+    b.L = lays[ch];
+    b.first_sg = p.lo[ch];
+    b.perm = ctx->perm.p;
+    b.gmean = ctx->gmean.p;
+    b.d = d;
+    b.x = x;
+    b.n_slots = plans[ch].n_slots;
+    bases[ch] = b;
+  }
+  // stage of event e of a chunk: ring -> e; butterfly -> halving stage
+  auto stage_of = [&](uint32_t ch, size_t e) -> uint32_t {
+    if (c.topology == DQ_RING) return static_cast<uint32_t>(e);
+    const Event& ev = plans[ch].red[e];
+    const uint32_t bit = ev.snd ^ ev.rcv;
+    uint32_t stages = 0;
+    while ((1u << stages) < n) ++stages;
+    uint32_t l = 0;
+    while ((1u << (stages - 1 - l)) != bit) ++l;
+    return l;
+  };
+  uint32_t n_stages = 0;
+  for (uint32_t ch = 0; ch < n; ++ch)
+    for (size_t e = 0; e < plans[ch].red.size(); ++e) n_stages = std::max(n_stages, stage_of(ch, e) + 1);
+  std::vector<char> held(n, 0), has_acc(n, 0);
+  auto operand = [&](uint32_t ch, CodecArgs& a) -> int {
+    if (has_acc[ch]) {
+      a.acc_in = acc_ptr(ch);
+      return 1;
+    }
+    return 0;
+  };
+  for (uint32_t s = 0; s < n_stages; ++s) {
+    struct Io { uint32_t ch; size_t e; };
+    std::vector<Io> sends, recvs;
+    for (uint32_t ch = 0; ch < n; ++ch)
+      for (size_t e = 0; e < plans[ch].red.size(); ++e) {
+        if (stage_of(ch, e) != s) continue;
+        if (plans[ch].red[e].snd == me) sends.push_back({ch, e});
+        if (plans[ch].red[e].rcv == me) recvs.push_back({ch, e});
+      }
+    for (const Io& io : sends) {
+      CodecArgs a = bases[io.ch];
+      a.slot = plans[io.ch].red[io.e].slot;
+      a.out = buf(0, io.ch);
+      const int src = operand(io.ch, a);
+      if (held[io.ch]) a.in = buf(2, io.ch);
+      const bool dar = held[io.ch] != 0;
+      timed(ctx, dar ? K_DAR : K_LEAF, quant_bytes(lays[io.ch], dar), st, [&] { launch_quant(a, src, dar, st); });
+      held[io.ch] = 0;
+    }
+    DQ_CUDA(cudaGetLastError());
+    double xbytes = 0;
+    for (const Io& io : sends) xbytes += lays[io.ch].bytes();
+    timed(ctx, K_NCCL, xbytes, st, [&] {
+      DQ_NCCL(ncclGroupStart());
+      for (const Io& io : sends)
+        DQ_NCCL(ncclSend(buf(0, io.ch), lays[io.ch].bytes(), ncclUint8, plans[io.ch].red[io.e].rcv, ctx->comm, st));
+      for (const Io& io : recvs)
+        DQ_NCCL(ncclRecv(buf(1, io.ch), lays[io.ch].bytes(), ncclUint8, plans[io.ch].red[io.e].snd, ctx->comm, st));
+      DQ_NCCL(ncclGroupEnd());
+    });
+    for (const Io& io : recvs) {
+      const Plan& pl = plans[io.ch];
+      size_t last = 0;
+      for (size_t e = 0; e < pl.red.size(); ++e)
+        if (pl.red[e].rcv == me) last = e;
+      CodecArgs a = bases[io.ch];
+      a.in = buf(1, io.ch);
+      if (io.e == last && me != pl.sink) {
+        DQ_CUDA(cudaMemcpyAsync(buf(2, io.ch), buf(1, io.ch), lays[io.ch].bytes(), cudaMemcpyDeviceToDevice, st));
+        held[io.ch] = 1;
+      } else if (io.e == last) {
+        a.slot = pl.sink_slot;
+        a.out = buf(3, io.ch);
+        const int src = operand(io.ch, a);
+        timed(ctx, K_DAR, quant_bytes(lays[io.ch], true), st, [&] { launch_quant(a, src, true, st); });
+      } else {
+        const int src = operand(io.ch, a);
+        a.acc_out = acc_ptr(io.ch);
+        timed(ctx, K_DA, 2048.0 * lays[io.ch].nsg + lays[io.ch].bytes(), st, [&] { launch_da(a, src, st); });
+        has_acc[io.ch] = 1;
+      }
+    }
+    DQ_CUDA(cudaGetLastError());
+  }
+  // all-gather of the sink-compressed chunks (sink of chunk ch is rank ch)
+  timed(ctx, K_NCCL, static_cast<double>(lays[me].bytes()) * (n - 1), st, [&] {
+    DQ_NCCL(ncclGroupStart());
+    for (uint32_t peer = 0; peer < n; ++peer) {
+      if (peer == me) continue;
+      DQ_NCCL(ncclSend(buf(3, me), lays[me].bytes(), ncclUint8, peer, ctx->comm, st));
+      DQ_NCCL(ncclRecv(buf(3, peer), lays[peer].bytes(), ncclUint8, peer, ctx->comm, st));
+    }
+    DQ_NCCL(ncclGroupEnd());
+  });
+  for (uint32_t ch = 0; ch < n; ++ch) {
+    CodecArgs a = bases[ch];
+    a.in = buf(3, ch);
+    a.acc_out = out;
+    timed(ctx, K_DECODE, 1032.0 * lays[ch].nsg + lays[ch].bytes(), st, [&] { launch_decode(a, 1, st); });
+    for (uint32_t g = 0; g < plans[ch].n_gat; ++g) account(info, lays[ch], g == 0);
+    for (size_t e = 0; e < plans[ch].red.size(); ++e) account(info, lays[ch], true);
+    info->stats_bits += static_cast<uint64_t>(plans[ch].red.size() + plans[ch].n_gat) * 64ull * lays[ch].nsg;
+  }
+  DQ_CUDA(cudaGetLastError());
+  DQ_CUDA(cudaEventRecord(ctx->ev1, st));
+  if (ctx->profile) {
+    DQ_CUDA(cudaStreamSynchronize(st));
+    harvest(ctx);
+    float ms = 0.f;
+    DQ_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    info->ms_total = ms;
+  }
+}
+
+}  // namespace
+}  // namespace dq
+
+// ====================================================================== C-ABI
+extern "C" {
+
+int dq_version(void) { return DQ_VERSION; }
+const char* dq_last_error(void) { return g_err.c_str(); }
+
+void dq_config_default(dq_config* c) {  // engine.hpp:22-43 defaults
+  *c = dq_config{};
+  c->n_workers = 4;
+  c->group_size = 16;
+  c->super_group_size = 256;
+  c->budget_bits = 5.0;
+  c->non_uniform = 1;
+  c->variable_width = 1;
+  c->hierarchical_scales = 1;
+  c->correlated = 1;
+  c->fixed_width = 4;
+  c->allocator = DQ_ALLOC_FAST;
+  c->topology = DQ_RING;
+  c->codec = 0;
+  c->seed = 1;
+  c->round = 0;
+  c->threads = 1;
+}
+
+int dq_ctx_create(const dq_config* cfg, int device, dq_ctx** out) {
+  return guarded([&] {
+    if (!cfg || !out) invalid("null argument");
+    validate(*cfg);
+    DQ_CUDA(cudaSetDevice(device));
+    auto* c = new dq_ctx;
+    c->cfg = *cfg;
+    c->device = device;
+    *out = c;
+  });
+}
+
+int dq_ctx_destroy(dq_ctx* ctx) {
+  delete ctx;
+  return DQ_OK;
+}
+
+int dq_ctx_set_config(dq_ctx* ctx, const dq_config* cfg) {
+  return guarded([&] {
+    if (!ctx || !cfg) invalid("null argument");
+    validate(*cfg);
+    ctx->cfg = *cfg;
+  });
+}
+
+size_t dq_chunk_bytes(uint32_t n8, uint32_t n4, uint32_t n2) {
+  Layout L{n8 + n4 + n2, n8, n4};
+  return static_cast<size_t>(L.bytes());
+}
+
+static CodecArgs prim_args(const dq_qctx* q, uint32_t n8, uint32_t n4, uint32_t n2, uint32_t first,
+                           int non_uniform) {
+  if (!q) invalid("null qctx");
+  if (q->correlated && (q->n_slots == 0 || q->hop_slot >= q->n_slots))
+    invalid("correlated_uniform slot out of range");
+  if (q->n_slots > 64) invalid("n_slots must be <= 64 on device");
+  dq_config c;
+  dq_config_default(&c);
+  c.seed = q->seed;
+  c.round = q->round;
+  c.correlated = q->correlated;
+  c.non_uniform = non_uniform;
+  CodecArgs a = base_args(c, q->chunk_index);
+  a.L = Layout{n8 + n4 + n2, n8, n4};
+  a.first_sg = first;
+  a.slot = q->hop_slot;
+  a.n_slots = q->n_slots ? q->n_slots : 1;
+  return a;
+}
+
+int dq_compress_chunk(const float* d_values, uint32_t n8, uint32_t n4, uint32_t n2, const dq_qctx* q,
+                      uint32_t first, int non_uniform, void* d_out, void* stream) {
+  return guarded([&] {
+    ensure_books();
+    CodecArgs a = prim_args(q, n8, n4, n2, first, non_uniform);
+    a.acc_in = d_values;
+    a.out = static_cast<uint8_t*>(d_out);
+    launch_quant(a, 1, false, S(stream));
+    DQ_CUDA(cudaGetLastError());
+  });
+}
+
+int dq_dar_chunk(const void* d_in, const float* d_local, uint32_t n8, uint32_t n4, uint32_t n2,
+                 const dq_qctx* q, uint32_t first, int non_uniform, void* d_out, void* stream) {
+  return guarded([&] {
+    ensure_books();
+    CodecArgs a = prim_args(q, n8, n4, n2, first, non_uniform);
+    a.acc_in = d_local;
+    a.in = static_cast<const uint8_t*>(d_in);
+    a.out = static_cast<uint8_t*>(d_out);
+    launch_quant(a, 1, true, S(stream));
+    DQ_CUDA(cudaGetLastError());
+  });
+}
+
+int dq_da_chunk(const void* d_in, float* d_acc, uint32_t n8, uint32_t n4, uint32_t n2, int non_uniform,
+                void* stream) {
+  return guarded([&] {
+    ensure_books();
+    dq_qctx q{0, 0, 0, 0, 1, 0};
+    CodecArgs a = prim_args(&q, n8, n4, n2, 0, non_uniform);
+    a.in = static_cast<const uint8_t*>(d_in);
+    a.acc_in = d_acc;
+    a.acc_out = d_acc;
+    launch_da(a, 1, S(stream));
+    DQ_CUDA(cudaGetLastError());
+  });
+}
+
+int dq_decompress_chunk(const void* d_in, float* d_out, uint32_t n8, uint32_t n4, uint32_t n2,
+                        int non_uniform, void* stream) {
+  return guarded([&] {
+    ensure_books();
+    dq_qctx q{0, 0, 0, 0, 1, 0};
+    CodecArgs a = prim_args(&q, n8, n4, n2, 0, non_uniform);
+    a.in = static_cast<const uint8_t*>(d_in);
+    a.acc_out = d_out;
+    launch_decode(a, 0, S(stream));
+    DQ_CUDA(cudaGetLastError());
+  });
+}
+
+int dq_to_reference_wire(const void* h_soa, uint32_t chunk_index, uint32_t n8, uint32_t n4, uint32_t n2,
+                         void* h_ref) {
+  return guarded([&] {
+    Layout L{n8 + n4 + n2, n8, n4};
+    to_reference(static_cast<const uint8_t*>(h_soa), chunk_index, L, static_cast<uint8_t*>(h_ref));
+  });
+}
+
+int dq_from_reference_wire(const void* h_ref, size_t len, void* h_soa, size_t soa_cap,
+                           uint32_t* chunk_index, uint32_t* n8, uint32_t* n4, uint32_t* n2) {
+  // strict parser with the reference's checks (codec.cpp:345-399), S=256, s=16, hierarchical
+  return guarded([&] {
+    const uint8_t* b = static_cast<const uint8_t*>(h_ref);
+    auto mal = [](const char* m) { throw Error(DQ_EMALFORMED, std::string("malformed compressed buffer: ") + m); };
+    auto get32 = [&](size_t at) {
+      return static_cast<uint32_t>(b[at]) | static_cast<uint32_t>(b[at + 1]) << 8 |
+             static_cast<uint32_t>(b[at + 2]) << 16 | static_cast<uint32_t>(b[at + 3]) << 24;
+    };
+    if (len < 24) mal("truncated header");
+    const uint32_t count = get32(4);
+    const uint32_t r8 = get32(8), r4 = get32(12), r2 = get32(16), r16 = get32(20);
+    if (static_cast<uint64_t>(r8) + r4 + r2 + r16 != count) mal("width run-lengths do not sum to the super-group count");
+    if (r16) invalid("width-16 passthrough is not supported by the device codec");
+    Layout L{count, r8, r4};
+    size_t at = 24;
+    for (uint32_t i = 0; i < count; ++i) {
+      const uint32_t w = L.width(i);
+      const size_t rec = 18 + 32 * w;
+      if (len - at < rec) mal("truncated super-group body");
+      if ((b[at] | b[at + 1] << 8) == 0) {
+        for (size_t k = 2; k < 18; ++k)
+          if (b[at + k]) mal("zero super-group scale with nonzero group scale");
+        for (size_t k = 18; k < rec; ++k)
+          if (b[at + k]) mal("zero super-group scale with nonzero payload");
+      }
+      at += rec;
+    }
+    if (at != len) mal("trailing bytes after chunk body");
+    if (soa_cap < L.bytes()) invalid("output capacity");
+    uint8_t* o = static_cast<uint8_t*>(h_soa);
+    at = 24;
+    for (uint32_t i = 0; i < count; ++i) {
+      const Layout::SG g = L.locate(i);
+      std::memcpy(o + g.scale, b + at, 2);
+      std::memcpy(o + g.codes, b + at + 2, 16);
+      std::memcpy(o + g.payload, b + at + 18, 32 * g.width);
+      at += 18 + 32 * g.width;
+    }
+    *chunk_index = get32(0);
+    *n8 = r8;
+    *n4 = r4;
+    *n2 = r2;
+  });
+}
+
+int dq_compute_stats(const float* d_x, size_t d, float* d_mean, float* d_sq, void* stream) {
+  return guarded([&] {
+    const uint32_t T = static_cast<uint32_t>((d + 255) / 256);
+    const float** dp = nullptr;
+    DQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dp), sizeof(float*), S(stream)));
+    DQ_CUDA(cudaMemcpyAsync(dp, &d_x, sizeof(float*), cudaMemcpyHostToDevice, S(stream)));
+    launch_stats(dp, 1, d, T, d_mean, d_sq, S(stream));
+    DQ_CUDA(cudaGetLastError());
+    DQ_CUDA(cudaFreeAsync(dp, S(stream)));
+    DQ_CUDA(cudaStreamSynchronize(S(stream)));  // the pointer array lives on the host stack
+  });
+}
+
+int dq_reduce_stats(const float* d_means, const float* d_sqs, uint32_t n, size_t nsg, float* d_gm,
+                    float* d_gs, void* stream) {
+  return guarded([&] {
+    if (n == 0) invalid("reduce_stats needs at least one worker");
+    launch_reduce_stats(d_means, d_sqs, n, static_cast<uint32_t>(nsg), d_gm, d_gs, S(stream));
+    DQ_CUDA(cudaGetLastError());
+  });
+}
+
+int dq_allocate_fast(dq_ctx* ctx, const float* d_F, size_t nsg, double b, uint8_t* d_widths,
+                     uint32_t* d_perm, double* u, uint64_t* payload, uint32_t counts[3], void* stream) {
+  return guarded([&] {
+    if (!ctx) invalid("null context");
+    dq_config c = ctx->cfg;
+    c.budget_bits = b;
+    c.variable_width = 1;
+    c.allocator = DQ_ALLOC_FAST;
+    AllocResult r = allocate(ctx, c, d_F, static_cast<uint32_t>(nsg), d_widths, d_perm, S(stream));
+    if (u) *u = r.u;
+    if (payload) *payload = r.payload;
+    if (counts) {
+      counts[0] = r.n8;
+      counts[1] = r.n4;
+      counts[2] = r.n2;
+    }
+  });
+}
+
+int dq_sim_round(dq_ctx* ctx, const float* const* d_workers, size_t d, float* d_synced, int flags,
+                 dq_round_info* info, void* stream) {
+  return guarded([&] {
+    if (!ctx || !d_workers || !d_synced || !info) invalid("null argument");
+    DQ_CUDA(cudaSetDevice(ctx->device));
+    sim_round(ctx, d_workers, d, d_synced, flags, info, S(stream));
+  });
+}
+
+int dq_run_round_host(dq_ctx* ctx, const float* const* h_workers, size_t d, float* h_synced,
+                      dq_round_info* info, void* stream) {
+  return guarded([&] {
+    if (!ctx || !h_workers || !h_synced || !info) invalid("null argument");
+    DQ_CUDA(cudaSetDevice(ctx->device));
+    const uint32_t n = ctx->cfg.n_workers;
+    const size_t dp = (d + 63) / 64 * 64;
+    ctx->stage.reserve((n + 1) * dp);
+    std::vector<const float*> xs(n);
+    for (uint32_t r = 0; r < n; ++r) {
+      float* dst = ctx->stage.p + r * dp;
+      DQ_CUDA(cudaMemcpyAsync(dst, h_workers[r], d * sizeof(float), cudaMemcpyHostToDevice, S(stream)));
+      xs[r] = dst;
+    }
+    float* y = ctx->stage.p + n * dp;
+    sim_round(ctx, xs.data(), d, y, DQ_SIM_NO_METRICS, info, S(stream));
+    DQ_CUDA(cudaMemcpyAsync(h_synced, y, d * sizeof(float), cudaMemcpyDeviceToHost, S(stream)));
+    DQ_CUDA(cudaStreamSynchronize(S(stream)));
+  });
+}
+
+int dq_round_allocation(dq_ctx* ctx, uint8_t* h_widths, uint32_t* h_perm, size_t nsg) {
+  return guarded([&] {
+    if (!ctx) invalid("null context");
+    if (nsg != ctx->last_T) invalid("super-group count does not match the last round");
+    if (h_widths) DQ_CUDA(cudaMemcpy(h_widths, ctx->widths.p, nsg, cudaMemcpyDeviceToHost));
+    if (h_perm) DQ_CUDA(cudaMemcpy(h_perm, ctx->perm.p, nsg * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  });
+}
+
+int dq_allreduce(dq_ctx* ctx, const float* d_in, float* d_out, size_t d, dq_round_info* info, void* stream) {
+  return guarded([&] {
+    if (!ctx || !d_in || !d_out || !info) invalid("null argument");
+    DQ_CUDA(cudaSetDevice(ctx->device));
+    dist_round(ctx, d_in, d, d_out, info, S(stream));
+  });
+}
+
+int dq_profile_enable(dq_ctx* ctx, int on) {
+  return guarded([&] {
+    if (!ctx) invalid("null context");
+    ctx->profile = on;
+  });
+}
+
+int dq_profile_read(dq_ctx* ctx, dq_kernel_profile* out, int cap, int* count, int reset) {
+  return guarded([&] {
+    if (!ctx) invalid("null context");
+    int k = 0;
+    for (int i = 0; i < K_NKINDS; ++i) {
+      if (!ctx->prof_launches[i] && !ctx->prof_ms[i]) continue;
+      if (out && k < cap) {
+        dq_kernel_profile& p = out[k];
+        std::snprintf(p.name, sizeof p.name, "%s", kKindName[i]);
+        p.launches = ctx->prof_launches[i];
+        p.ms = ctx->prof_ms[i];
+        p.bytes = ctx->prof_bytes[i];
+      }
+      ++k;
+    }
+    if (count) *count = k;
+    if (reset)
+      for (int i = 0; i < K_NKINDS; ++i) ctx->prof_ms[i] = ctx->prof_bytes[i] = 0, ctx->prof_launches[i] = 0;
+  });
+}
+
+int dq_comm_unique_id(uint8_t out[128]) {
+  return guarded([&] {
+    ncclUniqueId id;
+    DQ_NCCL(ncclGetUniqueId(&id));
+    std::memcpy(out, id.internal, 128);
+  });
+}
+
+int dq_comm_init(dq_ctx* ctx, int rank, int nranks, const uint8_t id[128]) {
+  return guarded([&] {
+    if (!ctx) invalid("null context");
+    if (static_cast<uint32_t>(nranks) != ctx->cfg.n_workers) invalid("nranks must equal cfg.n_workers");
+    DQ_CUDA(cudaSetDevice(ctx->device));
+    ncclUniqueId uid;
+    std::memcpy(uid.internal, id, 128);
+    DQ_NCCL(ncclCommInitRank(&ctx->comm, nranks, uid, rank));
+    ctx->rank = rank;
+    ctx->nranks = nranks;
+  });
+}
+
+}  // extern "C"

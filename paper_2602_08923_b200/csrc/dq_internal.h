@@ -1,0 +1,80 @@
+// dq_internal.h — kernel launch interface shared by the .cu files and the
+// host engine (not part of the public C-ABI).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "dq_device.cuh"
+
+namespace dq {
+
+// Arguments of every codec kernel (passed by value in the param space).
+struct CodecArgs {
+  Layout L;                 // geometry of the chunk being processed
+  uint32_t first_sg;        // permuted index of the chunk's first super-group (RNG key, perm lookup)
+  const float* x;           // raw gradient, original order (gather source)
+  const uint32_t* perm;     // permuted position -> original super-group
+  const float* gmean;       // global super-group means, original order
+  uint64_t d;               // logical gradient length (zero padding beyond)
+  const float* acc_in;      // chunk-local fp32 operand [nsg * 256]
+  float* acc_out;           // chunk-local fp32 result, or the output gradient (decode OUT=1)
+  const uint8_t* in;        // incoming compressed chunk
+  uint8_t* out;             // outgoing compressed chunk
+  float n_workers_f;        // float(n) for denormalize
+  uint64_t h3_eq, h3_sc, h3_pm;  // keyed prefixes through the chunk word, per purpose
+  uint32_t slot, n_slots;
+  int correlated;
+  int uniform_books;
+};
+
+void launch_quant(const CodecArgs& a, int src, bool dar, cudaStream_t st);
+void launch_da(const CodecArgs& a, int src, cudaStream_t st);
+void launch_decode(const CodecArgs& a, int out_mode, cudaStream_t st);
+cudaError_t upload_codebooks(const float* books);
+
+// ------------------------------------------------------------ statistics
+// per-super-group fp64 sequential sum / sum of squares of `n_workers` gradients
+// (pointer array in device memory) -> mean[w * T + j], sq[w * T + j]
+void launch_stats(const float* const* xs, uint32_t n_workers, uint64_t d, uint32_t T, float* mean,
+                  float* sq, cudaStream_t st);
+// rank-ordered fp64 reduction of [n][T] stats -> global [T]
+void launch_reduce_stats(const float* mean, const float* sq, uint32_t n, uint32_t T, float* gmean,
+                         float* gsq, cudaStream_t st);
+
+// ------------------------------------------------------------ allocation
+struct AllocState {
+  uint64_t klo, khi;       // key range searched by the current pass (inclusive)
+  uint64_t below_w;        // total weight of flips with key < klo
+  uint64_t pred_key;       // largest flip key below klo (valid when has_pred)
+  uint64_t cross_key;      // key of the crossing flip (status 1)
+  uint64_t kmin, kmax;     // smallest / largest flip key
+  uint64_t wmax;           // largest cumulative flip weight within budget
+  uint32_t npos;           // super-groups with F > 0
+  uint32_t has_pred;
+  uint32_t status;         // 0 searching, 1 crossing found, 2 all flips fit, 3 no flips
+  uint32_t passes;
+};
+constexpr int kAllocBins = 1024;
+constexpr int kAllocMaxPasses = 8;
+struct AllocWork {           // device scratch owned by the context
+  double* level;             // alpha * log2(F_j) per super-group (NaN when F_j <= 0)
+  AllocState* state;
+  uint64_t* bins;            // [kAllocBins][4]: weight, count, min key, max key
+  uint32_t* blockcnt;        // [nblocks][4] class counts (8, 4, 2, -)
+  uint32_t* counts;          // [4]: n8, n4, n2, payload_units
+};
+uint32_t alloc_blocks(uint32_t T);
+// Search for the crossing flip (fully on device, no host sync).
+void launch_alloc_search(const float* F, uint32_t T, double alpha, uint64_t wmax, AllocWork w,
+                         cudaStream_t st);
+// Widths from the float thresholds + stable width-class partition (8,4,2).
+void launch_alloc_assign(const float* F, uint32_t T, float t24, float t48, AllocWork w,
+                         uint8_t* widths, uint32_t* perm, cudaStream_t st);
+void launch_fixed_assign(uint32_t T, int width, AllocWork w, uint8_t* widths, uint32_t* perm,
+                         cudaStream_t st);
+
+// vNMSE accumulators (simulation only): err += (y - sum_r x_r)^2, ref += (sum_r x_r)^2
+void launch_vnmse(const float* const* xs, uint32_t n, const float* y, uint64_t d, double* acc2,
+                  cudaStream_t st);
+
+}  // namespace dq

@@ -1,0 +1,425 @@
+// dq_stats_alloc.cu — super-group statistics and the fast bit allocator on device.
+//
+// Statistics (proj/src/stats.cpp:23-54): the reference sums every super-group
+// sequentially in fp64; fp64 addition is not associative, so the only way to be
+// bit-exact is to keep that order.  k_stats stages a 128-super-group x 32-entry
+// tile through shared memory with fully coalesced 128-byte row loads and lets
+// each thread run its super-group's sequential fp64 chain from the conflict-free
+// (stride 33) tile — HBM-bound, the fp64 adds are ~15% of the issue budget.
+//
+// Fast allocator (proj/src/allocation.cpp:170-260): payload(u) is a step
+// function whose steps sit at the flips 4 - a*log2(F_j) (width 2->4, +2 bits per
+// entry) and 8 - a*log2(F_j) (4->8, +4); the reference sorts all 2T flips and
+// bisects over plateau midpoints.  Here the crossing flip — the first flip, in
+// ascending order, at which the cumulative weight exceeds the budget — is
+// found with no sort: each pass histograms the flips of the current key range
+// into 1024 bins (order-preserving u64 keys of the doubles, so ranges are exact),
+// a one-CTA scan picks the bin where the weight crosses, and the next pass
+// narrows to that bin's [min, max] key.  <= 8 passes isolate a single flip value
+// (each pass removes >= 9 bits of key range); the plateau midpoint with its
+// predecessor is then u exactly as the reference computes it.
+#include <cfloat>
+#include <cstdint>
+
+#include "dq_internal.h"
+
+namespace dq {
+
+// ------------------------------------------------------------ statistics
+constexpr int kStatSG = 128;
+
+__global__ void __launch_bounds__(kStatSG) k_stats(const float* const* xs, uint64_t d, uint32_t T,
+                                                   float* mean, float* sq) {
+  __shared__ float tile[kStatSG][33];
+  const float* __restrict__ x = xs[blockIdx.y];
+  const uint32_t sg0 = blockIdx.x * kStatSG;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double s = 0.0, q = 0.0;
+#pragma unroll 1
+  for (int part = 0; part < kS / 32; ++part) {
+    float v[32];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      const uint32_t sg = sg0 + warp * 32 + r;
+      const uint64_t idx = static_cast<uint64_t>(sg) * kS + part * 32 + lane;
+      v[r] = (sg < T && idx < d) ? __ldcs(x + idx) : 0.0f;  // streaming: read once
+    }
+#pragma unroll
+    for (int r = 0; r < 32; ++r) tile[warp * 32 + r][lane] = v[r];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const double t = tile[threadIdx.x][k];
+      s = __dadd_rn(s, t);
+      q = __dadd_rn(q, __dmul_rn(t, t));
+    }
+    __syncthreads();
+  }
+  const uint32_t sg = sg0 + threadIdx.x;
+  if (sg < T) {
+    mean[static_cast<uint64_t>(blockIdx.y) * T + sg] = static_cast<float>(__ddiv_rn(s, static_cast<double>(kS)));
+    sq[static_cast<uint64_t>(blockIdx.y) * T + sg] = static_cast<float>(q);
+  }
+}
+
+void launch_stats(const float* const* xs, uint32_t n_workers, uint64_t d, uint32_t T, float* mean,
+                  float* sq, cudaStream_t st) {
+  if (T == 0) return;
+  k_stats<<<dim3((T + kStatSG - 1) / kStatSG, n_workers), kStatSG, 0, st>>>(xs, d, T, mean, sq);
+}
+
+__global__ void k_reduce_stats(const float* mean, const float* sq, uint32_t n, uint32_t T,
+                               float* gm, float* gs) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= T) return;
+  double a = 0.0, b = 0.0;
+  for (uint32_t r = 0; r < n; ++r) {
+    a = __dadd_rn(a, static_cast<double>(mean[static_cast<uint64_t>(r) * T + j]));
+    b = __dadd_rn(b, static_cast<double>(sq[static_cast<uint64_t>(r) * T + j]));
+  }
+  gm[j] = static_cast<float>(__ddiv_rn(a, static_cast<double>(n)));
+  gs[j] = static_cast<float>(b);
+}
+
+void launch_reduce_stats(const float* mean, const float* sq, uint32_t n, uint32_t T, float* gm,
+                         float* gs, cudaStream_t st) {
+  if (T == 0) return;
+  k_reduce_stats<<<(T + 255) / 256, 256, 0, st>>>(mean, sq, n, T, gm, gs);
+}
+
+// ------------------------------------------------------------ allocation
+__device__ __forceinline__ uint64_t dkey(double f) {
+  const uint64_t b = static_cast<uint64_t>(__double_as_longlong(f));
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__global__ void k_alloc_init(AllocState* s, uint64_t* bins, uint64_t wmax) {
+  const int t = threadIdx.x;
+  for (int b = t; b < kAllocBins; b += blockDim.x) {
+    bins[4 * b + 0] = 0;
+    bins[4 * b + 1] = 0;
+    bins[4 * b + 2] = ~0ull;
+    bins[4 * b + 3] = 0;
+  }
+  if (t == 0) {
+    *s = AllocState{};
+    s->kmin = ~0ull;
+    s->kmax = 0;
+    s->wmax = wmax;
+  }
+}
+
+__global__ void k_alloc_prep(const float* __restrict__ F, uint32_t T, double alpha, double* level,
+                             AllocState* s) {
+  uint64_t kmin = ~0ull, kmax = 0;
+  uint32_t npos = 0;
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < T; j += gridDim.x * blockDim.x) {
+    const float f = F[j];
+    double l = __longlong_as_double(0x7ff8000000000000ll);  // NaN: no flips (allocation.cpp:206)
+    if (f > 0.0f) {
+      l = __dmul_rn(alpha, log2(static_cast<double>(f)));
+      kmin = min(kmin, dkey(__dsub_rn(4.0, l)));
+      kmax = max(kmax, dkey(__dsub_rn(8.0, l)));
+      ++npos;
+    }
+    level[j] = l;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+    kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    npos += __shfl_xor_sync(0xffffffffu, npos, o);
+  }
+  if ((threadIdx.x & 31) == 0 && npos) {
+    atomicMin(reinterpret_cast<unsigned long long*>(&s->kmin), kmin);
+    atomicMax(reinterpret_cast<unsigned long long*>(&s->kmax), kmax);
+    atomicAdd(&s->npos, npos);
+  }
+}
+
+__global__ void k_alloc_start(AllocState* s) {
+  if (s->npos == 0) {
+    s->status = 3;
+  } else {
+    s->klo = s->kmin;
+    s->khi = s->kmax;
+  }
+}
+
+__global__ void __launch_bounds__(512) k_alloc_hist(const double* __restrict__ level, uint32_t T,
+                                                   const AllocState* s, uint64_t* bins) {
+  if (s->status != 0) return;
+  __shared__ uint32_t bw[kAllocBins], bc[kAllocBins];
+  __shared__ unsigned long long bmn[kAllocBins], bmx[kAllocBins];
+  for (int b = threadIdx.x; b < kAllocBins; b += blockDim.x) {
+    bw[b] = 0;
+    bc[b] = 0;
+    bmn[b] = ~0ull;
+    bmx[b] = 0;
+  }
+  __syncthreads();
+  const uint64_t klo = s->klo, span = s->khi - s->klo;
+  const int bits = span ? 64 - __clzll(static_cast<long long>(span)) : 0;
+  const int shift = bits > 10 ? bits - 10 : 0;
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < T; j += gridDim.x * blockDim.x) {
+    const double l = level[j];
+    if (l != l) continue;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const uint64_t k = dkey(__dsub_rn(t ? 8.0 : 4.0, l));
+      if (k - klo <= span) {  // unsigned: k in [klo, khi]
+        const uint32_t b = static_cast<uint32_t>((k - klo) >> shift);
+        atomicAdd(&bw[b], t ? 4u : 2u);
+        atomicAdd(&bc[b], 1u);
+        atomicMin(&bmn[b], static_cast<unsigned long long>(k));
+        atomicMax(&bmx[b], static_cast<unsigned long long>(k));
+      }
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < kAllocBins; b += blockDim.x) {
+    if (bc[b] == 0) continue;
+    unsigned long long* g = reinterpret_cast<unsigned long long*>(bins + 4 * b);
+    atomicAdd(g + 0, static_cast<unsigned long long>(bw[b]));
+    atomicAdd(g + 1, static_cast<unsigned long long>(bc[b]));
+    atomicMin(g + 2, bmn[b]);
+    atomicMax(g + 3, bmx[b]);
+  }
+}
+
+__global__ void __launch_bounds__(kAllocBins) k_alloc_scan(AllocState* s, uint64_t* bins) {
+  __shared__ uint64_t wsum[32];
+  __shared__ uint32_t cross_bin;
+  __shared__ unsigned long long pred_max;
+  if (s->status != 0) return;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const uint64_t w = bins[4 * t], c = bins[4 * t + 1], mn = bins[4 * t + 2], mx = bins[4 * t + 3];
+  bins[4 * t] = 0;
+  bins[4 * t + 1] = 0;
+  bins[4 * t + 2] = ~0ull;
+  bins[4 * t + 3] = 0;
+  if (t == 0) {
+    cross_bin = 0xffffffffu;
+    pred_max = 0;
+  }
+  // block inclusive scan of the bin weights
+  uint64_t incl = w;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    uint64_t v = wsum[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t u = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += u;
+    }
+    wsum[lane] = v - wsum[lane];  // exclusive per warp
+  }
+  __syncthreads();
+  incl += wsum[warp];
+  const uint64_t below = s->below_w, wmax = s->wmax;
+  if (w > 0 && below + incl > wmax && below + incl - w <= wmax) cross_bin = t;
+  __syncthreads();
+  const uint32_t cb = cross_bin;
+  if (cb != 0xffffffffu && static_cast<uint32_t>(t) < cb && c > 0) atomicMax(&pred_max, static_cast<unsigned long long>(mx));
+  __syncthreads();
+  if (static_cast<uint32_t>(t) == cb) {
+    s->below_w = below + incl - w;
+    if (pred_max != 0 || (s->has_pred == 0 && false)) {
+    }
+    if (pred_max != 0) {
+      s->pred_key = s->has_pred ? max(s->pred_key, static_cast<uint64_t>(pred_max)) : pred_max;
+      s->has_pred = 1;
+    }
+    if (mn == mx) {
+      s->status = 1;
+      s->cross_key = mn;
+    } else {
+      s->klo = mn;
+      s->khi = mx;
+    }
+    s->passes += 1;
+  }
+  if (t == 0 && cb == 0xffffffffu) s->status = s->passes == 0 ? 2 : 4;  // 4: internal error
+}
+
+uint32_t alloc_blocks(uint32_t T) { return (T + 2047) / 2048; }
+
+void launch_alloc_search(const float* F, uint32_t T, double alpha, uint64_t wmax, AllocWork w,
+                         cudaStream_t st) {
+  k_alloc_init<<<1, 256, 0, st>>>(w.state, w.bins, wmax);
+  const uint32_t grid = T ? (T + 511) / 512 < 1184 ? (T + 511) / 512 : 1184 : 1;
+  k_alloc_prep<<<grid, 512, 0, st>>>(F, T, alpha, w.level, w.state);
+  k_alloc_start<<<1, 1, 0, st>>>(w.state);
+  const uint32_t hgrid = T ? ((T + 4095) / 4096 < 296 ? (T + 4095) / 4096 : 296) : 1;
+  for (int p = 0; p < kAllocMaxPasses; ++p) {
+    k_alloc_hist<<<hgrid, 512, 0, st>>>(w.level, T, w.state, w.bins);
+    k_alloc_scan<<<1, kAllocBins, 0, st>>>(w.state, w.bins);
+  }
+}
+
+// ---------------------------------------------------- width assignment
+// widths (proj/src/allocation.cpp:186-199) and the stable 8,4,2 partition
+// (allocation.cpp:302-310).  Block b owns super-groups [2048 b, 2048 b + 2048),
+// thread t the 8 consecutive ones starting at 2048 b + 8 t.
+__device__ __forceinline__ int cls_of(float f, float t24, float t48) {
+  return f >= t48 ? 0 : (f >= t24 ? 1 : 2);
+}
+
+__device__ __forceinline__ uint64_t block_excl_scan_u64(uint64_t v, uint64_t* tot) {
+  __shared__ uint64_t ws[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += u;
+  }
+  if (lane == 31) ws[warp] = incl;
+  __syncthreads();
+  uint64_t off = 0, all = 0;
+  for (int k = 0; k < 8; ++k) {
+    if (k < warp) off += ws[k];
+    all += ws[k];
+  }
+  __syncthreads();
+  *tot = all;
+  return off + incl - v;
+}
+
+template <bool FIXED>
+__global__ void __launch_bounds__(256) k_assign_count(const float* __restrict__ F, uint32_t T, float t24,
+                                                      float t48, int fixed_cls, uint8_t* widths,
+                                                      uint32_t* blockcnt) {
+  const uint32_t j0 = blockIdx.x * 2048 + threadIdx.x * 8;
+  uint64_t packed = 0;  // 16-bit counts per class
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t j = j0 + k;
+    if (j >= T) break;
+    const int c = FIXED ? fixed_cls : cls_of(F[j], t24, t48);
+    widths[j] = static_cast<uint8_t>(c == 0 ? 8 : (c == 1 ? 4 : 2));
+    packed += 1ull << (16 * c);
+  }
+  uint64_t tot;
+  block_excl_scan_u64(packed, &tot);
+  if (threadIdx.x == 0) {
+    blockcnt[4 * blockIdx.x + 0] = static_cast<uint32_t>(tot & 0xffff);
+    blockcnt[4 * blockIdx.x + 1] = static_cast<uint32_t>((tot >> 16) & 0xffff);
+    blockcnt[4 * blockIdx.x + 2] = static_cast<uint32_t>((tot >> 32) & 0xffff);
+  }
+}
+
+// exclusive scan of the per-block class counts (one CTA), totals -> counts[0..2]
+__global__ void __launch_bounds__(1024) k_assign_scan(uint32_t nb, uint32_t* blockcnt, uint32_t* counts) {
+  __shared__ uint64_t carry[3];
+  if (threadIdx.x < 3) carry[threadIdx.x] = 0;
+  __syncthreads();
+  for (uint32_t base = 0; base < nb; base += blockDim.x) {
+    const uint32_t b = base + threadIdx.x;
+    uint64_t v[3];
+    for (int c = 0; c < 3; ++c) v[c] = b < nb ? blockcnt[4 * b + c] : 0;
+    for (int c = 0; c < 3; ++c) {
+      // block-wide exclusive scan (1024 threads = 32 warps)
+      __shared__ uint64_t ws[32];
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      uint64_t incl = v[c];
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+      }
+      if (lane == 31) ws[warp] = incl;
+      __syncthreads();
+      uint64_t off = 0, all = 0;
+      for (int k = 0; k < 32; ++k) {
+        if (k < warp) off += ws[k];
+        all += ws[k];
+      }
+      if (b < nb) blockcnt[4 * b + c] = static_cast<uint32_t>(carry[c] + off + incl - v[c]);
+      __syncthreads();
+      if (threadIdx.x == 0) carry[c] += all;
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x == 0) {
+    counts[0] = static_cast<uint32_t>(carry[0]);
+    counts[1] = static_cast<uint32_t>(carry[1]);
+    counts[2] = static_cast<uint32_t>(carry[2]);
+  }
+}
+
+template <bool FIXED>
+__global__ void __launch_bounds__(256) k_assign_scatter(const float* __restrict__ F, uint32_t T, float t24,
+                                                        float t48, int fixed_cls, const uint32_t* blockcnt,
+                                                        const uint32_t* counts, uint32_t* perm) {
+  const uint32_t j0 = blockIdx.x * 2048 + threadIdx.x * 8;
+  int cls[8];
+  uint64_t packed = 0;
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t j = j0 + k;
+    cls[k] = j < T ? (FIXED ? fixed_cls : cls_of(F[j], t24, t48)) : 3;
+    if (cls[k] < 3) packed += 1ull << (16 * cls[k]);
+  }
+  uint64_t tot;
+  const uint64_t excl = block_excl_scan_u64(packed, &tot);
+  uint32_t pos[3];
+  const uint32_t base[3] = {0, counts[0], counts[0] + counts[1]};
+  for (int c = 0; c < 3; ++c)
+    pos[c] = base[c] + blockcnt[4 * blockIdx.x + c] + static_cast<uint32_t>((excl >> (16 * c)) & 0xffff);
+  for (int k = 0; k < 8; ++k)
+    if (cls[k] < 3) perm[pos[cls[k]]++] = j0 + k;
+}
+
+static void assign_impl(const float* F, uint32_t T, float t24, float t48, int fixed_cls, bool fixed,
+                        AllocWork w, uint8_t* widths, uint32_t* perm, cudaStream_t st) {
+  const uint32_t nb = alloc_blocks(T);
+  if (nb == 0) return;
+  if (fixed) k_assign_count<true><<<nb, 256, 0, st>>>(F, T, t24, t48, fixed_cls, widths, w.blockcnt);
+  else k_assign_count<false><<<nb, 256, 0, st>>>(F, T, t24, t48, fixed_cls, widths, w.blockcnt);
+  k_assign_scan<<<1, 1024, 0, st>>>(nb, w.blockcnt, w.counts);
+  if (fixed) k_assign_scatter<true><<<nb, 256, 0, st>>>(F, T, t24, t48, fixed_cls, w.blockcnt, w.counts, perm);
+  else k_assign_scatter<false><<<nb, 256, 0, st>>>(F, T, t24, t48, fixed_cls, w.blockcnt, w.counts, perm);
+}
+
+void launch_alloc_assign(const float* F, uint32_t T, float t24, float t48, AllocWork w, uint8_t* widths,
+                         uint32_t* perm, cudaStream_t st) {
+  assign_impl(F, T, t24, t48, 0, false, w, widths, perm, st);
+}
+
+void launch_fixed_assign(uint32_t T, int width, AllocWork w, uint8_t* widths, uint32_t* perm,
+                         cudaStream_t st) {
+  assign_impl(nullptr, T, 0.f, 0.f, width == 8 ? 0 : (width == 4 ? 1 : 2), true, w, widths, perm, st);
+}
+
+// ------------------------------------------------------------------ vNMSE
+__global__ void k_vnmse(const float* const* xs, uint32_t n, const float* y, uint64_t d, double* acc) {
+  double err = 0.0, ref = 0.0;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < d;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    double e = 0.0;
+    for (uint32_t r = 0; r < n; ++r) e += static_cast<double>(xs[r][i]);
+    const double diff = static_cast<double>(y[i]) - e;
+    err += diff * diff;
+    ref += e * e;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    err += __shfl_xor_sync(0xffffffffu, err, o);
+    ref += __shfl_xor_sync(0xffffffffu, ref, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(acc, err);
+    atomicAdd(acc + 1, ref);
+  }
+}
+
+void launch_vnmse(const float* const* xs, uint32_t n, const float* y, uint64_t d, double* acc2,
+                  cudaStream_t st) {
+  k_vnmse<<<148 * 4, 256, 0, st>>>(xs, n, y, d, acc2);
+}
+
+}  // namespace dq

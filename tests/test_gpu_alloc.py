@@ -1,0 +1,80 @@
+"""Parity of the statistics and fast-allocation kernels with the oracle.
+
+Cases follow proj/tests/test_stats.cpp and test_allocation.cpp: sequential fp64
+stats, rank-ordered reduction, allocation boundary ties, no positive norms,
+every flip within budget, infeasible budgets.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def dq():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2602_08923_b200 as dq
+    return dq
+
+
+@pytest.mark.parametrize("d", [256, 1000, 1 << 16, (1 << 16) + 3])
+def test_stats_match(dq, port, d):
+    rng = np.random.default_rng(d)
+    x = (rng.standard_normal(d) * np.exp(3 * rng.standard_normal(d))).astype(np.float32)
+    m, q = dq.compute_stats(torch.from_numpy(x).cuda())
+    mo, qo = port.compute_stats(x)
+    assert np.array_equal(m.cpu().numpy().view(np.uint32), mo.view(np.uint32))
+    assert np.array_equal(q.cpu().numpy().view(np.uint32), qo.view(np.uint32))
+
+
+def test_reduce_stats_match(dq, port):
+    rng = np.random.default_rng(1)
+    means = rng.standard_normal((5, 3000)).astype(np.float32)
+    sqs = np.abs(rng.standard_normal((5, 3000)) * 1e3).astype(np.float32)
+    gm, gs = dq.reduce_stats(torch.from_numpy(means).cuda(), torch.from_numpy(sqs).cuda())
+    om, os_ = port.reduce_stats(means, sqs)
+    assert np.array_equal(gm.cpu().numpy().view(np.uint32), om.view(np.uint32))
+    assert np.array_equal(gs.cpu().numpy().view(np.uint32), os_.view(np.uint32))
+
+
+def _F_cases():
+    rng = np.random.default_rng(7)
+    yield "lognormal", np.exp(8 * rng.standard_normal(50000)).astype(np.float32)
+    yield "normal_sq", (rng.standard_normal(20000) ** 2 * 256).astype(np.float32)
+    f = np.exp(4 * rng.standard_normal(10000)).astype(np.float32)
+    f[::7] = 0.0
+    yield "with_zeros", f
+    yield "all_zero", np.zeros(1000, np.float32)
+    yield "constant", np.full(4096, 3.0, np.float32)
+    yield "two_levels", np.repeat(np.array([1.0, 1000.0], np.float32), 3000)
+    yield "single", np.array([5.0], np.float32)
+    yield "tiny", np.array([1e-30, 2e-30, 1e-20], np.float32)
+    yield "ratio_ties", np.array([17.0, 512.0, 17.0 * 512 / 17, 1.0, 512 / 17], np.float32)
+    g = np.exp(2 * rng.standard_normal(3000)).astype(np.float32)
+    yield "dupes", np.concatenate([g, g, g])
+
+
+@pytest.mark.parametrize("b", [2.6, 3, 4, 5, 6, 8, 12])
+@pytest.mark.parametrize("name,F", list(_F_cases()), ids=[c[0] for c in _F_cases()])
+def test_allocate_fast_matches(dq, port, name, F, b):
+    from oracle.oracle import OracleError
+    try:
+        w, p, u, pay = port.allocate_fast(F, b)
+    except OracleError as e:
+        assert e.code == 3
+        with pytest.raises(dq.InfeasibleBudget):
+            dq.allocate_fast(torch.from_numpy(F).cuda(), b)
+        return
+    got = dq.allocate_fast(torch.from_numpy(F).cuda(), b)
+    assert np.array_equal(got.widths.cpu().numpy(), w)
+    assert np.array_equal(got.permutation.cpu().numpy().astype(np.uint32), p)
+    assert got.u == u
+    assert got.payload_bits == pay
+
+
+def test_allocate_infeasible(dq):
+    with pytest.raises(dq.InfeasibleBudget):
+        dq.allocate_fast(torch.ones(100, device="cuda"), 2.0)
