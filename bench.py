@@ -44,7 +44,7 @@ UNIT = "GB/s"
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--d", type=int, default=0, help="entries per worker (default 2^26 at N=1, 2^28 at N>1)")
@@ -80,10 +80,14 @@ class Clocks:
                  "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 10:  # sampler is live before timing starts
+                time.sleep(0.02)
+            self.rows.clear()
         except Exception:
             self.proc = None
         return self
@@ -93,6 +97,7 @@ class Clocks:
             self.rows.append([x.strip() for x in line.split(",")])
 
     def __exit__(self, *a):
+        time.sleep(0.06)  # one more sample covering the end of the timed region
         if self.proc:
             self.proc.terminate()
             try:

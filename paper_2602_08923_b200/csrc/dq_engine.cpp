@@ -215,7 +215,7 @@ cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 enum Kind { K_STATS, K_REDUCE, K_ALLOC_SEARCH, K_ALLOC_ASSIGN, K_LEAF, K_DAR, K_DA, K_DECODE, K_NCCL, K_NKINDS };
 const char* const kKindName[K_NKINDS] = {"stats", "reduce_stats", "alloc_search", "alloc_assign", "quant_leaf",
                                          "quant_dar", "decompress_accumulate", "decode_out", "nccl"};
-const int kKindLaunches[K_NKINDS] = {1, 1, 3 + 2 * kAllocMaxPasses, 3, 1, 1, 1, 1, 0};
+const int kKindLaunches[K_NKINDS] = {1, 1, 4 + 2 * kAllocMaxPasses, 3, 1, 1, 1, 1, 0};
 
 cudaEvent_t pool_event(dq_ctx* ctx) {
   if (!ctx->ev_pool.empty()) {
@@ -339,13 +339,21 @@ AllocResult allocate(dq_ctx* ctx, const dq_config& c, const float* dF, uint32_t 
   DQ_CUDA(cudaMemcpyAsync(ctx->h_state, w.state, sizeof(AllocState), cudaMemcpyDeviceToHost, st));
   DQ_CUDA(cudaStreamSynchronize(st));
   const AllocState s = *ctx->h_state;
+  // the flips adjacent to the chosen plateau, recomputed with the host libm exactly as
+  // fast_sample_points does (allocation.cpp:201-224)
+  auto flip = [](uint32_t fbits, uint32_t type) {
+    float f;
+    std::memcpy(&f, &fbits, 4);
+    const double l = kAlpha * std::log2(static_cast<double>(f));
+    return (type ? 8.0 : 4.0) - l;
+  };
   double u;
   switch (s.status) {
     case 3: u = 0.0; break;                                  // no positive F (allocation.cpp:212-215)
-    case 2: u = key_to_double(s.kmax) + 1.0; break;          // every flip fits: flips.back() + 1
+    case 2: u = flip(s.max_f, 1) + 1.0; break;               // every flip fits: flips.back() + 1
     case 1:
-      u = s.has_pred ? 0.5 * (key_to_double(s.pred_key) + key_to_double(s.cross_key))
-                     : key_to_double(s.cross_key) - 1.0;     // plateau midpoint / flips.front() - 1
+      u = s.has_pred ? 0.5 * (flip(s.pred_f, s.pred_t) + flip(s.cross_f, s.cross_t))
+                     : flip(s.cross_f, s.cross_t) - 1.0;     // plateau midpoint / flips.front() - 1
       break;
     default: throw Error(DQ_ECUDA, "allocation search did not converge (status " + std::to_string(s.status) + ")");
   }

@@ -53,6 +53,9 @@ struct AllocState {
   uint32_t has_pred;
   uint32_t status;         // 0 searching, 1 crossing found, 2 all flips fit, 3 no flips
   uint32_t passes;
+  // F (float bits) and flip type (0: 4 - a log2 F, 1: 8 - a log2 F) of the crossing,
+  // predecessor and largest flips, so the host recomputes them with the reference's libm
+  uint32_t cross_f, cross_t, pred_f, pred_t, max_f, pad_;
 };
 constexpr int kAllocBins = 1024;
 constexpr int kAllocMaxPasses = 8;

@@ -230,8 +230,6 @@ __global__ void __launch_bounds__(kAllocBins) k_alloc_scan(AllocState* s, uint64
   __syncthreads();
   if (static_cast<uint32_t>(t) == cb) {
     s->below_w = below + incl - w;
-    if (pred_max != 0 || (s->has_pred == 0 && false)) {
-    }
     if (pred_max != 0) {
       s->pred_key = s->has_pred ? max(s->pred_key, static_cast<uint64_t>(pred_max)) : pred_max;
       s->has_pred = 1;
@@ -248,6 +246,27 @@ __global__ void __launch_bounds__(kAllocBins) k_alloc_scan(AllocState* s, uint64
   if (t == 0 && cb == 0xffffffffu) s->status = s->passes == 0 ? 2 : 4;  // 4: internal error
 }
 
+// Find an F_j behind each flip key the host needs (crossing, predecessor, largest).
+__global__ void k_alloc_identify(const double* __restrict__ level, const float* __restrict__ F, uint32_t T,
+                                 AllocState* s) {
+  const uint32_t status = s->status;
+  if (status != 1 && status != 2) return;
+  const uint64_t ck = s->cross_key, pk = s->pred_key, mk = s->kmax;
+  const bool has_pred = s->has_pred;
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < T; j += gridDim.x * blockDim.x) {
+    const double l = level[j];
+    if (l != l) continue;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const uint64_t k = dkey(__dsub_rn(t ? 8.0 : 4.0, l));
+      const uint32_t fb = __float_as_uint(F[j]);
+      if (status == 1 && k == ck) { atomicExch(&s->cross_f, fb); atomicExch(&s->cross_t, t); }
+      if (status == 1 && has_pred && k == pk) { atomicExch(&s->pred_f, fb); atomicExch(&s->pred_t, t); }
+      if (status == 2 && t == 1 && k == mk) atomicExch(&s->max_f, fb);
+    }
+  }
+}
+
 uint32_t alloc_blocks(uint32_t T) { return (T + 2047) / 2048; }
 
 void launch_alloc_search(const float* F, uint32_t T, double alpha, uint64_t wmax, AllocWork w,
@@ -261,6 +280,7 @@ void launch_alloc_search(const float* F, uint32_t T, double alpha, uint64_t wmax
     k_alloc_hist<<<hgrid, 512, 0, st>>>(w.level, T, w.state, w.bins);
     k_alloc_scan<<<1, kAllocBins, 0, st>>>(w.state, w.bins);
   }
+  k_alloc_identify<<<grid, 512, 0, st>>>(w.level, F, T, w.state);
 }
 
 // ---------------------------------------------------- width assignment
