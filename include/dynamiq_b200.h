@@ -167,6 +167,11 @@ typedef struct dq_kernel_profile {
 int dq_profile_enable(dq_ctx* ctx, int on);
 int dq_profile_read(dq_ctx* ctx, dq_kernel_profile* out, int cap, int* count, int reset);
 
+/* Device self-checks of internal arithmetic (tests only): which = 0 compares
+ * the shared-reciprocal division with IEEE div.rn on n hashed pairs; which = 1
+ * compares the O(1) codebook bracket with binary search.  *mismatches = count. */
+int dq_selftest(int which, uint64_t n, uint64_t seed, uint64_t* mismatches);
+
 /* Multi-GPU: one process per GPU.  Rank 0 creates the id, the caller ships the
  * 128 bytes to every rank (e.g. torch.distributed), every rank joins. */
 int dq_comm_unique_id(uint8_t out[128]);

@@ -97,6 +97,7 @@ SIGNATURES = {
     "dq_sim_round": (C.c_int, [_V, _P(_V), C.c_size_t, _V, C.c_int, _P(RoundInfo), _V]),
     "dq_run_round_host": (C.c_int, [_V, _P(_V), C.c_size_t, _V, _P(RoundInfo), _V]),
     "dq_round_allocation": (C.c_int, [_V, _u8p, _u32p, C.c_size_t]),
+    "dq_selftest": (C.c_int, [C.c_int, C.c_uint64, C.c_uint64, _P(C.c_uint64)]),
     "dq_profile_enable": (C.c_int, [_V, C.c_int]),
     "dq_profile_read": (C.c_int, [_V, _P(KernelProfile), C.c_int, _P(C.c_int), C.c_int]),
     "dq_comm_unique_id": (C.c_int, [_u8p]),

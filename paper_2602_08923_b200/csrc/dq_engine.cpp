@@ -393,6 +393,10 @@ CodecArgs base_args(const dq_config& c, uint32_t chunk) {
   a.h3_pm = absorb(purpose_prefix(c.seed, c.round, kPermutation), chunk);
   a.correlated = c.correlated;
   a.uniform_books = c.non_uniform ? 0 : 1;
+  // width-8 index estimate: q[r] = (B^r - 1) / (B^127 - 1), B = 1 + 2 eps^2 (codebook.cpp:20-48)
+  const double B = 1.0 + 2.0 * 0.05 * 0.05;
+  a.est_c1 = c.non_uniform ? static_cast<float>(std::pow(B, 127) - 1.0) : 0.0f;
+  a.est_c2 = c.non_uniform ? static_cast<float>(1.0 / std::log2(B)) : 127.0f;
   a.n_workers_f = static_cast<float>(c.n_workers);
   return a;
 }
@@ -1086,6 +1090,25 @@ int dq_allreduce(dq_ctx* ctx, const float* d_in, float* d_out, size_t d, dq_roun
     if (!ctx || !d_in || !d_out || !info) invalid("null argument");
     DQ_CUDA(cudaSetDevice(ctx->device));
     dist_round(ctx, d_in, d, d_out, info, S(stream));
+  });
+}
+
+int dq_selftest(int which, uint64_t n, uint64_t seed, uint64_t* mismatches) {
+  return guarded([&] {
+    if (!mismatches) invalid("null argument");
+    ensure_books();
+    dq_config c;
+    dq_config_default(&c);
+    const CodecArgs a = base_args(c, 0);
+    unsigned long long* d = nullptr;
+    DQ_CUDA(cudaMalloc(&d, sizeof(*d)));
+    DQ_CUDA(cudaMemset(d, 0, sizeof(*d)));
+    launch_selftest(which, n, seed, d, a.est_c1, a.est_c2, nullptr);
+    DQ_CUDA(cudaGetLastError());
+    unsigned long long h = 0;
+    DQ_CUDA(cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost));
+    DQ_CUDA(cudaFree(d));
+    *mismatches = h;
   });
 }
 

@@ -25,12 +25,15 @@ struct CodecArgs {
   uint32_t slot, n_slots;
   int correlated;
   int uniform_books;
+  float est_c1, est_c2;     // width-8 codebook index estimator (see bracket())
 };
 
 void launch_quant(const CodecArgs& a, int src, bool dar, cudaStream_t st);
 void launch_da(const CodecArgs& a, int src, cudaStream_t st);
 void launch_decode(const CodecArgs& a, int out_mode, cudaStream_t st);
 cudaError_t upload_codebooks(const float* books);
+void launch_selftest(int which, uint64_t n, uint64_t seed, unsigned long long* bad, float c1, float c2,
+                     cudaStream_t st);
 
 // ------------------------------------------------------------ statistics
 // per-super-group fp64 sequential sum / sum of squares of `n_workers` gradients
