@@ -192,6 +192,9 @@ struct dq_ctx {
   // distributed
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1;
+  cudaStream_t cs = nullptr;            // communication stream (NCCL p2p)
+  std::vector<cudaEvent_t> pipe_ev;     // per (hop, piece) handshakes compute <-> comm
+  int pieces = 4;                       // pipeline pieces per chunk
   ~dq_ctx() {
     if (h_state) cudaFreeHost(h_state);
     if (h_counts) cudaFreeHost(h_counts);
@@ -199,6 +202,8 @@ struct dq_ctx {
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (comm) ncclCommDestroy(comm);
+    if (cs) cudaStreamDestroy(cs);
+    for (cudaEvent_t e : pipe_ev) cudaEventDestroy(e);
     for (auto& p : pending) {
       cudaEventDestroy(p.a);
       cudaEventDestroy(p.b);
@@ -650,6 +655,106 @@ void sim_round(dq_ctx* ctx, const float* const* xs, size_t d, float* out, int fl
 // parent, incoming = held (last parent), DA'd (earlier parents) or, at the
 // chunk's sink, fused DAR at the sink slot.  The all-gather forwards the sink
 // bytes verbatim (engine.cpp:219-229) as one group of n-1 sends and receives.
+// Ring reduce-scatter with per-piece software pipelining (tile-aligned pieces of
+// each chunk): at hop h rank r DARs chunk r-1-h piece by piece on the compute
+// stream, and the comm stream ships each finished piece to r+1 while receiving
+// the same piece of the next hop's chunk from r-1, so NVLink transfers overlap
+// the fused kernels.  Returns the device pointer of this rank's sink chunk.
+struct Piece {
+  uint32_t sg0, sg1;     // super-group range (chunk-local, tile aligned)
+  uint64_t b0, b1;       // byte range in the chunk layout
+};
+std::vector<Piece> split_pieces(const Layout& L, int want) {
+  std::vector<Piece> v;
+  const uint32_t tiles = L.tiles();
+  const uint32_t per = tiles == 0 ? 1 : (tiles + want - 1) / want;
+  for (uint32_t t = 0; t < tiles; t += per) {
+    const uint32_t t1 = t + per < tiles ? t + per : tiles;
+    const uint32_t s0 = t * kTileSG, s1 = t1 * kTileSG < L.nsg ? t1 * kTileSG : L.nsg;
+    v.push_back({s0, s1, L.tile_offset(t), L.tile_offset(t1)});
+  }
+  if (v.empty()) v.push_back({0, 0, 0, 0});
+  return v;
+}
+
+// A piece as a standalone chunk: its own run lengths, first_sg and base pointers.
+CodecArgs piece_args(const CodecArgs& base, const Layout& L, const Piece& p) {
+  CodecArgs a = base;
+  auto overlap = [](uint32_t a0, uint32_t a1, uint32_t b0, uint32_t b1) {
+    const uint32_t l = a0 > b0 ? a0 : b0, h = a1 < b1 ? a1 : b1;
+    return h > l ? h - l : 0u;
+  };
+  a.L.nsg = p.sg1 - p.sg0;
+  a.L.n8 = overlap(p.sg0, p.sg1, 0, L.n8);
+  a.L.n4 = overlap(p.sg0, p.sg1, L.n8, L.n8 + L.n4);
+  a.first_sg = base.first_sg + p.sg0;
+  return a;
+}
+
+uint8_t* ring_pipelined(dq_ctx* ctx, const Prepared& pr, const std::vector<CodecArgs>& bases,
+                        const std::vector<Layout>& lays, size_t mb, dq_round_info* info, cudaStream_t st) {
+  const uint32_t n = ctx->cfg.n_workers, me = static_cast<uint32_t>(ctx->rank);
+  const uint32_t right = (me + 1) % n, left = (me + n - 1) % n;
+  if (!ctx->cs) DQ_CUDA(cudaStreamCreateWithFlags(&ctx->cs, cudaStreamNonBlocking));
+  const int P = ctx->pieces;
+  const size_t nev = 2ull * n * P + 2;
+  while (ctx->pipe_ev.size() < nev) {
+    cudaEvent_t e;
+    DQ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->pipe_ev.push_back(e);
+  }
+  // buffers: out[2] (hop parity), in[2], sink
+  auto obuf = [&](uint32_t h) { return ctx->msgs.p + static_cast<size_t>(h & 1) * mb; };
+  auto ibuf = [&](uint32_t h) { return ctx->msgs.p + static_cast<size_t>(2 + (h & 1)) * mb; };
+  uint8_t* sink = ctx->msgs.p + 4ull * mb;
+  auto ev_comp = [&](uint32_t h, int p) { return ctx->pipe_ev[(static_cast<size_t>(h) * P + p) * 2]; };
+  auto ev_recv = [&](uint32_t h, int p) { return ctx->pipe_ev[(static_cast<size_t>(h) * P + p) * 2 + 1]; };
+  cudaEvent_t start = ctx->pipe_ev[nev - 1];
+  DQ_CUDA(cudaEventRecord(start, st));
+  DQ_CUDA(cudaStreamWaitEvent(ctx->cs, start, 0));  // comm work of this round follows its prologue
+  for (uint32_t h = 0; h < n; ++h) {
+    const uint32_t ch = (me + 2 * n - 1 - h) % n;  // chunk handled at hop h (sink at h = n-1)
+    const Layout& L = lays[ch];
+    const std::vector<Piece> pcs = split_pieces(L, P);
+    for (int p = 0; p < static_cast<int>(pcs.size()); ++p) {
+      CodecArgs a = piece_args(bases[ch], L, pcs[p]);
+      a.slot = h;
+      a.out = (h + 1 < n ? obuf(h) : sink) + pcs[p].b0;
+      if (h > 0) {
+        DQ_CUDA(cudaStreamWaitEvent(st, ev_recv(h, p), 0));
+        a.in = ibuf(h) + pcs[p].b0;
+      }
+      const bool dar = h > 0;
+      timed(ctx, dar ? K_DAR : K_LEAF, quant_bytes(a.L, dar), st, [&] { launch_quant(a, 0, dar, st); });
+      DQ_CUDA(cudaEventRecord(ev_comp(h, p), st));
+      if (h + 1 < n) {
+        // ship piece p of this hop's result; receive piece p of the next hop's chunk
+        const uint32_t nch = (me + 2 * n - 2 - h) % n;
+        const std::vector<Piece> npcs = split_pieces(lays[nch], P);
+        DQ_CUDA(cudaStreamWaitEvent(ctx->cs, ev_comp(h, p), 0));
+        DQ_NCCL(ncclGroupStart());
+        DQ_NCCL(ncclSend(obuf(h) + pcs[p].b0, pcs[p].b1 - pcs[p].b0, ncclUint8, right, ctx->comm, ctx->cs));
+        if (p < static_cast<int>(npcs.size()))
+          DQ_NCCL(ncclRecv(ibuf(h + 1) + npcs[p].b0, npcs[p].b1 - npcs[p].b0, ncclUint8, left, ctx->comm, ctx->cs));
+        DQ_NCCL(ncclGroupEnd());
+        DQ_CUDA(cudaEventRecord(ev_recv(h + 1, p), ctx->cs));
+        // piece counts of consecutive chunks may differ: receive the tail pieces here
+        if (p + 1 == static_cast<int>(pcs.size()))
+          for (int q = p + 1; q < static_cast<int>(npcs.size()); ++q) {
+            DQ_NCCL(ncclRecv(ibuf(h + 1) + npcs[q].b0, npcs[q].b1 - npcs[q].b0, ncclUint8, left, ctx->comm, ctx->cs));
+            DQ_CUDA(cudaEventRecord(ev_recv(h + 1, q), ctx->cs));
+          }
+      }
+    }
+  }
+  // the compute stream must not run ahead of the last sends (buffers are reused next round)
+  cudaEvent_t done = ctx->pipe_ev[nev - 2];
+  DQ_CUDA(cudaEventRecord(done, ctx->cs));
+  DQ_CUDA(cudaStreamWaitEvent(st, done, 0));
+  (void)pr;
+  return sink;
+}
+
 void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info* info, cudaStream_t st) {
   const dq_config& c = ctx->cfg;
   const uint32_t n = c.n_workers, me = static_cast<uint32_t>(ctx->rank);
@@ -714,95 +819,100 @@ void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info
     b.n_slots = plans[ch].n_slots;
     bases[ch] = b;
   }
-  // stage of event e of a chunk: ring -> e; butterfly -> halving stage
-  auto stage_of = [&](uint32_t ch, size_t e) -> uint32_t {
-    if (c.topology == DQ_RING) return static_cast<uint32_t>(e);
-    const Event& ev = plans[ch].red[e];
-    const uint32_t bit = ev.snd ^ ev.rcv;
-    uint32_t stages = 0;
-    while ((1u << stages) < n) ++stages;
-    uint32_t l = 0;
-    while ((1u << (stages - 1 - l)) != bit) ++l;
-    return l;
-  };
-  uint32_t n_stages = 0;
-  for (uint32_t ch = 0; ch < n; ++ch)
-    for (size_t e = 0; e < plans[ch].red.size(); ++e) n_stages = std::max(n_stages, stage_of(ch, e) + 1);
-  std::vector<char> held(n, 0), has_acc(n, 0);
-  auto operand = [&](uint32_t ch, CodecArgs& a) -> int {
-    if (has_acc[ch]) {
-      a.acc_in = acc_ptr(ch);
-      return 1;
-    }
-    return 0;
-  };
-  for (uint32_t s = 0; s < n_stages; ++s) {
-    struct Io { uint32_t ch; size_t e; };
-    std::vector<Io> sends, recvs;
+  uint8_t* mysink = buf(3, me);
+  if (c.topology == DQ_RING) {
+    mysink = ring_pipelined(ctx, p, bases, lays, mb, info, st);
+  } else {
+    // stage of event e of a chunk: ring -> e; butterfly -> halving stage
+    auto stage_of = [&](uint32_t ch, size_t e) -> uint32_t {
+      if (c.topology == DQ_RING) return static_cast<uint32_t>(e);
+      const Event& ev = plans[ch].red[e];
+      const uint32_t bit = ev.snd ^ ev.rcv;
+      uint32_t stages = 0;
+      while ((1u << stages) < n) ++stages;
+      uint32_t l = 0;
+      while ((1u << (stages - 1 - l)) != bit) ++l;
+      return l;
+    };
+    uint32_t n_stages = 0;
     for (uint32_t ch = 0; ch < n; ++ch)
-      for (size_t e = 0; e < plans[ch].red.size(); ++e) {
-        if (stage_of(ch, e) != s) continue;
-        if (plans[ch].red[e].snd == me) sends.push_back({ch, e});
-        if (plans[ch].red[e].rcv == me) recvs.push_back({ch, e});
+      for (size_t e = 0; e < plans[ch].red.size(); ++e) n_stages = std::max(n_stages, stage_of(ch, e) + 1);
+    std::vector<char> held(n, 0), has_acc(n, 0);
+    auto operand = [&](uint32_t ch, CodecArgs& a) -> int {
+      if (has_acc[ch]) {
+        a.acc_in = acc_ptr(ch);
+        return 1;
       }
-    for (const Io& io : sends) {
-      CodecArgs a = bases[io.ch];
-      a.slot = plans[io.ch].red[io.e].slot;
-      a.out = buf(0, io.ch);
-      const int src = operand(io.ch, a);
-      if (held[io.ch]) a.in = buf(2, io.ch);
-      const bool dar = held[io.ch] != 0;
-      timed(ctx, dar ? K_DAR : K_LEAF, quant_bytes(lays[io.ch], dar), st, [&] { launch_quant(a, src, dar, st); });
-      held[io.ch] = 0;
-    }
-    DQ_CUDA(cudaGetLastError());
-    double xbytes = 0;
-    for (const Io& io : sends) xbytes += lays[io.ch].bytes();
-    timed(ctx, K_NCCL, xbytes, st, [&] {
-      DQ_NCCL(ncclGroupStart());
-      for (const Io& io : sends)
-        DQ_NCCL(ncclSend(buf(0, io.ch), lays[io.ch].bytes(), ncclUint8, plans[io.ch].red[io.e].rcv, ctx->comm, st));
-      for (const Io& io : recvs)
-        DQ_NCCL(ncclRecv(buf(1, io.ch), lays[io.ch].bytes(), ncclUint8, plans[io.ch].red[io.e].snd, ctx->comm, st));
-      DQ_NCCL(ncclGroupEnd());
-    });
-    for (const Io& io : recvs) {
-      const Plan& pl = plans[io.ch];
-      size_t last = 0;
-      for (size_t e = 0; e < pl.red.size(); ++e)
-        if (pl.red[e].rcv == me) last = e;
-      CodecArgs a = bases[io.ch];
-      a.in = buf(1, io.ch);
-      if (io.e == last && me != pl.sink) {
-        DQ_CUDA(cudaMemcpyAsync(buf(2, io.ch), buf(1, io.ch), lays[io.ch].bytes(), cudaMemcpyDeviceToDevice, st));
-        held[io.ch] = 1;
-      } else if (io.e == last) {
-        a.slot = pl.sink_slot;
-        a.out = buf(3, io.ch);
+      return 0;
+    };
+    for (uint32_t s = 0; s < n_stages; ++s) {
+      struct Io { uint32_t ch; size_t e; };
+      std::vector<Io> sends, recvs;
+      for (uint32_t ch = 0; ch < n; ++ch)
+        for (size_t e = 0; e < plans[ch].red.size(); ++e) {
+          if (stage_of(ch, e) != s) continue;
+          if (plans[ch].red[e].snd == me) sends.push_back({ch, e});
+          if (plans[ch].red[e].rcv == me) recvs.push_back({ch, e});
+        }
+      for (const Io& io : sends) {
+        CodecArgs a = bases[io.ch];
+        a.slot = plans[io.ch].red[io.e].slot;
+        a.out = buf(0, io.ch);
         const int src = operand(io.ch, a);
-        timed(ctx, K_DAR, quant_bytes(lays[io.ch], true), st, [&] { launch_quant(a, src, true, st); });
-      } else {
-        const int src = operand(io.ch, a);
-        a.acc_out = acc_ptr(io.ch);
-        timed(ctx, K_DA, 2048.0 * lays[io.ch].nsg + lays[io.ch].bytes(), st, [&] { launch_da(a, src, st); });
-        has_acc[io.ch] = 1;
+        if (held[io.ch]) a.in = buf(2, io.ch);
+        const bool dar = held[io.ch] != 0;
+        timed(ctx, dar ? K_DAR : K_LEAF, quant_bytes(lays[io.ch], dar), st, [&] { launch_quant(a, src, dar, st); });
+        held[io.ch] = 0;
       }
+      DQ_CUDA(cudaGetLastError());
+      double xbytes = 0;
+      for (const Io& io : sends) xbytes += lays[io.ch].bytes();
+      timed(ctx, K_NCCL, xbytes, st, [&] {
+        DQ_NCCL(ncclGroupStart());
+        for (const Io& io : sends)
+          DQ_NCCL(ncclSend(buf(0, io.ch), lays[io.ch].bytes(), ncclUint8, plans[io.ch].red[io.e].rcv, ctx->comm, st));
+        for (const Io& io : recvs)
+          DQ_NCCL(ncclRecv(buf(1, io.ch), lays[io.ch].bytes(), ncclUint8, plans[io.ch].red[io.e].snd, ctx->comm, st));
+        DQ_NCCL(ncclGroupEnd());
+      });
+      for (const Io& io : recvs) {
+        const Plan& pl = plans[io.ch];
+        size_t last = 0;
+        for (size_t e = 0; e < pl.red.size(); ++e)
+          if (pl.red[e].rcv == me) last = e;
+        CodecArgs a = bases[io.ch];
+        a.in = buf(1, io.ch);
+        if (io.e == last && me != pl.sink) {
+          DQ_CUDA(cudaMemcpyAsync(buf(2, io.ch), buf(1, io.ch), lays[io.ch].bytes(), cudaMemcpyDeviceToDevice, st));
+          held[io.ch] = 1;
+        } else if (io.e == last) {
+          a.slot = pl.sink_slot;
+          a.out = buf(3, io.ch);
+          const int src = operand(io.ch, a);
+          timed(ctx, K_DAR, quant_bytes(lays[io.ch], true), st, [&] { launch_quant(a, src, true, st); });
+        } else {
+          const int src = operand(io.ch, a);
+          a.acc_out = acc_ptr(io.ch);
+          timed(ctx, K_DA, 2048.0 * lays[io.ch].nsg + lays[io.ch].bytes(), st, [&] { launch_da(a, src, st); });
+          has_acc[io.ch] = 1;
+        }
+      }
+      DQ_CUDA(cudaGetLastError());
     }
-    DQ_CUDA(cudaGetLastError());
   }
   // all-gather of the sink-compressed chunks (sink of chunk ch is rank ch)
   timed(ctx, K_NCCL, static_cast<double>(lays[me].bytes()) * (n - 1), st, [&] {
     DQ_NCCL(ncclGroupStart());
     for (uint32_t peer = 0; peer < n; ++peer) {
       if (peer == me) continue;
-      DQ_NCCL(ncclSend(buf(3, me), lays[me].bytes(), ncclUint8, peer, ctx->comm, st));
+      DQ_NCCL(ncclSend(mysink, lays[me].bytes(), ncclUint8, peer, ctx->comm, st));
       DQ_NCCL(ncclRecv(buf(3, peer), lays[peer].bytes(), ncclUint8, peer, ctx->comm, st));
     }
     DQ_NCCL(ncclGroupEnd());
   });
   for (uint32_t ch = 0; ch < n; ++ch) {
     CodecArgs a = bases[ch];
-    a.in = buf(3, ch);
+    a.in = ch == me ? mysink : buf(3, ch);
     a.acc_out = out;
     timed(ctx, K_DECODE, 1032.0 * lays[ch].nsg + lays[ch].bytes(), st, [&] { launch_decode(a, 1, st); });
     for (uint32_t g = 0; g < plans[ch].n_gat; ++g) account(info, lays[ch], g == 0);
@@ -1101,14 +1211,24 @@ int dq_selftest(int which, uint64_t n, uint64_t seed, uint64_t* mismatches) {
     dq_config_default(&c);
     const CodecArgs a = base_args(c, 0);
     unsigned long long* d = nullptr;
-    DQ_CUDA(cudaMalloc(&d, sizeof(*d)));
-    DQ_CUDA(cudaMemset(d, 0, sizeof(*d)));
-    launch_selftest(which, n, seed, d, a.est_c1, a.est_c2, nullptr);
+    DQ_CUDA(cudaMalloc(&d, 2 * sizeof(*d) + 64 * sizeof(float)));
+    DQ_CUDA(cudaMemset(d, 0, 2 * sizeof(*d) + 64 * sizeof(float)));
+    float* ex = reinterpret_cast<float*>(d + 2);
+    launch_selftest(which, n, seed, d, a.est_c1, a.est_c2, ex, nullptr);
     DQ_CUDA(cudaGetLastError());
     unsigned long long h = 0;
+    float hx[64];
     DQ_CUDA(cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost));
+    DQ_CUDA(cudaMemcpy(hx, ex, sizeof(hx), cudaMemcpyDeviceToHost));
     DQ_CUDA(cudaFree(d));
     *mismatches = h;
+    if (h) {  // leave examples in the error string for the test report
+      char msg[1024];
+      int k = std::snprintf(msg, sizeof msg, "%llu mismatches; a b got want:", h);
+      for (int i = 0; i < 4 && k < 900; ++i)
+        k += std::snprintf(msg + k, sizeof msg - k, " [%a %a %a %a]", hx[4 * i], hx[4 * i + 1], hx[4 * i + 2], hx[4 * i + 3]);
+      g_err = msg;
+    }
   });
 }
 

@@ -33,7 +33,7 @@ void launch_da(const CodecArgs& a, int src, cudaStream_t st);
 void launch_decode(const CodecArgs& a, int out_mode, cudaStream_t st);
 cudaError_t upload_codebooks(const float* books);
 void launch_selftest(int which, uint64_t n, uint64_t seed, unsigned long long* bad, float c1, float c2,
-                     cudaStream_t st);
+                     float* examples, cudaStream_t st);
 
 // ------------------------------------------------------------ statistics
 // per-super-group fp64 sequential sum / sum of squares of `n_workers` gradients

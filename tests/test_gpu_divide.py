@@ -26,7 +26,7 @@ def test_division_matches_ieee(L, seed):
     bad = C.c_uint64()
     from paper_2602_08923_b200._lib import check
     check(L.dq_selftest(0, 1 << 28, seed, C.byref(bad)))
-    assert bad.value == 0
+    assert bad.value == 0, L.dq_last_error().decode()
 
 
 @pytest.mark.parametrize("seed", [1, 2])
@@ -34,4 +34,4 @@ def test_bracket_matches_lower_bound(L, seed):
     bad = C.c_uint64()
     from paper_2602_08923_b200._lib import check
     check(L.dq_selftest(1, 1 << 26, seed, C.byref(bad)))
-    assert bad.value == 0
+    assert bad.value == 0, L.dq_last_error().decode()
