@@ -1,0 +1,372 @@
+// dynamiq_b200.hpp — header-only C++ drop-in for the reference's hot-path API.
+//
+// A caller of the reference library (namespace dynamiq, proj/include/dynamiq/)
+// switches to the B200 path by including this header and using namespace
+// dynamiq_b200: the same function names, argument meaning, return types and
+// exception types, implemented over the C-ABI in dynamiq_b200.h (device
+// buffers, sm_100a kernels).  Host spans in, host vectors out, exactly like the
+// reference; device-resident callers use the C-ABI directly.
+//
+//   reference                                         here
+//   codec.hpp:64  compress_chunk(values, widths, books, cfg, qctx, first_sg)
+//   codec.hpp:71  decompress_chunk(chunk, books, cfg, out)
+//   codec.hpp:75  decompress_accumulate(chunk, acc, books, cfg)
+//   codec.hpp:86  decompress_accumulate_recompress(chunk, local, books, cfg, qctx, first_sg)
+//   codec.hpp:94  serialize_chunk(chunk, cfg) / parse_chunk(bytes, cfg)
+//   stats.hpp:19  compute_stats / reduce_stats
+//   allocation.hpp:63 allocate_fast(sq_norms, spec)
+//   engine.hpp:63 run_round(worker_values, config)
+//
+// CompressedChunk keeps the reference's serialized bytes (its wire format), so
+// chunks interoperate with the reference library byte for byte.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "dynamiq_b200.h"
+
+namespace dynamiq_b200 {
+
+struct InfeasibleBudget : std::runtime_error {  // allocation.hpp:14-16
+  explicit InfeasibleBudget(const std::string& w) : std::runtime_error(w) {}
+};
+
+namespace detail {
+inline void check(int rc) {
+  if (rc == DQ_OK) return;
+  const std::string msg = dq_last_error();
+  if (rc == DQ_EINVAL) throw std::invalid_argument(msg);
+  if (rc == DQ_EINFEASIBLE) throw InfeasibleBudget(msg);
+  if (rc == DQ_EMALFORMED) throw std::runtime_error(msg);
+  throw std::runtime_error("dynamiq_b200: " + msg);
+}
+inline void cuda(cudaError_t e) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string("dynamiq_b200: ") + cudaGetErrorString(e));
+}
+template <class T>
+struct Dev {  // owning device buffer
+  T* p = nullptr;
+  explicit Dev(size_t n) { cuda(cudaMalloc(&p, sizeof(T) * (n ? n : 1))); }
+  ~Dev() { cudaFree(p); }
+  Dev(const Dev&) = delete;
+  Dev& operator=(const Dev&) = delete;
+};
+struct Runs {
+  uint32_t n8 = 0, n4 = 0, n2 = 0;
+};
+inline Runs runs_of(std::span<const uint8_t> widths) {  // codec.cpp:298-315 order check
+  Runs r;
+  int prev = -1;
+  for (uint8_t w : widths) {
+    const int cls = w == 8 ? 0 : w == 4 ? 1 : w == 2 ? 2 : -1;
+    if (cls < 0) throw std::invalid_argument("unsupported codec width " + std::to_string(w) + " on device");
+    if (cls < prev) throw std::invalid_argument("chunk body must be ordered by width class 8,4,2,16");
+    prev = cls;
+    (cls == 0 ? r.n8 : cls == 1 ? r.n4 : r.n2)++;
+  }
+  return r;
+}
+}  // namespace detail
+
+struct SharedSeed {  // random.hpp:12-15
+  std::uint64_t seed = 0;
+  std::uint64_t round = 0;
+};
+
+struct QuantContext {  // codec.hpp:33-40
+  SharedSeed seed;
+  std::uint32_t chunk_index = 0;
+  std::uint32_t hop_slot = 0;
+  std::uint32_t n_slots = 1;
+  bool correlated = true;
+};
+
+struct CodecConfig {  // codec.hpp:26-31 (device: s = 16, S = 256, hierarchical)
+  std::uint32_t group_size = 16;
+  std::uint32_t super_group_size = 256;
+  bool hierarchical_scales = true;
+  void validate() const {
+    if (group_size == 0 || super_group_size % group_size != 0)
+      throw std::invalid_argument("super-group size must be a positive multiple of the group size");
+    if (super_group_size % 4 != 0) throw std::invalid_argument("super-group size must be a multiple of 4 for byte alignment");
+    if (group_size != 16 || super_group_size != 256 || !hierarchical_scales)
+      throw std::invalid_argument("device codec supports s=16, S=256 with hierarchical scales");
+  }
+};
+
+// Stand-in for CodebookSet: which default family (codebook.hpp:46-52).
+struct CodebookSet {
+  bool non_uniform = true;
+  static CodebookSet non_uniform_defaults() { return {true}; }
+  static CodebookSet uniform_all() { return {false}; }
+};
+
+struct CompressedChunk {  // codec.hpp:20-31, held as the reference's serialized bytes
+  std::uint32_t chunk_index = 0;
+  std::vector<std::uint8_t> widths;
+  std::vector<std::uint8_t> wire;  // serialize_chunk() bytes
+};
+
+inline std::uint64_t compressed_size_bits(std::span<const std::uint8_t> widths, std::uint32_t S, std::uint32_t s,
+                                          bool hierarchical_scales) {  // codec.cpp:281-291
+  std::uint64_t bits = 6 * 32;
+  for (std::uint8_t w : widths) {
+    if (w != 2 && w != 4 && w != 8 && w != 16) throw std::invalid_argument("unsupported codec width");
+    bits += static_cast<std::uint64_t>(S) * w;
+    if (w != 16) bits += hierarchical_scales ? 16 + static_cast<std::uint64_t>(S / s) * 8 : static_cast<std::uint64_t>(S / s) * 16;
+  }
+  return bits;
+}
+
+namespace detail {
+// reference bytes -> device SoA chunk
+inline std::unique_ptr<Dev<uint8_t>> upload(const CompressedChunk& c, Runs* r) {
+  std::vector<uint8_t> soa(c.wire.size() + 1);
+  uint32_t ci = 0;
+  check(dq_from_reference_wire(c.wire.data(), c.wire.size(), soa.data(), soa.size(), &ci, &r->n8, &r->n4, &r->n2));
+  const size_t bytes = dq_chunk_bytes(r->n8, r->n4, r->n2);
+  auto d = std::make_unique<Dev<uint8_t>>(bytes);
+  cuda(cudaMemcpy(d->p, soa.data(), bytes, cudaMemcpyHostToDevice));
+  return d;
+}
+inline CompressedChunk download(const uint8_t* dsoa, uint32_t chunk_index, Runs r) {
+  const size_t bytes = dq_chunk_bytes(r.n8, r.n4, r.n2);
+  std::vector<uint8_t> soa(bytes + 1);
+  cuda(cudaMemcpy(soa.data(), dsoa, bytes, cudaMemcpyDeviceToHost));
+  CompressedChunk c;
+  c.chunk_index = chunk_index;
+  c.widths.assign(r.n8, 8);
+  c.widths.insert(c.widths.end(), r.n4, 4);
+  c.widths.insert(c.widths.end(), r.n2, 2);
+  c.wire.resize(bytes + 24);
+  check(dq_to_reference_wire(soa.data(), chunk_index, r.n8, r.n4, r.n2, c.wire.data()));
+  return c;
+}
+inline dq_qctx qctx(const QuantContext& q) {
+  return dq_qctx{q.seed.seed, q.seed.round, q.chunk_index, q.hop_slot, q.n_slots, q.correlated ? 1 : 0};
+}
+}  // namespace detail
+
+inline CompressedChunk compress_chunk(std::span<const float> values, std::span<const std::uint8_t> widths,
+                                      const CodebookSet& books, const CodecConfig& cfg, const QuantContext& q,
+                                      std::uint32_t first_sg_index) {
+  cfg.validate();
+  if (values.size() != widths.size() * cfg.super_group_size)
+    throw std::invalid_argument("chunk length does not match widths");
+  const detail::Runs r = detail::runs_of(widths);
+  detail::Dev<float> dv(values.size());
+  detail::Dev<uint8_t> out(dq_chunk_bytes(r.n8, r.n4, r.n2));
+  detail::cuda(cudaMemcpy(dv.p, values.data(), values.size_bytes(), cudaMemcpyHostToDevice));
+  const dq_qctx c = detail::qctx(q);
+  detail::check(dq_compress_chunk(dv.p, r.n8, r.n4, r.n2, &c, first_sg_index, books.non_uniform, out.p, nullptr));
+  return detail::download(out.p, q.chunk_index, r);
+}
+
+inline CompressedChunk decompress_accumulate_recompress(const CompressedChunk& chunk, std::span<const float> local,
+                                                        const CodebookSet& books, const CodecConfig& cfg,
+                                                        const QuantContext& q, std::uint32_t first_sg_index) {
+  cfg.validate();
+  detail::Runs r;
+  auto in = detail::upload(chunk, &r);
+  if (local.size() != static_cast<size_t>(r.n8 + r.n4 + r.n2) * 256)
+    throw std::invalid_argument("local buffer length does not match chunk");
+  detail::Dev<float> dl(local.size());
+  detail::Dev<uint8_t> out(dq_chunk_bytes(r.n8, r.n4, r.n2));
+  detail::cuda(cudaMemcpy(dl.p, local.data(), local.size_bytes(), cudaMemcpyHostToDevice));
+  const dq_qctx c = detail::qctx(q);
+  detail::check(dq_dar_chunk(in->p, dl.p, r.n8, r.n4, r.n2, &c, first_sg_index, books.non_uniform, out.p, nullptr));
+  return detail::download(out.p, q.chunk_index, r);
+}
+
+inline void decompress_chunk(const CompressedChunk& chunk, const CodebookSet& books, const CodecConfig& cfg,
+                             std::span<float> out) {
+  cfg.validate();
+  detail::Runs r;
+  auto in = detail::upload(chunk, &r);
+  if (out.size() != static_cast<size_t>(r.n8 + r.n4 + r.n2) * 256)
+    throw std::invalid_argument("output length does not match chunk");
+  detail::Dev<float> d(out.size());
+  detail::check(dq_decompress_chunk(in->p, d.p, r.n8, r.n4, r.n2, books.non_uniform, nullptr));
+  detail::cuda(cudaMemcpy(out.data(), d.p, out.size_bytes(), cudaMemcpyDeviceToHost));
+}
+
+inline void decompress_accumulate(const CompressedChunk& chunk, std::span<float> acc, const CodebookSet& books,
+                                  const CodecConfig& cfg) {
+  cfg.validate();
+  detail::Runs r;
+  auto in = detail::upload(chunk, &r);
+  if (acc.size() != static_cast<size_t>(r.n8 + r.n4 + r.n2) * 256)
+    throw std::invalid_argument("accumulator length does not match chunk");
+  detail::Dev<float> d(acc.size());
+  detail::cuda(cudaMemcpy(d.p, acc.data(), acc.size_bytes(), cudaMemcpyHostToDevice));
+  detail::check(dq_da_chunk(in->p, d.p, r.n8, r.n4, r.n2, books.non_uniform, nullptr));
+  detail::cuda(cudaMemcpy(acc.data(), d.p, acc.size_bytes(), cudaMemcpyDeviceToHost));
+}
+
+inline std::vector<std::uint8_t> serialize_chunk(const CompressedChunk& chunk, const CodecConfig& cfg) {
+  cfg.validate();
+  return chunk.wire;
+}
+
+inline CompressedChunk parse_chunk(std::span<const std::uint8_t> bytes, const CodecConfig& cfg) {  // strict
+  cfg.validate();
+  CompressedChunk c;
+  c.wire.assign(bytes.begin(), bytes.end());
+  std::vector<uint8_t> soa(bytes.size() + 1);
+  uint32_t n8, n4, n2;
+  detail::check(dq_from_reference_wire(bytes.data(), bytes.size(), soa.data(), soa.size(), &c.chunk_index, &n8, &n4, &n2));
+  c.widths.assign(n8, 8);
+  c.widths.insert(c.widths.end(), n4, 4);
+  c.widths.insert(c.widths.end(), n2, 2);
+  return c;
+}
+
+struct SuperGroupStats {  // stats.hpp:14-17
+  float mean = 0.0f;
+  float sq_norm = 0.0f;
+};
+
+inline std::vector<SuperGroupStats> compute_stats(std::span<const float> values) {
+  const size_t T = (values.size() + 255) / 256;
+  detail::Dev<float> x(values.size()), m(T), q(T);
+  detail::cuda(cudaMemcpy(x.p, values.data(), values.size_bytes(), cudaMemcpyHostToDevice));
+  detail::check(dq_compute_stats(x.p, values.size(), m.p, q.p, nullptr));
+  std::vector<float> hm(T), hq(T);
+  detail::cuda(cudaMemcpy(hm.data(), m.p, T * 4, cudaMemcpyDeviceToHost));
+  detail::cuda(cudaMemcpy(hq.data(), q.p, T * 4, cudaMemcpyDeviceToHost));
+  std::vector<SuperGroupStats> s(T);
+  for (size_t j = 0; j < T; ++j) s[j] = {hm[j], hq[j]};
+  return s;
+}
+
+struct BudgetSpec {  // allocation.hpp:24-30 (fast allocator: W = {2,4,8})
+  double total_bits_per_coordinate = 5.0;
+  std::uint32_t group_size = 16;
+  std::uint32_t super_group_size = 256;
+  std::vector<int> widths = {2, 4, 8};
+  bool hierarchical_scales = true;
+};
+
+struct BitAllocation {  // allocation.hpp:40-45
+  std::vector<std::uint8_t> widths;
+  std::vector<std::uint32_t> permutation;
+  std::uint64_t payload_bits = 0;
+  double u = 0.0;
+};
+
+inline BitAllocation allocate_fast(std::span<const float> sq_norms, const BudgetSpec& spec) {
+  if (spec.widths != std::vector<int>{2, 4, 8}) throw std::invalid_argument("allocate_fast requires W = {2,4,8}");
+  dq_config c;
+  dq_config_default(&c);
+  c.budget_bits = spec.total_bits_per_coordinate;
+  dq_ctx* ctx = nullptr;
+  detail::check(dq_ctx_create(&c, 0, &ctx));
+  std::unique_ptr<dq_ctx, int (*)(dq_ctx*)> guard(ctx, dq_ctx_destroy);
+  const size_t T = sq_norms.size();
+  detail::Dev<float> F(T);
+  detail::Dev<uint8_t> w(T);
+  detail::Dev<uint32_t> p(T);
+  detail::cuda(cudaMemcpy(F.p, sq_norms.data(), T * 4, cudaMemcpyHostToDevice));
+  BitAllocation a;
+  uint32_t counts[3];
+  detail::check(dq_allocate_fast(ctx, F.p, T, spec.total_bits_per_coordinate, w.p, p.p, &a.u, &a.payload_bits, counts, nullptr));
+  a.widths.resize(T);
+  a.permutation.resize(T);
+  detail::cuda(cudaMemcpy(a.widths.data(), w.p, T, cudaMemcpyDeviceToHost));
+  detail::cuda(cudaMemcpy(a.permutation.data(), p.p, T * 4, cudaMemcpyDeviceToHost));
+  return a;
+}
+
+enum class TopologyKind { kRing, kButterfly };
+enum class AllocatorKind { kGeneral, kFast, kFixed };
+enum class CodecKind { kQuantized, kLossless };
+
+struct PipelineConfig {  // engine.hpp:22-43
+  std::uint32_t n_workers = 4;
+  std::uint32_t group_size = 16;
+  std::uint32_t super_group_size = 256;
+  double budget_bits = 5.0;
+  bool non_uniform = true;
+  bool variable_width = true;
+  bool hierarchical_scales = true;
+  bool correlated = true;
+  int fixed_width = 4;
+  AllocatorKind allocator = AllocatorKind::kFast;
+  TopologyKind topology = TopologyKind::kRing;
+  CodecKind codec = CodecKind::kQuantized;
+  SharedSeed seed{1, 0};
+  unsigned threads = 1;
+};
+
+struct RoundResult {  // engine.hpp:45-54 (exact sum / hop errors: reference-side diagnostics)
+  std::vector<float> synced;
+  double vnmse = 0.0;
+  double mse = 0.0;
+  std::uint64_t wire_hash = 0;
+  BitAllocation allocation;
+  dq_round_info info{};
+};
+
+inline RoundResult run_round(const std::vector<std::vector<float>>& worker_values, const PipelineConfig& p,
+                             bool collect_wire = true) {
+  if (worker_values.empty()) throw std::invalid_argument("no workers");
+  for (const auto& v : worker_values)
+    if (v.size() != worker_values.front().size()) throw std::invalid_argument("worker gradients must have equal length");
+  if (worker_values.front().empty()) throw std::invalid_argument("empty gradient");
+  if (worker_values.size() != p.n_workers) throw std::invalid_argument("worker count does not match config");
+  dq_config c;
+  dq_config_default(&c);
+  c.n_workers = p.n_workers;
+  c.group_size = p.group_size;
+  c.super_group_size = p.super_group_size;
+  c.budget_bits = p.budget_bits;
+  c.non_uniform = p.non_uniform;
+  c.variable_width = p.variable_width;
+  c.hierarchical_scales = p.hierarchical_scales;
+  c.correlated = p.correlated;
+  c.fixed_width = p.fixed_width;
+  c.allocator = static_cast<int32_t>(p.allocator);
+  c.topology = static_cast<int32_t>(p.topology);
+  c.codec = static_cast<int32_t>(p.codec);
+  c.seed = p.seed.seed;
+  c.round = p.seed.round;
+  c.threads = p.threads;
+  dq_ctx* ctx = nullptr;
+  detail::check(dq_ctx_create(&c, 0, &ctx));
+  std::unique_ptr<dq_ctx, int (*)(dq_ctx*)> guard(ctx, dq_ctx_destroy);
+  const size_t d = worker_values.front().size(), n = worker_values.size();
+  std::vector<std::unique_ptr<detail::Dev<float>>> xs;
+  std::vector<const float*> ptrs;
+  for (const auto& v : worker_values) {
+    xs.push_back(std::make_unique<detail::Dev<float>>(d));
+    detail::cuda(cudaMemcpy(xs.back()->p, v.data(), d * 4, cudaMemcpyHostToDevice));
+    ptrs.push_back(xs.back()->p);
+  }
+  detail::Dev<float> y(d);
+  RoundResult r;
+  detail::check(dq_sim_round(ctx, ptrs.data(), d, y.p, collect_wire ? DQ_SIM_COLLECT_WIRE : 0, &r.info, nullptr));
+  r.synced.resize(d);
+  detail::cuda(cudaMemcpy(r.synced.data(), y.p, d * 4, cudaMemcpyDeviceToHost));
+  r.vnmse = r.info.vnmse;
+  r.mse = r.info.mse;
+  r.wire_hash = r.info.wire_hash;
+  r.allocation.u = r.info.u;
+  r.allocation.payload_bits = r.info.payload_bits;
+  if (n > 1) {
+    const size_t T = (d + 255) / 256;
+    r.allocation.widths.resize(T);
+    r.allocation.permutation.resize(T);
+    detail::check(dq_round_allocation(ctx, r.allocation.widths.data(), r.allocation.permutation.data(), T));
+  }
+  return r;
+}
+
+}  // namespace dynamiq_b200
