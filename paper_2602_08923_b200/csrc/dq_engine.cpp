@@ -521,9 +521,11 @@ void sim_round(dq_ctx* ctx, const float* const* xs, size_t d, float* out, int fl
   Prepared p = prepare(ctx, T, st);
   fill_info_alloc(info, p);
 
-  // message pool: per-worker pending slot + one scratch; per-worker accumulators
+  // message pool: per-worker pending slots + scratch, reused per chunk; plus one gather
+  // (sink output) buffer per chunk, decoded together at the end of the round
   const size_t mb = p.max_chunk_bytes;
-  ctx->msgs.reserve((n + 2) * mb);
+  ctx->msgs.reserve((n + 2 + n) * mb);
+  std::vector<int> gslots(n, -1);
   uint32_t max_nsg = 0;
   for (uint32_t i = 0; i < n; ++i) max_nsg = std::max(max_nsg, p.lo[i + 1] - p.lo[i]);
   const bool need_acc = c.topology == DQ_BUTTERFLY;
@@ -546,6 +548,7 @@ void sim_round(dq_ctx* ctx, const float* const* xs, size_t d, float* out, int fl
     for (size_t e = 0; e < plan.red.size(); ++e) last_in[plan.red[e].rcv] = static_cast<int>(e);
     std::vector<int> free_slots;
     for (int k = static_cast<int>(n) + 1; k >= 0; --k) free_slots.push_back(k);
+    const int gather_dst = static_cast<int>(n + 2 + ch);  // this chunk's sink output lives here
     auto slot_ptr = [&](int k) { return ctx->msgs.p + static_cast<size_t>(k) * mb; };
     auto acc_ptr = [&](uint32_t w) { return ctx->accs.p + static_cast<size_t>(w) * max_nsg * 256; };
     uint64_t hsh = 0xcbf29ce484222325ULL;
@@ -590,8 +593,7 @@ void sim_round(dq_ctx* ctx, const float* const* xs, size_t d, float* out, int fl
         pend_slot[r] = os;
       } else if (static_cast<int>(e) == last_in[r] && r == plan.sink) {
         // fused sink: compress(dec(last) + buf[sink]) at the sink slot (== DA then compress)
-        const int gs = free_slots.back();
-        free_slots.pop_back();
+        const int gs = gather_dst;
         CodecArgs g = base;
         g.slot = plan.sink_slot;
         g.out = slot_ptr(gs);
@@ -615,14 +617,33 @@ void sim_round(dq_ctx* ctx, const float* const* xs, size_t d, float* out, int fl
     if (collect_wire) hash_msg(slot_ptr(gather_slot), static_cast<int>(plan.n_gat));
     for (uint32_t g = 0; g < plan.n_gat; ++g) account(info, L, g == 0);
     info->stats_bits += static_cast<uint64_t>(plan.red.size() + plan.n_gat) * 64ull * L.nsg;
-    CodecArgs dec = base;
-    dec.in = slot_ptr(gather_slot);
-    dec.acc_out = out;
-    timed(ctx, K_DECODE, 1032.0 * L.nsg + L.bytes(), st, [&] { launch_decode(dec, 1, st); });
-    DQ_CUDA(cudaGetLastError());
+    gslots[ch] = gather_slot;
     H ^= hsh + 0x9e3779b97f4a7c15ULL + (H << 6) + (H >> 2);
   }
   if (collect_wire) info->wire_hash = H;
+  {
+    GatherArgs g{};
+    uint32_t max_nsg_g = 0;
+    for (uint32_t ch = 0; ch < n; ++ch) {
+      const Layout L = chunk_layout(p.a, p.lo[ch], p.lo[ch + 1]);
+      g.in[ch] = ctx->msgs.p + static_cast<size_t>(gslots[ch]) * mb;
+      g.lo[ch] = p.lo[ch];
+      g.n8[ch] = L.n8;
+      g.n4[ch] = L.n4;
+      max_nsg_g = std::max(max_nsg_g, L.nsg);
+    }
+    g.lo[n] = p.lo[n];
+    g.perm = ctx->perm.p;
+    g.gmean = ctx->gmean.p;
+    g.out = out;
+    g.d = d;
+    g.n_workers_f = static_cast<float>(n);
+    g.uniform_books = c.non_uniform ? 0 : 1;
+    double gbytes = 0;
+    for (uint32_t ch = 0; ch < n; ++ch) gbytes += 1032.0 * (p.lo[ch + 1] - p.lo[ch]) + chunk_layout(p.a, p.lo[ch], p.lo[ch + 1]).bytes();
+    timed(ctx, K_DECODE, gbytes, st, [&] { launch_gather_decode(g, n, max_nsg_g, st); });
+    DQ_CUDA(cudaGetLastError());
+  }
   DQ_CUDA(cudaEventRecord(ctx->ev1, st));
   if (flags & DQ_SIM_NO_METRICS) {
     DQ_CUDA(cudaStreamSynchronize(st));
@@ -910,11 +931,28 @@ void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info
     }
     DQ_NCCL(ncclGroupEnd());
   });
+  {
+    GatherArgs g{};
+    uint32_t max_nsg_g = 0;
+    double gbytes = 0;
+    for (uint32_t ch = 0; ch < n; ++ch) {
+      g.in[ch] = ch == me ? mysink : buf(3, ch);
+      g.lo[ch] = p.lo[ch];
+      g.n8[ch] = lays[ch].n8;
+      g.n4[ch] = lays[ch].n4;
+      max_nsg_g = std::max(max_nsg_g, lays[ch].nsg);
+      gbytes += 1032.0 * lays[ch].nsg + lays[ch].bytes();
+    }
+    g.lo[n] = p.lo[n];
+    g.perm = ctx->perm.p;
+    g.gmean = ctx->gmean.p;
+    g.out = out;
+    g.d = d;
+    g.n_workers_f = static_cast<float>(n);
+    g.uniform_books = c.non_uniform ? 0 : 1;
+    timed(ctx, K_DECODE, gbytes, st, [&] { launch_gather_decode(g, n, max_nsg_g, st); });
+  }
   for (uint32_t ch = 0; ch < n; ++ch) {
-    CodecArgs a = bases[ch];
-    a.in = ch == me ? mysink : buf(3, ch);
-    a.acc_out = out;
-    timed(ctx, K_DECODE, 1032.0 * lays[ch].nsg + lays[ch].bytes(), st, [&] { launch_decode(a, 1, st); });
     for (uint32_t g = 0; g < plans[ch].n_gat; ++g) account(info, lays[ch], g == 0);
     for (size_t e = 0; e < plans[ch].red.size(); ++e) account(info, lays[ch], true);
     info->stats_bits += static_cast<uint64_t>(plans[ch].red.size() + plans[ch].n_gat) * 64ull * lays[ch].nsg;

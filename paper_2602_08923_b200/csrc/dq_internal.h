@@ -28,6 +28,20 @@ struct CodecArgs {
   float est_c1, est_c2;     // width-8 codebook index estimator (see bracket())
 };
 
+// All chunks of a round decoded into the output gradient in one launch.
+struct GatherArgs {
+  const uint8_t* in[64];     // compressed chunk c (dq tiled SoA)
+  uint32_t lo[65];           // chunk c = permuted super-groups [lo[c], lo[c+1])
+  uint32_t n8[64], n4[64];   // width runs of chunk c
+  const uint32_t* perm;
+  const float* gmean;
+  float* out;
+  uint64_t d;
+  float n_workers_f;
+  int uniform_books;
+};
+void launch_gather_decode(const GatherArgs& g, uint32_t n_chunks, uint32_t max_nsg, cudaStream_t st);
+
 void launch_quant(const CodecArgs& a, int src, bool dar, cudaStream_t st);
 void launch_da(const CodecArgs& a, int src, cudaStream_t st);
 void launch_decode(const CodecArgs& a, int out_mode, cudaStream_t st);
