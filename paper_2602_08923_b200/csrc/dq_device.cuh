@@ -38,40 +38,6 @@ __host__ __device__ __forceinline__ uint64_t absorb(uint64_t h, uint64_t w) {
 __host__ __device__ __forceinline__ uint64_t absorb_base(uint64_t h) {
   return kGolden + (h << 6) + (h >> 2);
 }
-// absorb(h, w0 + t) for many small t (Fisher-Yates counters, entry indices):
-// with K = w0 + golden + (h << 6) + (h >> 2), the mixed input is h ^ (K + t).
-// While K.lo + t does not carry, its high word zh = h.hi ^ K.hi is the same for
-// every t, so mix64's first xorshift (lo ^= zh >> 1) and the zh * C1.lo partial
-// product are hoisted; only the low word changes per t.  ok == false means some
-// t <= tmax could carry and the caller must use absorb() (probability ~tmax 2^-32).
-struct AbsorbSmall {
-  uint32_t klo;   // K.lo
-  uint32_t xlo;   // h.lo ^ (zh >> 1)
-  uint32_t zh;    // h.hi ^ K.hi
-  uint32_t zhc;   // zh * C1.lo (low 32 bits)
-  bool ok;
-};
-constexpr uint64_t kMixC1 = 0xff51afd7ed558ccdULL, kMixC2 = 0xc4ceb9fe1a85ec53ULL;
-__host__ __device__ __forceinline__ AbsorbSmall absorb_small_prep(uint64_t h, uint64_t w0, uint32_t tmax) {
-  const uint64_t K = w0 + kGolden + (h << 6) + (h >> 2);
-  AbsorbSmall a;
-  a.klo = static_cast<uint32_t>(K);
-  a.zh = static_cast<uint32_t>(h >> 32) ^ static_cast<uint32_t>(K >> 32);
-  a.xlo = static_cast<uint32_t>(h) ^ (a.zh >> 1);
-  a.zhc = a.zh * static_cast<uint32_t>(kMixC1);
-  a.ok = a.klo <= 0xffffffffu - tmax;
-  return a;
-}
-// == absorb(h, w0 + t) when a.ok and t <= tmax
-__host__ __device__ __forceinline__ uint64_t absorb_small(const AbsorbSmall& a, uint32_t t) {
-  const uint32_t zl = a.xlo ^ (a.klo + t);  // low word after the first xorshift
-  const uint64_t p = static_cast<uint64_t>(zl) * static_cast<uint32_t>(kMixC1);
-  const uint32_t hi = static_cast<uint32_t>(p >> 32) + zl * static_cast<uint32_t>(kMixC1 >> 32) + a.zhc;
-  uint64_t z = (static_cast<uint64_t>(hi) << 32) | static_cast<uint32_t>(p);
-  z = (z ^ (z >> 33)) * kMixC2;
-  return z ^ (z >> 33);
-}
-
 __host__ __device__ __forceinline__ double unit53(uint64_t b) {
   return static_cast<double>(b >> 11) * 0x1.0p-53;
 }
