@@ -161,7 +161,7 @@ struct dq_ctx {
   dq_config cfg{};
   int device = 0;
   // round scratch
-  DevBuf<float> mean_all, sq_all, gmean, gsq;
+  DevBuf<float> mean_all, sq_all, gmean, gsq, pmean;
   DevBuf<uint8_t> widths;
   DevBuf<uint32_t> perm;
   DevBuf<double> level;
@@ -177,6 +177,7 @@ struct dq_ctx {
   uint32_t* h_counts = nullptr;
   double* h_vn = nullptr;
   uint32_t last_T = 0;
+  uint64_t alloc_redos = 0;  // rounds where the device thresholds differed from glibc's
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   // per-kernel-family device timing (CUDA events bracketing each launch)
   struct Prof {
@@ -220,7 +221,7 @@ cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 enum Kind { K_STATS, K_REDUCE, K_ALLOC_SEARCH, K_ALLOC_ASSIGN, K_LEAF, K_DAR, K_DA, K_DECODE, K_NCCL, K_NKINDS };
 const char* const kKindName[K_NKINDS] = {"stats", "reduce_stats", "alloc_search", "alloc_assign", "quant_leaf",
                                          "quant_dar", "decompress_accumulate", "decode_out", "nccl"};
-const int kKindLaunches[K_NKINDS] = {1, 1, 4 + 2 * kAllocMaxPasses, 3, 1, 1, 1, 1, 0};
+const int kKindLaunches[K_NKINDS] = {1, 1, 1, 3, 1, 1, 1, 1, 0};
 
 cudaEvent_t pool_event(dq_ctx* ctx) {
   if (!ctx->ev_pool.empty()) {
@@ -304,7 +305,10 @@ AllocWork work_of(dq_ctx* ctx, uint32_t T) {
   ctx->counts.reserve(4);
   if (!ctx->h_state) DQ_CUDA(cudaMallocHost(&ctx->h_state, sizeof(AllocState)));
   if (!ctx->h_counts) DQ_CUDA(cudaMallocHost(&ctx->h_counts, 4 * sizeof(uint32_t)));
-  return AllocWork{ctx->level.p, ctx->astate.p, ctx->bins.p, ctx->blockcnt.p, ctx->counts.p};
+  ctx->pmean.reserve(T);
+  const bool have_means = ctx->gmean.n >= T && ctx->gmean.p;  // round path; dq_allocate_fast alone has none
+  return AllocWork{ctx->level.p, ctx->astate.p, ctx->bins.p, ctx->blockcnt.p, ctx->counts.p,
+                   have_means ? ctx->gmean.p : nullptr, have_means ? ctx->pmean.p : nullptr};
 }
 
 struct AllocResult {
@@ -339,9 +343,14 @@ AllocResult allocate(dq_ctx* ctx, const dq_config& c, const float* dF, uint32_t 
   while (fits(W + 1)) ++W;
   while (W >= 0 && !fits(W)) --W;
   if (W < 0) throw Error(DQ_EINFEASIBLE, "bit allocation infeasible within budget");
+  // search + device thresholds, assignment with the device thresholds, then ONE sync that
+  // brings back the state and the class counts together
   timed(ctx, K_ALLOC_SEARCH, 8.0 * T, st, [&] { launch_alloc_search(dF, T, kAlpha, static_cast<uint64_t>(W), w, st); });
   DQ_CUDA(cudaGetLastError());
+  timed(ctx, K_ALLOC_ASSIGN, 13.0 * T, st, [&] { launch_alloc_assign(dF, T, 0.f, 0.f, true, w, dW, dP, st); });
+  DQ_CUDA(cudaGetLastError());
   DQ_CUDA(cudaMemcpyAsync(ctx->h_state, w.state, sizeof(AllocState), cudaMemcpyDeviceToHost, st));
+  DQ_CUDA(cudaMemcpyAsync(ctx->h_counts, w.counts, 3 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   DQ_CUDA(cudaStreamSynchronize(st));
   const AllocState s = *ctx->h_state;
   // the flips adjacent to the chosen plateau, recomputed with the host libm exactly as
@@ -365,10 +374,13 @@ AllocResult allocate(dq_ctx* ctx, const dq_config& c, const float* dF, uint32_t 
   u = u < -1e6 ? -1e6 : (u > 1e6 ? 1e6 : u);
   const float t24 = static_cast<float>(std::exp2((4.0 - u) / kAlpha));
   const float t48 = static_cast<float>(std::exp2((8.0 - u) / kAlpha));
-  timed(ctx, K_ALLOC_ASSIGN, 13.0 * T, st, [&] { launch_alloc_assign(dF, T, t24, t48, w, dW, dP, st); });
-  DQ_CUDA(cudaGetLastError());
-  DQ_CUDA(cudaMemcpyAsync(ctx->h_counts, w.counts, 3 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-  DQ_CUDA(cudaStreamSynchronize(st));
+  if (t24 != s.t24 || t48 != s.t48) {  // device libm disagreed in the last place: redo with glibc's
+    ++ctx->alloc_redos;
+    timed(ctx, K_ALLOC_ASSIGN, 13.0 * T, st, [&] { launch_alloc_assign(dF, T, t24, t48, false, w, dW, dP, st); });
+    DQ_CUDA(cudaGetLastError());
+    DQ_CUDA(cudaMemcpyAsync(ctx->h_counts, w.counts, 3 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    DQ_CUDA(cudaStreamSynchronize(st));
+  }
   r.u = u;
   r.n8 = ctx->h_counts[0];
   r.n4 = ctx->h_counts[1];
@@ -540,7 +552,7 @@ void sim_round(dq_ctx* ctx, const float* const* xs, size_t d, float* out, int fl
     base.L = L;
     base.first_sg = p.lo[ch];
     base.perm = ctx->perm.p;
-    base.gmean = ctx->gmean.p;
+    base.gmean = ctx->pmean.p;
     base.d = d;
     base.n_slots = plan.n_slots;
     std::vector<int> pend_slot(n, -1), last_in(n, -1);
@@ -634,7 +646,7 @@ void sim_round(dq_ctx* ctx, const float* const* xs, size_t d, float* out, int fl
     }
     g.lo[n] = p.lo[n];
     g.perm = ctx->perm.p;
-    g.gmean = ctx->gmean.p;
+    g.gmean = ctx->pmean.p;
     g.out = out;
     g.d = d;
     g.n_workers_f = static_cast<float>(n);
@@ -834,7 +846,7 @@ void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info
     b.L = lays[ch];
     b.first_sg = p.lo[ch];
     b.perm = ctx->perm.p;
-    b.gmean = ctx->gmean.p;
+    b.gmean = ctx->pmean.p;
     b.d = d;
     b.x = x;
     b.n_slots = plans[ch].n_slots;
@@ -945,7 +957,7 @@ void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info
     }
     g.lo[n] = p.lo[n];
     g.perm = ctx->perm.p;
-    g.gmean = ctx->gmean.p;
+    g.gmean = ctx->pmean.p;
     g.out = out;
     g.d = d;
     g.n_workers_f = static_cast<float>(n);

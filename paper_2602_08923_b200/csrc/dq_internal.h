@@ -14,7 +14,7 @@ struct CodecArgs {
   uint32_t first_sg;        // permuted index of the chunk's first super-group (RNG key, perm lookup)
   const float* x;           // raw gradient, original order (gather source)
   const uint32_t* perm;     // permuted position -> original super-group
-  const float* gmean;       // global super-group means, original order
+  const float* gmean;       // global super-group means, permuted order (gmean[k] = mean of perm[k])
   uint64_t d;               // logical gradient length (zero padding beyond)
   const float* acc_in;      // chunk-local fp32 operand [nsg * 256]
   float* acc_out;           // chunk-local fp32 result, or the output gradient (decode OUT=1)
@@ -34,7 +34,7 @@ struct GatherArgs {
   uint32_t lo[65];           // chunk c = permuted super-groups [lo[c], lo[c+1])
   uint32_t n8[64], n4[64];   // width runs of chunk c
   const uint32_t* perm;
-  const float* gmean;
+  const float* gmean;        // permuted order
   float* out;
   uint64_t d;
   float n_workers_f;
@@ -73,6 +73,10 @@ struct AllocState {
   // F (float bits) and flip type (0: 4 - a log2 F, 1: 8 - a log2 F) of the crossing,
   // predecessor and largest flips, so the host recomputes them with the reference's libm
   uint32_t cross_f, cross_t, pred_f, pred_t, max_f, pad_;
+  // the plateau midpoint and thresholds as computed on device with CUDA libm; the host
+  // recomputes them with the reference's libm and redoes the assignment on a mismatch
+  double u;
+  float t24, t48;
 };
 constexpr int kAllocBins = 1024;
 constexpr int kAllocMaxPasses = 8;
@@ -82,13 +86,18 @@ struct AllocWork {           // device scratch owned by the context
   uint64_t* bins;            // [kAllocBins][4]: weight, count, min key, max key
   uint32_t* blockcnt;        // [nblocks][4] class counts (8, 4, 2, -)
   uint32_t* counts;          // [4]: n8, n4, n2, payload_units
+  const float* gmean;        // global means, original order (input of the permuted copy)
+  float* pmean;              // pmean[k] = gmean[perm[k]]
 };
 uint32_t alloc_blocks(uint32_t T);
-// Search for the crossing flip (fully on device, no host sync).
+// Search for the crossing flip and the plateau midpoint u, fully on device: one
+// cooperative launch (grid-wide syncs between histogram passes), no host sync.
 void launch_alloc_search(const float* F, uint32_t T, double alpha, uint64_t wmax, AllocWork w,
                          cudaStream_t st);
-// Widths from the float thresholds + stable width-class partition (8,4,2).
-void launch_alloc_assign(const float* F, uint32_t T, float t24, float t48, AllocWork w,
+// Widths from the float thresholds + stable width-class partition (8,4,2).  With
+// `from_state` the thresholds are read from w.state (t24/t48 of the search);
+// otherwise the given host values are used.
+void launch_alloc_assign(const float* F, uint32_t T, float t24, float t48, bool from_state, AllocWork w,
                          uint8_t* widths, uint32_t* perm, cudaStream_t st);
 void launch_fixed_assign(uint32_t T, int width, AllocWork w, uint8_t* widths, uint32_t* perm,
                          cudaStream_t st);

@@ -21,6 +21,8 @@
 #include <cfloat>
 #include <cstdint>
 
+#include <cooperative_groups.h>
+
 #include "dq_internal.h"
 
 namespace dq {
@@ -93,7 +95,7 @@ __device__ __forceinline__ uint64_t dkey(double f) {
   return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 
-__global__ void k_alloc_init(AllocState* s, uint64_t* bins, uint64_t wmax) {
+__device__ void alloc_init(AllocState* s, uint64_t* bins, uint64_t wmax) {
   const int t = threadIdx.x;
   for (int b = t; b < kAllocBins; b += blockDim.x) {
     bins[4 * b + 0] = 0;
@@ -109,8 +111,8 @@ __global__ void k_alloc_init(AllocState* s, uint64_t* bins, uint64_t wmax) {
   }
 }
 
-__global__ void k_alloc_prep(const float* __restrict__ F, uint32_t T, double alpha, double* level,
-                             AllocState* s) {
+__device__ void alloc_prep(const float* __restrict__ F, uint32_t T, double alpha, double* level,
+                           AllocState* s) {
   uint64_t kmin = ~0ull, kmax = 0;
   uint32_t npos = 0;
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < T; j += gridDim.x * blockDim.x) {
@@ -137,7 +139,7 @@ __global__ void k_alloc_prep(const float* __restrict__ F, uint32_t T, double alp
   }
 }
 
-__global__ void k_alloc_start(AllocState* s) {
+__device__ void alloc_start(AllocState* s) {
   if (s->npos == 0) {
     s->status = 3;
   } else {
@@ -146,11 +148,16 @@ __global__ void k_alloc_start(AllocState* s) {
   }
 }
 
-__global__ void __launch_bounds__(512) k_alloc_hist(const double* __restrict__ level, uint32_t T,
-                                                   const AllocState* s, uint64_t* bins) {
-  if (s->status != 0) return;
-  __shared__ uint32_t bw[kAllocBins], bc[kAllocBins];
-  __shared__ unsigned long long bmn[kAllocBins], bmx[kAllocBins];
+struct HistSmem {
+  uint32_t bw[kAllocBins], bc[kAllocBins];
+  unsigned long long bmn[kAllocBins], bmx[kAllocBins];
+};
+__device__ void alloc_hist(const double* __restrict__ level, uint32_t T, const AllocState* s, uint64_t* bins,
+                           HistSmem& hs) {
+  uint32_t* bw = hs.bw;
+  uint32_t* bc = hs.bc;
+  unsigned long long* bmn = hs.bmn;
+  unsigned long long* bmx = hs.bmx;
   for (int b = threadIdx.x; b < kAllocBins; b += blockDim.x) {
     bw[b] = 0;
     bc[b] = 0;
@@ -187,11 +194,10 @@ __global__ void __launch_bounds__(512) k_alloc_hist(const double* __restrict__ l
   }
 }
 
-__global__ void __launch_bounds__(kAllocBins) k_alloc_scan(AllocState* s, uint64_t* bins) {
+__device__ void alloc_scan(AllocState* s, uint64_t* bins) {  // one CTA of kAllocBins threads
   __shared__ uint64_t wsum[32];
   __shared__ uint32_t cross_bin;
   __shared__ unsigned long long pred_max;
-  if (s->status != 0) return;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const uint64_t w = bins[4 * t], c = bins[4 * t + 1], mn = bins[4 * t + 2], mx = bins[4 * t + 3];
   bins[4 * t] = 0;
@@ -247,8 +253,8 @@ __global__ void __launch_bounds__(kAllocBins) k_alloc_scan(AllocState* s, uint64
 }
 
 // Find an F_j behind each flip key the host needs (crossing, predecessor, largest).
-__global__ void k_alloc_identify(const double* __restrict__ level, const float* __restrict__ F, uint32_t T,
-                                 AllocState* s) {
+__device__ void alloc_identify(const double* __restrict__ level, const float* __restrict__ F, uint32_t T,
+                               AllocState* s) {
   const uint32_t status = s->status;
   if (status != 1 && status != 2) return;
   const uint64_t ck = s->cross_key, pk = s->pred_key, mk = s->kmax;
@@ -269,18 +275,64 @@ __global__ void k_alloc_identify(const double* __restrict__ level, const float* 
 
 uint32_t alloc_blocks(uint32_t T) { return (T + 2047) / 2048; }
 
+// u and the thresholds on device (CUDA libm), mirroring fast_sample_points /
+// fast_threshold_* (allocation.cpp:170-224); the host re-derives them with glibc.
+__device__ void alloc_finish(AllocState* s, double alpha) {
+  auto flip = [&](uint32_t fbits, uint32_t type) {
+    return __dsub_rn(type ? 8.0 : 4.0, __dmul_rn(alpha, log2(static_cast<double>(__uint_as_float(fbits)))));
+  };
+  double u = 0.0;
+  if (s->status == 2) u = __dadd_rn(flip(s->max_f, 1), 1.0);
+  else if (s->status == 1)
+    u = s->has_pred ? __dmul_rn(0.5, __dadd_rn(flip(s->pred_f, s->pred_t), flip(s->cross_f, s->cross_t)))
+                    : __dsub_rn(flip(s->cross_f, s->cross_t), 1.0);
+  u = u < -1e6 ? -1e6 : (u > 1e6 ? 1e6 : u);
+  s->u = u;
+  s->t24 = static_cast<float>(exp2(__ddiv_rn(__dsub_rn(4.0, u), alpha)));
+  s->t48 = static_cast<float>(exp2(__ddiv_rn(__dsub_rn(8.0, u), alpha)));
+}
+
+// The whole search in one cooperative launch: prep -> up to kAllocMaxPasses x
+// (histogram on every CTA, scan on CTA 0) -> identify -> finish, with grid-wide
+// syncs in between (every CTA reads the same state after each sync, so the
+// early exit is uniform).
+__global__ void __launch_bounds__(kAllocBins) k_alloc_coop(const float* __restrict__ F, uint32_t T, double alpha,
+                                                           uint64_t wmax, AllocWork w) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ HistSmem hs;
+  if (blockIdx.x == 0) alloc_init(w.state, w.bins, wmax);
+  grid.sync();
+  alloc_prep(F, T, alpha, w.level, w.state);
+  grid.sync();
+  if (blockIdx.x == 0 && threadIdx.x == 0) alloc_start(w.state);
+  grid.sync();
+  for (int p = 0; p < kAllocMaxPasses; ++p) {
+    if (w.state->status != 0) break;
+    alloc_hist(w.level, T, w.state, w.bins, hs);
+    grid.sync();
+    if (blockIdx.x == 0) alloc_scan(w.state, w.bins);
+    grid.sync();
+  }
+  alloc_identify(w.level, F, T, w.state);
+  grid.sync();
+  if (blockIdx.x == 0 && threadIdx.x == 0) alloc_finish(w.state, alpha);
+}
+
 void launch_alloc_search(const float* F, uint32_t T, double alpha, uint64_t wmax, AllocWork w,
                          cudaStream_t st) {
-  k_alloc_init<<<1, 256, 0, st>>>(w.state, w.bins, wmax);
-  const uint32_t grid = T ? (T + 511) / 512 < 1184 ? (T + 511) / 512 : 1184 : 1;
-  k_alloc_prep<<<grid, 512, 0, st>>>(F, T, alpha, w.level, w.state);
-  k_alloc_start<<<1, 1, 0, st>>>(w.state);
-  const uint32_t hgrid = T ? ((T + 4095) / 4096 < 296 ? (T + 4095) / 4096 : 296) : 1;
-  for (int p = 0; p < kAllocMaxPasses; ++p) {
-    k_alloc_hist<<<hgrid, 512, 0, st>>>(w.level, T, w.state, w.bins);
-    k_alloc_scan<<<1, kAllocBins, 0, st>>>(w.state, w.bins);
+  static int max_blocks = 0;
+  if (!max_blocks) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_alloc_coop, kAllocBins, 0);
+    max_blocks = sms * (per_sm > 0 ? per_sm : 1);
   }
-  k_alloc_identify<<<grid, 512, 0, st>>>(w.level, F, T, w.state);
+  const uint32_t want = T ? (T + 4 * kAllocBins - 1) / (4 * kAllocBins) : 1;
+  const uint32_t grid = want < static_cast<uint32_t>(max_blocks) ? want : static_cast<uint32_t>(max_blocks);
+  void* args[] = {const_cast<float**>(&F), &T, &alpha, &wmax, &w};
+  cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_alloc_coop), dim3(grid), dim3(kAllocBins), args, 0, st);
 }
 
 // ---------------------------------------------------- width assignment
@@ -314,8 +366,12 @@ __device__ __forceinline__ uint64_t block_excl_scan_u64(uint64_t v, uint64_t* to
 
 template <bool FIXED>
 __global__ void __launch_bounds__(256) k_assign_count(const float* __restrict__ F, uint32_t T, float t24,
-                                                      float t48, int fixed_cls, uint8_t* widths,
-                                                      uint32_t* blockcnt) {
+                                                      float t48, const AllocState* st_thr, int fixed_cls,
+                                                      uint8_t* widths, uint32_t* blockcnt) {
+  if (st_thr) {
+    t24 = st_thr->t24;
+    t48 = st_thr->t48;
+  }
   const uint32_t j0 = blockIdx.x * 2048 + threadIdx.x * 8;
   uint64_t packed = 0;  // 16-bit counts per class
   for (int k = 0; k < 8; ++k) {
@@ -374,8 +430,13 @@ __global__ void __launch_bounds__(1024) k_assign_scan(uint32_t nb, uint32_t* blo
 
 template <bool FIXED>
 __global__ void __launch_bounds__(256) k_assign_scatter(const float* __restrict__ F, uint32_t T, float t24,
-                                                        float t48, int fixed_cls, const uint32_t* blockcnt,
-                                                        const uint32_t* counts, uint32_t* perm) {
+                                                        float t48, const AllocState* st_thr, int fixed_cls,
+                                                        const uint32_t* blockcnt, const uint32_t* counts,
+                                                        uint32_t* perm, const float* gmean, float* pmean) {
+  if (st_thr) {
+    t24 = st_thr->t24;
+    t48 = st_thr->t48;
+  }
   const uint32_t j0 = blockIdx.x * 2048 + threadIdx.x * 8;
   int cls[8];
   uint64_t packed = 0;
@@ -391,28 +452,34 @@ __global__ void __launch_bounds__(256) k_assign_scatter(const float* __restrict_
   for (int c = 0; c < 3; ++c)
     pos[c] = base[c] + blockcnt[4 * blockIdx.x + c] + static_cast<uint32_t>((excl >> (16 * c)) & 0xffff);
   for (int k = 0; k < 8; ++k)
-    if (cls[k] < 3) perm[pos[cls[k]]++] = j0 + k;
+    if (cls[k] < 3) {
+      const uint32_t at = pos[cls[k]]++;
+      perm[at] = j0 + k;
+      if (pmean) pmean[at] = gmean[j0 + k];
+    }
 }
 
-static void assign_impl(const float* F, uint32_t T, float t24, float t48, int fixed_cls, bool fixed,
-                        AllocWork w, uint8_t* widths, uint32_t* perm, cudaStream_t st) {
+static void assign_impl(const float* F, uint32_t T, float t24, float t48, const AllocState* thr, int fixed_cls,
+                        bool fixed, AllocWork w, uint8_t* widths, uint32_t* perm, cudaStream_t st) {
   const uint32_t nb = alloc_blocks(T);
   if (nb == 0) return;
-  if (fixed) k_assign_count<true><<<nb, 256, 0, st>>>(F, T, t24, t48, fixed_cls, widths, w.blockcnt);
-  else k_assign_count<false><<<nb, 256, 0, st>>>(F, T, t24, t48, fixed_cls, widths, w.blockcnt);
+  if (fixed) k_assign_count<true><<<nb, 256, 0, st>>>(F, T, t24, t48, thr, fixed_cls, widths, w.blockcnt);
+  else k_assign_count<false><<<nb, 256, 0, st>>>(F, T, t24, t48, thr, fixed_cls, widths, w.blockcnt);
   k_assign_scan<<<1, 1024, 0, st>>>(nb, w.blockcnt, w.counts);
-  if (fixed) k_assign_scatter<true><<<nb, 256, 0, st>>>(F, T, t24, t48, fixed_cls, w.blockcnt, w.counts, perm);
-  else k_assign_scatter<false><<<nb, 256, 0, st>>>(F, T, t24, t48, fixed_cls, w.blockcnt, w.counts, perm);
+  if (fixed)
+    k_assign_scatter<true><<<nb, 256, 0, st>>>(F, T, t24, t48, thr, fixed_cls, w.blockcnt, w.counts, perm, w.gmean, w.pmean);
+  else
+    k_assign_scatter<false><<<nb, 256, 0, st>>>(F, T, t24, t48, thr, fixed_cls, w.blockcnt, w.counts, perm, w.gmean, w.pmean);
 }
 
-void launch_alloc_assign(const float* F, uint32_t T, float t24, float t48, AllocWork w, uint8_t* widths,
-                         uint32_t* perm, cudaStream_t st) {
-  assign_impl(F, T, t24, t48, 0, false, w, widths, perm, st);
+void launch_alloc_assign(const float* F, uint32_t T, float t24, float t48, bool from_state, AllocWork w,
+                         uint8_t* widths, uint32_t* perm, cudaStream_t st) {
+  assign_impl(F, T, t24, t48, from_state ? w.state : nullptr, 0, false, w, widths, perm, st);
 }
 
 void launch_fixed_assign(uint32_t T, int width, AllocWork w, uint8_t* widths, uint32_t* perm,
                          cudaStream_t st) {
-  assign_impl(nullptr, T, 0.f, 0.f, width == 8 ? 0 : (width == 4 ? 1 : 2), true, w, widths, perm, st);
+  assign_impl(nullptr, T, 0.f, 0.f, nullptr, width == 8 ? 0 : (width == 4 ? 1 : 2), true, w, widths, perm, st);
 }
 
 // ------------------------------------------------------------------ vNMSE
