@@ -933,36 +933,46 @@ void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info
       DQ_CUDA(cudaGetLastError());
     }
   }
-  // all-gather of the sink-compressed chunks (sink of chunk ch is rank ch)
-  timed(ctx, K_NCCL, static_cast<double>(lays[me].bytes()) * (n - 1), st, [&] {
-    DQ_NCCL(ncclGroupStart());
-    for (uint32_t peer = 0; peer < n; ++peer) {
-      if (peer == me) continue;
-      DQ_NCCL(ncclSend(mysink, lays[me].bytes(), ncclUint8, peer, ctx->comm, st));
-      DQ_NCCL(ncclRecv(buf(3, peer), lays[peer].bytes(), ncclUint8, peer, ctx->comm, st));
-    }
-    DQ_NCCL(ncclGroupEnd());
-  });
-  {
+  // all-gather of the sink-compressed chunks (sink of chunk ch is rank ch), overlapped
+  // with decode: the bytes are forwarded verbatim (engine.cpp:219-229) peer by peer on
+  // the comm stream (step k: send to me+k, receive from me-k over NVSwitch) while the
+  // compute stream decodes every chunk that has arrived, fused with unpermute +
+  // denormalize into the output.
+  if (!ctx->cs) DQ_CUDA(cudaStreamCreateWithFlags(&ctx->cs, cudaStreamNonBlocking));
+  while (ctx->pipe_ev.size() < 2ull * n * ctx->pieces + 4 + n) {
+    cudaEvent_t e;
+    DQ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->pipe_ev.push_back(e);
+  }
+  cudaEvent_t* gev = ctx->pipe_ev.data() + 2ull * n * ctx->pieces + 4;
+  auto decode_one = [&](uint32_t ch, const uint8_t* src) {
     GatherArgs g{};
-    uint32_t max_nsg_g = 0;
-    double gbytes = 0;
-    for (uint32_t ch = 0; ch < n; ++ch) {
-      g.in[ch] = ch == me ? mysink : buf(3, ch);
-      g.lo[ch] = p.lo[ch];
-      g.n8[ch] = lays[ch].n8;
-      g.n4[ch] = lays[ch].n4;
-      max_nsg_g = std::max(max_nsg_g, lays[ch].nsg);
-      gbytes += 1032.0 * lays[ch].nsg + lays[ch].bytes();
-    }
-    g.lo[n] = p.lo[n];
+    g.in[0] = src;
+    g.lo[0] = p.lo[ch];
+    g.lo[1] = p.lo[ch + 1];
+    g.n8[0] = lays[ch].n8;
+    g.n4[0] = lays[ch].n4;
     g.perm = ctx->perm.p;
     g.gmean = ctx->pmean.p;
     g.out = out;
     g.d = d;
     g.n_workers_f = static_cast<float>(n);
     g.uniform_books = c.non_uniform ? 0 : 1;
-    timed(ctx, K_DECODE, gbytes, st, [&] { launch_gather_decode(g, n, max_nsg_g, st); });
+    timed(ctx, K_DECODE, 1032.0 * lays[ch].nsg + lays[ch].bytes(), st,
+          [&] { launch_gather_decode(g, 1, lays[ch].nsg, st); });
+  };
+  DQ_CUDA(cudaEventRecord(gev[0], st));  // this rank's sink chunk is complete
+  DQ_CUDA(cudaStreamWaitEvent(ctx->cs, gev[0], 0));
+  decode_one(me, mysink);
+  for (uint32_t k = 1; k < n; ++k) {
+    const uint32_t to = (me + k) % n, from = (me + n - k) % n;
+    DQ_NCCL(ncclGroupStart());
+    DQ_NCCL(ncclSend(mysink, lays[me].bytes(), ncclUint8, to, ctx->comm, ctx->cs));
+    DQ_NCCL(ncclRecv(buf(3, from), lays[from].bytes(), ncclUint8, from, ctx->comm, ctx->cs));
+    DQ_NCCL(ncclGroupEnd());
+    DQ_CUDA(cudaEventRecord(gev[k], ctx->cs));
+    DQ_CUDA(cudaStreamWaitEvent(st, gev[k], 0));
+    decode_one(from, buf(3, from));
   }
   for (uint32_t ch = 0; ch < n; ++ch) {
     for (uint32_t g = 0; g < plans[ch].n_gat; ++g) account(info, lays[ch], g == 0);
