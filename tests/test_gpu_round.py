@@ -56,6 +56,14 @@ def test_round_matches_oracle(dq, port, topo, n, b):
     _check_round(dq, port, ws, _cfg(dq, n, b, topo), port.round_cfg(n, b, topo, seed=1))
 
 
+@pytest.mark.parametrize("n,topo", [(16, "ring"), (16, "butterfly"), (12, "ring")])
+def test_more_than_eight_workers(dq, port, n, topo):
+    """n_slots > 8 takes the runtime-n permutation path of the fused kernels."""
+    d = 1 << 14
+    ws = _workers(port, n, d, seed=31)
+    _check_round(dq, port, ws, _cfg(dq, n, 4, topo, seed=6), port.round_cfg(n, 4, topo, seed=6))
+
+
 @pytest.mark.parametrize("n", [3, 5, 7])
 def test_ring_odd_worker_counts(dq, port, n):
     d = (1 << 14) + 77  # padding in the last super-group
