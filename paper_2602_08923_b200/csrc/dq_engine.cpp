@@ -963,16 +963,40 @@ void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info
   };
   DQ_CUDA(cudaEventRecord(gev[0], st));  // this rank's sink chunk is complete
   DQ_CUDA(cudaStreamWaitEvent(ctx->cs, gev[0], 0));
-  decode_one(me, mysink);
+  // one all-to-all group: every peer link of the NVSwitch busy at once
+  DQ_NCCL(ncclGroupStart());
   for (uint32_t k = 1; k < n; ++k) {
     const uint32_t to = (me + k) % n, from = (me + n - k) % n;
-    DQ_NCCL(ncclGroupStart());
     DQ_NCCL(ncclSend(mysink, lays[me].bytes(), ncclUint8, to, ctx->comm, ctx->cs));
     DQ_NCCL(ncclRecv(buf(3, from), lays[from].bytes(), ncclUint8, from, ctx->comm, ctx->cs));
-    DQ_NCCL(ncclGroupEnd());
-    DQ_CUDA(cudaEventRecord(gev[k], ctx->cs));
-    DQ_CUDA(cudaStreamWaitEvent(st, gev[k], 0));
-    decode_one(from, buf(3, from));
+  }
+  DQ_NCCL(ncclGroupEnd());
+  DQ_CUDA(cudaEventRecord(gev[1], ctx->cs));
+  decode_one(me, mysink);  // overlaps the exchange
+  DQ_CUDA(cudaStreamWaitEvent(st, gev[1], 0));
+  {
+    GatherArgs g{};
+    uint32_t k = 0, max_nsg_g = 0;
+    double gbytes = 0;
+    for (uint32_t ch = 0; ch < n; ++ch) {
+      if (ch == me) continue;
+      g.in[k] = buf(3, ch);
+      g.lo[k] = p.lo[ch];  // chunks of this list are not adjacent: explicit ends in hi[]
+      g.n8[k] = lays[ch].n8;
+      g.n4[k] = lays[ch].n4;
+      g.hi[k] = p.lo[ch + 1];
+      max_nsg_g = std::max(max_nsg_g, lays[ch].nsg);
+      gbytes += 1032.0 * lays[ch].nsg + lays[ch].bytes();
+      ++k;
+    }
+    g.perm = ctx->perm.p;
+    g.gmean = ctx->pmean.p;
+    g.out = out;
+    g.d = d;
+    g.n_workers_f = static_cast<float>(n);
+    g.uniform_books = c.non_uniform ? 0 : 1;
+    g.use_hi = 1;
+    timed(ctx, K_DECODE, gbytes, st, [&] { launch_gather_decode(g, k, max_nsg_g, st); });
   }
   for (uint32_t ch = 0; ch < n; ++ch) {
     for (uint32_t g = 0; g < plans[ch].n_gat; ++g) account(info, lays[ch], g == 0);

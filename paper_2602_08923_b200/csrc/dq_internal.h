@@ -31,7 +31,9 @@ struct CodecArgs {
 // All chunks of a round decoded into the output gradient in one launch.
 struct GatherArgs {
   const uint8_t* in[64];     // compressed chunk c (dq tiled SoA)
-  uint32_t lo[65];           // chunk c = permuted super-groups [lo[c], lo[c+1])
+  uint32_t lo[65];           // chunk c = permuted super-groups [lo[c], lo[c+1]) (or [lo[c], hi[c]))
+  uint32_t hi[64];           // explicit end of chunk c when use_hi (non-adjacent chunk lists)
+  int use_hi;
   uint32_t n8[64], n4[64];   // width runs of chunk c
   const uint32_t* perm;
   const float* gmean;        // permuted order
