@@ -179,6 +179,10 @@ struct dq_ctx {
   uint32_t last_T = 0;
   uint64_t alloc_redos = 0;  // rounds where the device thresholds differed from glibc's
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // round-boundary events of the last asynchronously finished round (measured at the next sync)
+  cudaEvent_t lr0 = nullptr, lr1 = nullptr;
+  bool lr_pending = false;
+  double last_round_ms = 0.0;
   // per-kernel-family device timing (CUDA events bracketing each launch)
   struct Prof {
     int kind;
@@ -202,6 +206,8 @@ struct dq_ctx {
     if (h_vn) cudaFreeHost(h_vn);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
+    if (lr0) cudaEventDestroy(lr0);
+    if (lr1) cudaEventDestroy(lr1);
     if (comm) ncclCommDestroy(comm);
     if (cs) cudaStreamDestroy(cs);
     for (cudaEvent_t e : pipe_ev) cudaEventDestroy(e);
@@ -252,6 +258,12 @@ void timed(dq_ctx* ctx, int kind, double bytes, cudaStream_t st, F&& launch) {
 
 // after a stream sync: fold the pending event pairs into the per-kind totals
 void harvest(dq_ctx* ctx) {
+  if (ctx->lr_pending && cudaEventQuery(ctx->lr1) == cudaSuccess) {
+    float ms = 0.f;
+    DQ_CUDA(cudaEventElapsedTime(&ms, ctx->lr0, ctx->lr1));
+    ctx->last_round_ms = ms;
+    ctx->lr_pending = false;
+  }
   for (auto& p : ctx->pending) {
     float ms = 0.f;
     DQ_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
@@ -261,6 +273,20 @@ void harvest(dq_ctx* ctx) {
     ctx->ev_pool.push_back(p.b);
   }
   ctx->pending.clear();
+}
+
+// A round returned without a host sync: keep its boundary events for the next sync
+// (ev0/ev1 are re-recorded by the next round, so copy them into lr0/lr1 on the GPU
+// timeline by recording the copies right here) and report the previous round's time.
+void finish_async(dq_ctx* ctx, dq_round_info* info) {
+  if (!ctx->lr0) {
+    DQ_CUDA(cudaEventCreate(&ctx->lr0));
+    DQ_CUDA(cudaEventCreate(&ctx->lr1));
+  }
+  std::swap(ctx->ev0, ctx->lr0);  // lr0 := this round's start event
+  std::swap(ctx->ev1, ctx->lr1);  // lr1 := this round's end event
+  ctx->lr_pending = true;
+  info->ms_total = ctx->last_round_ms;
 }
 
 double quant_bytes(const Layout& L, bool dar) {  // local fp32 + mean/perm + in (DAR) + out
@@ -352,6 +378,7 @@ AllocResult allocate(dq_ctx* ctx, const dq_config& c, const float* dF, uint32_t 
   DQ_CUDA(cudaMemcpyAsync(ctx->h_state, w.state, sizeof(AllocState), cudaMemcpyDeviceToHost, st));
   DQ_CUDA(cudaMemcpyAsync(ctx->h_counts, w.counts, 3 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   DQ_CUDA(cudaStreamSynchronize(st));
+  harvest(ctx);  // events of the previous round (finished asynchronously) are complete now
   const AllocState s = *ctx->h_state;
   // the flips adjacent to the chosen plateau, recomputed with the host libm exactly as
   // fast_sample_points does (allocation.cpp:201-224)
@@ -657,12 +684,8 @@ void sim_round(dq_ctx* ctx, const float* const* xs, size_t d, float* out, int fl
     DQ_CUDA(cudaGetLastError());
   }
   DQ_CUDA(cudaEventRecord(ctx->ev1, st));
-  if (flags & DQ_SIM_NO_METRICS) {
-    DQ_CUDA(cudaStreamSynchronize(st));
-    harvest(ctx);
-    float ms = 0.f;
-    DQ_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
-    info->ms_total = ms;
+  if (flags & DQ_SIM_NO_METRICS) {  // asynchronous return: timing resolved at the next sync point
+    finish_async(ctx, info);
     return;
   }
   // vNMSE against the fp64 sum of the inputs (metrics, not part of the timed path)
@@ -1005,13 +1028,7 @@ void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info
   }
   DQ_CUDA(cudaGetLastError());
   DQ_CUDA(cudaEventRecord(ctx->ev1, st));
-  if (ctx->profile) {
-    DQ_CUDA(cudaStreamSynchronize(st));
-    harvest(ctx);
-    float ms = 0.f;
-    DQ_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
-    info->ms_total = ms;
-  }
+  finish_async(ctx, info);
 }
 
 }  // namespace
@@ -1326,6 +1343,9 @@ int dq_profile_enable(dq_ctx* ctx, int on) {
 int dq_profile_read(dq_ctx* ctx, dq_kernel_profile* out, int cap, int* count, int reset) {
   return guarded([&] {
     if (!ctx) invalid("null context");
+    DQ_CUDA(cudaSetDevice(ctx->device));
+    DQ_CUDA(cudaDeviceSynchronize());
+    harvest(ctx);
     int k = 0;
     for (int i = 0; i < K_NKINDS; ++i) {
       if (!ctx->prof_launches[i] && !ctx->prof_ms[i]) continue;
