@@ -371,7 +371,8 @@ AllocResult allocate(dq_ctx* ctx, const dq_config& c, const float* dF, uint32_t 
   if (W < 0) throw Error(DQ_EINFEASIBLE, "bit allocation infeasible within budget");
   // search + device thresholds, assignment with the device thresholds, then ONE sync that
   // brings back the state and the class counts together
-  timed(ctx, K_ALLOC_SEARCH, 8.0 * T, st, [&] { launch_alloc_search(dF, T, kAlpha, static_cast<uint64_t>(W), w, st); });
+  timed(ctx, K_ALLOC_SEARCH, 8.0 * T, st,
+        [&] { DQ_CUDA(launch_alloc_search(dF, T, kAlpha, static_cast<uint64_t>(W), w, st)); });
   DQ_CUDA(cudaGetLastError());
   timed(ctx, K_ALLOC_ASSIGN, 13.0 * T, st, [&] { launch_alloc_assign(dF, T, 0.f, 0.f, true, w, dW, dP, st); });
   DQ_CUDA(cudaGetLastError());

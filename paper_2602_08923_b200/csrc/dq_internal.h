@@ -94,8 +94,8 @@ struct AllocWork {           // device scratch owned by the context
 uint32_t alloc_blocks(uint32_t T);
 // Search for the crossing flip and the plateau midpoint u, fully on device: one
 // cooperative launch (grid-wide syncs between histogram passes), no host sync.
-void launch_alloc_search(const float* F, uint32_t T, double alpha, uint64_t wmax, AllocWork w,
-                         cudaStream_t st);
+cudaError_t launch_alloc_search(const float* F, uint32_t T, double alpha, uint64_t wmax, AllocWork w,
+                                cudaStream_t st);
 // Widths from the float thresholds + stable width-class partition (8,4,2).  With
 // `from_state` the thresholds are read from w.state (t24/t48 of the search);
 // otherwise the given host values are used.

@@ -319,8 +319,8 @@ __global__ void __launch_bounds__(kAllocBins) k_alloc_coop(const float* __restri
   if (blockIdx.x == 0 && threadIdx.x == 0) alloc_finish(w.state, alpha);
 }
 
-void launch_alloc_search(const float* F, uint32_t T, double alpha, uint64_t wmax, AllocWork w,
-                         cudaStream_t st) {
+cudaError_t launch_alloc_search(const float* F, uint32_t T, double alpha, uint64_t wmax, AllocWork w,
+                                cudaStream_t st) {
   static int max_blocks = 0;
   if (!max_blocks) {
     int dev = 0, sms = 0, per_sm = 0;
@@ -332,7 +332,7 @@ void launch_alloc_search(const float* F, uint32_t T, double alpha, uint64_t wmax
   const uint32_t want = T ? (T + 4 * kAllocBins - 1) / (4 * kAllocBins) : 1;
   const uint32_t grid = want < static_cast<uint32_t>(max_blocks) ? want : static_cast<uint32_t>(max_blocks);
   void* args[] = {const_cast<float**>(&F), &T, &alpha, &wmax, &w};
-  cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_alloc_coop), dim3(grid), dim3(kAllocBins), args, 0, st);
+  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_alloc_coop), dim3(grid), dim3(kAllocBins), args, 0, st);
 }
 
 // ---------------------------------------------------- width assignment
