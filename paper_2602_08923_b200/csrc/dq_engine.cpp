@@ -415,7 +415,15 @@ AllocResult allocate(dq_ctx* ctx, const dq_config& c, const float* dF, uint32_t 
   r.n2 = ctx->h_counts[2];
   r.passes = s.passes;
   r.payload = static_cast<uint64_t>(S) * (8ull * r.n8 + 4ull * r.n4 + 2ull * r.n2);
-  if (static_cast<double>(r.payload) > budget) throw Error(DQ_EINFEASIBLE, "bit allocation infeasible within budget");
+  if (static_cast<double>(r.payload) > budget) {
+    char m[512];
+    std::snprintf(m, sizeof m,
+                  "bit allocation infeasible within budget (T=%u W=%lld status=%u passes=%u has_pred=%u "
+                  "u=%.17g t24=%a/%a t48=%a/%a counts=%u,%u,%u payload=%llu budget=%.17g)",
+                  T, static_cast<long long>(W), s.status, s.passes, s.has_pred, u, t24, s.t24, t48, s.t48, r.n8,
+                  r.n4, r.n2, static_cast<unsigned long long>(r.payload), budget);
+    throw Error(DQ_EINFEASIBLE, m);
+  }
   return r;
 }
 
@@ -753,8 +761,12 @@ uint8_t* ring_pipelined(dq_ctx* ctx, const Prepared& pr, const std::vector<Codec
   const uint32_t n = ctx->cfg.n_workers, me = static_cast<uint32_t>(ctx->rank);
   const uint32_t right = (me + 1) % n, left = (me + n - 1) % n;
   if (!ctx->cs) DQ_CUDA(cudaStreamCreateWithFlags(&ctx->cs, cudaStreamNonBlocking));
-  const int P = ctx->pieces;
-  const size_t nev = 2ull * n * P + 2;
+  // pieces per chunk: enough to overlap transfers with the fused kernels on big
+  // chunks, one on small ones (each piece costs a launch + an NCCL group).  Derived
+  // from the round-global max chunk size, so every rank splits identically.
+  const size_t piece_target = 8u << 20;
+  const int P = static_cast<int>(std::max<size_t>(1, std::min<size_t>(ctx->pieces, mb / piece_target)));
+  const size_t nev = 2ull * n * ctx->pieces + 2;
   while (ctx->pipe_ev.size() < nev) {
     cudaEvent_t e;
     DQ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));

@@ -11,8 +11,6 @@ Each call advances SharedSeed.round so successive rounds draw fresh shared
 randomness (proj/include/dynamiq/random.hpp:12-15).  The hook returns the mean
 (sum estimate / world size), like DDP's default all-reduce hook.
 """
-from __future__ import annotations
-
 import torch
 import torch.distributed as dist
 
@@ -28,7 +26,7 @@ class DynamiQHookState:
                                      seed=SharedSeed(seed, 0))
         self.comm = Communicator(self.config, self.rank, self.world_size, group=group)
         self.round = 0
-        self.last_info: dict = {}
+        self.last_info = {}
 
     def next_round(self) -> None:
         self.config.seed = SharedSeed(self.config.seed.seed, self.round)
@@ -36,7 +34,7 @@ class DynamiQHookState:
         self.round += 1
 
 
-def dynamiq_hook(state: DynamiQHookState, bucket) -> torch.futures.Future:
+def dynamiq_hook(state: DynamiQHookState, bucket: dist.GradBucket) -> torch.futures.Future[torch.Tensor]:
     buf = bucket.buffer()
     x = buf if buf.dtype == torch.float32 else buf.float()
     state.next_round()
@@ -45,6 +43,6 @@ def dynamiq_hook(state: DynamiQHookState, bucket) -> torch.futures.Future:
     out.div_(state.world_size)
     if buf.dtype != torch.float32:
         out = out.to(buf.dtype)
-    fut: torch.futures.Future = torch.futures.Future()
+    fut = torch.futures.Future()
     fut.set_result(out)
     return fut
