@@ -168,6 +168,8 @@ struct dq_ctx {
   DevBuf<AllocState> astate;
   DevBuf<uint64_t> bins;
   DevBuf<uint32_t> blockcnt, counts;
+  DevBuf<FlipRec> nrec;                 // slow allocation path scratch
+  DevBuf<unsigned long long> tcount;
   DevBuf<const float*> xptrs;
   DevBuf<double> vn;
   DevBuf<uint8_t> msgs;   // message pool
@@ -369,11 +371,10 @@ AllocResult allocate(dq_ctx* ctx, const dq_config& c, const float* dF, uint32_t 
   while (fits(W + 1)) ++W;
   while (W >= 0 && !fits(W)) --W;
   if (W < 0) throw Error(DQ_EINFEASIBLE, "bit allocation infeasible within budget");
-  // search + device thresholds, assignment with the device thresholds, then ONE sync that
-  // brings back the state and the class counts together
+  // search + neighbourhood decision on device, assignment with the device thresholds,
+  // then ONE sync that brings back the state and the class counts together
   timed(ctx, K_ALLOC_SEARCH, 8.0 * T, st,
-        [&] { DQ_CUDA(launch_alloc_search(dF, T, kAlpha, static_cast<uint64_t>(W), w, st)); });
-  DQ_CUDA(cudaGetLastError());
+        [&] { DQ_CUDA(launch_alloc_search(dF, T, kAlpha, static_cast<uint64_t>(W), budget, S, w, st)); });
   timed(ctx, K_ALLOC_ASSIGN, 13.0 * T, st, [&] { launch_alloc_assign(dF, T, 0.f, 0.f, true, w, dW, dP, st); });
   DQ_CUDA(cudaGetLastError());
   DQ_CUDA(cudaMemcpyAsync(ctx->h_state, w.state, sizeof(AllocState), cudaMemcpyDeviceToHost, st));
@@ -381,29 +382,133 @@ AllocResult allocate(dq_ctx* ctx, const dq_config& c, const float* dF, uint32_t 
   DQ_CUDA(cudaStreamSynchronize(st));
   harvest(ctx);  // events of the previous round (finished asynchronously) are complete now
   const AllocState s = *ctx->h_state;
-  // the flips adjacent to the chosen plateau, recomputed with the host libm exactly as
-  // fast_sample_points does (allocation.cpp:201-224)
-  auto flip = [](uint32_t fbits, uint32_t type) {
+  if (s.status == 0 || s.status > 3)
+    throw Error(DQ_ECUDA, "allocation search did not converge (status " + std::to_string(s.status) + ")");
+  // Re-derive every candidate with the host libm exactly as fast_sample_points /
+  // fast_threshold_* do (allocation.cpp:170-224).  Identical thresholds => identical
+  // float-threshold counts => the device's choice is the reference's.
+  auto hflip = [](const FlipRec& r) {
     float f;
-    std::memcpy(&f, &fbits, 4);
-    const double l = kAlpha * std::log2(static_cast<double>(f));
-    return (type ? 8.0 : 4.0) - l;
+    std::memcpy(&f, &r.fbits, 4);
+    return (r.type ? 8.0 : 4.0) - kAlpha * std::log2(static_cast<double>(f));
   };
-  double u;
-  switch (s.status) {
-    case 3: u = 0.0; break;                                  // no positive F (allocation.cpp:212-215)
-    case 2: u = flip(s.max_f, 1) + 1.0; break;               // every flip fits: flips.back() + 1
-    case 1:
-      u = s.has_pred ? 0.5 * (flip(s.pred_f, s.pred_t) + flip(s.cross_f, s.cross_t))
-                     : flip(s.cross_f, s.cross_t) - 1.0;     // plateau midpoint / flips.front() - 1
-      break;
-    default: throw Error(DQ_ECUDA, "allocation search did not converge (status " + std::to_string(s.status) + ")");
+  struct Sample {
+    bool has_l = false, has_r = false;
+    FlipRec l{}, r{};
+    double u() const {
+      double v = has_l && has_r ? 0.5 * (hflip_s(l) + hflip_s(r)) : has_r ? hflip_s(r) - 1.0 : has_l ? hflip_s(l) + 1.0 : 0.0;
+      return v < -1e6 ? -1e6 : (v > 1e6 ? 1e6 : v);
+    }
+    static double hflip_s(const FlipRec& q) {
+      float f;
+      std::memcpy(&f, &q.fbits, 4);
+      return (q.type ? 8.0 : 4.0) - kAlpha * std::log2(static_cast<double>(f));
+    }
+  };
+  (void)hflip;
+  auto thr = [](double uu, float* a, float* b) {
+    *a = static_cast<float>(std::exp2((4.0 - uu) / kAlpha));
+    *b = static_cast<float>(std::exp2((8.0 - uu) / kAlpha));
+  };
+  Sample cand[3];  // L-1, L, L+1 as the device built them
+  if (s.status == 2) {
+    cand[1].has_l = true;
+    cand[1].l = s.slot[1];
+    cand[0].has_r = true;
+    cand[0].r = s.slot[1];
+    if (s.slot[0].present) {
+      cand[0].has_l = true;
+      cand[0].l = s.slot[0];
+    }
+  } else if (s.status == 1) {
+    cand[1].has_r = true;
+    cand[1].r = s.slot[2];
+    if (s.slot[1].present) {
+      cand[1].has_l = true;
+      cand[1].l = s.slot[1];
+      cand[0].has_r = true;
+      cand[0].r = s.slot[1];
+      if (s.slot[0].present) {
+        cand[0].has_l = true;
+        cand[0].l = s.slot[0];
+      }
+    }
+    cand[2].has_l = true;
+    cand[2].l = s.slot[2];
+    if (s.slot[3].present) {
+      cand[2].has_r = true;
+      cand[2].r = s.slot[3];
+    }
   }
-  u = u < -1e6 ? -1e6 : (u > 1e6 ? 1e6 : u);
-  const float t24 = static_cast<float>(std::exp2((4.0 - u) / kAlpha));
-  const float t48 = static_cast<float>(std::exp2((8.0 - u) / kAlpha));
-  if (t24 != s.t24 || t48 != s.t48) {  // device libm disagreed in the last place: redo with glibc's
+  bool mismatch = false;
+  for (int c = 0; c < 3; ++c) {
+    if (!s.cand_present[c]) continue;
+    float a, b;
+    thr(cand[c].u(), &a, &b);
+    mismatch |= a != s.cand_t24[c] || b != s.cand_t48[c];
+  }
+  double u;
+  float t24, t48;
+  if (!mismatch && s.choice == -2) throw Error(DQ_EINFEASIBLE, "bit allocation infeasible within budget");
+  if (!mismatch && s.choice >= 0) {
+    u = cand[s.choice].u();
+    t24 = s.t24;
+    t48 = s.t48;
+  } else {
+    // Exact host-driven walk over the samples (rare): the reference's bisection on a
+    // non-decreasing payload(u) ends at the largest sample whose float-threshold
+    // payload fits; step from the device's candidate until that boundary.
     ++ctx->alloc_redos;
+    ctx->nrec.reserve(1);
+    ctx->tcount.reserve(2);
+    auto neighbor = [&](const FlipRec& q, int dir) {
+      launch_flip_neighbor(w.level, dF, T, kAlpha, q.key, dir, ctx->nrec.p, st);
+      FlipRec out;
+      DQ_CUDA(cudaMemcpyAsync(&out, ctx->nrec.p, sizeof(FlipRec), cudaMemcpyDeviceToHost, st));
+      DQ_CUDA(cudaStreamSynchronize(st));
+      return out;
+    };
+    auto fits = [&](const Sample& sm) {
+      float a, b;
+      thr(sm.u(), &a, &b);
+      launch_threshold_counts(dF, T, a, b, ctx->tcount.p, st);
+      unsigned long long cnt[2];
+      DQ_CUDA(cudaMemcpyAsync(cnt, ctx->tcount.p, sizeof(cnt), cudaMemcpyDeviceToHost, st));
+      DQ_CUDA(cudaStreamSynchronize(st));
+      const unsigned long long pay = static_cast<unsigned long long>(S) * (2ull * T + 2ull * cnt[1] + 4ull * cnt[0]);
+      return static_cast<double>(pay) <= budget;
+    };
+    Sample cur = cand[1];
+    if (fits(cur)) {
+      while (cur.has_r) {
+        Sample nx;
+        nx.has_l = true;
+        nx.l = cur.r;
+        const FlipRec q = neighbor(cur.r, +1);
+        if (q.present) {
+          nx.has_r = true;
+          nx.r = q;
+        }
+        if (!fits(nx)) break;
+        cur = nx;
+      }
+    } else {
+      for (;;) {
+        if (!cur.has_l) throw Error(DQ_EINFEASIBLE, "bit allocation infeasible within budget");
+        Sample pv;
+        pv.has_r = true;
+        pv.r = cur.l;
+        const FlipRec q = neighbor(cur.l, -1);
+        if (q.present) {
+          pv.has_l = true;
+          pv.l = q;
+        }
+        cur = pv;
+        if (fits(cur)) break;
+      }
+    }
+    u = cur.u();
+    thr(u, &t24, &t48);
     timed(ctx, K_ALLOC_ASSIGN, 13.0 * T, st, [&] { launch_alloc_assign(dF, T, t24, t48, false, w, dW, dP, st); });
     DQ_CUDA(cudaGetLastError());
     DQ_CUDA(cudaMemcpyAsync(ctx->h_counts, w.counts, 3 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));

@@ -61,6 +61,12 @@ void launch_reduce_stats(const float* mean, const float* sq, uint32_t n, uint32_
                          float* gsq, cudaStream_t st);
 
 // ------------------------------------------------------------ allocation
+// Flips around the chosen plateau: slot 0..3 = f_{L-2}, f_{L-1}, f_L, f_{L+1} in the
+// sorted unique flip order (sample L lies between f_{L-1} and f_L).
+struct FlipRec {
+  uint64_t key;
+  uint32_t fbits, type, present, pad_;
+};
 struct AllocState {
   uint64_t klo, khi;       // key range searched by the current pass (inclusive)
   uint64_t below_w;        // total weight of flips with key < klo
@@ -72,11 +78,15 @@ struct AllocState {
   uint32_t has_pred;
   uint32_t status;         // 0 searching, 1 crossing found, 2 all flips fit, 3 no flips
   uint32_t passes;
-  // F (float bits) and flip type (0: 4 - a log2 F, 1: 8 - a log2 F) of the crossing,
-  // predecessor and largest flips, so the host recomputes them with the reference's libm
-  uint32_t cross_f, cross_t, pred_f, pred_t, max_f, pad_;
-  // the plateau midpoint and thresholds as computed on device with CUDA libm; the host
-  // recomputes them with the reference's libm and redoes the assignment on a mismatch
+  FlipRec slot[4];
+  // candidate samples L-1, L, L+1 (present[c]) with device-libm u / thresholds and the
+  // float-threshold payload counts (n8, n4 + n8) the reference's bisection would see
+  uint32_t cand_present[3];
+  double cand_u[3];
+  float cand_t24[3], cand_t48[3];
+  unsigned long long cand_n8[3], cand_n48[3];
+  int32_t choice;          // chosen candidate (0..2); -1 ambiguous (host walk); -2 infeasible
+  // chosen u and thresholds (read by the assignment kernels)
   double u;
   float t24, t48;
 };
@@ -94,8 +104,15 @@ struct AllocWork {           // device scratch owned by the context
 uint32_t alloc_blocks(uint32_t T);
 // Search for the crossing flip and the plateau midpoint u, fully on device: one
 // cooperative launch (grid-wide syncs between histogram passes), no host sync.
-cudaError_t launch_alloc_search(const float* F, uint32_t T, double alpha, uint64_t wmax, AllocWork w,
-                                cudaStream_t st);
+cudaError_t launch_alloc_search(const float* F, uint32_t T, double alpha, uint64_t wmax, double budget,
+                                uint32_t S, AllocWork w, cudaStream_t st);
+// Slow exact path helpers (rare): neighbour flip of `key` (dir -1: largest key below,
+// +1: smallest key above) -> rec; float-threshold counts -> counts[0] = #F>=t48,
+// counts[1] = #F>=t24.  Both asynchronous on st.
+void launch_flip_neighbor(const double* level, const float* F, uint32_t T, double alpha, uint64_t key, int dir,
+                          FlipRec* rec, cudaStream_t st);
+void launch_threshold_counts(const float* F, uint32_t T, float t24, float t48, unsigned long long* counts,
+                             cudaStream_t st);
 // Widths from the float thresholds + stable width-class partition (8,4,2).  With
 // `from_state` the thresholds are read from w.state (t24/t48 of the search);
 // otherwise the given host values are used.

@@ -253,74 +253,212 @@ __device__ void alloc_scan(AllocState* s, uint64_t* bins) {  // one CTA of kAllo
 }
 
 // Find an F_j behind each flip key the host needs (crossing, predecessor, largest).
-__device__ void alloc_identify(const double* __restrict__ level, const float* __restrict__ F, uint32_t T,
-                               AllocState* s) {
-  const uint32_t status = s->status;
-  if (status != 1 && status != 2) return;
-  const uint64_t ck = s->cross_key, pk = s->pred_key, mk = s->kmax;
-  const bool has_pred = s->has_pred;
+// ---- neighbourhood of the chosen plateau (exactness against the reference's
+// float-threshold bisection, allocation.cpp:238-251): the crossing flip found in
+// exact arithmetic names sample L; the reference evaluates payload(u) with float
+// thresholds, which can differ from the exact count when a flip sits within float
+// rounding of a threshold.  The candidates L-1, L, L+1 are evaluated the way the
+// reference does and the choice is made like its bisection (largest in budget).
+__device__ void alloc_slots_init(AllocState* s) {
+  for (int i = 0; i < 4; ++i) s->slot[i] = FlipRec{0, 0, 0, 0, 0};
+  s->slot[0].key = 0;      // max-below accumulator
+  s->slot[3].key = ~0ull;  // min-above accumulator
+  if (s->status == 1) {
+    s->slot[2].key = s->cross_key;
+    s->slot[2].present = 1;
+    if (s->has_pred) {
+      s->slot[1].key = s->pred_key;
+      s->slot[1].present = 1;
+    }
+  } else if (s->status == 2) {
+    s->slot[1].key = s->kmax;
+    s->slot[1].present = 1;
+  }
+}
+
+__device__ void alloc_neighbors(const double* __restrict__ level, uint32_t T, AllocState* s) {
+  const bool want_below = s->slot[1].present != 0, want_above = s->status == 1;
+  const uint64_t below = s->slot[1].key, above = s->slot[2].key;
+  unsigned long long mx = 0, mn = ~0ull;
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < T; j += gridDim.x * blockDim.x) {
     const double l = level[j];
     if (l != l) continue;
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
       const uint64_t k = dkey(__dsub_rn(t ? 8.0 : 4.0, l));
-      const uint32_t fb = __float_as_uint(F[j]);
-      if (status == 1 && k == ck) { atomicExch(&s->cross_f, fb); atomicExch(&s->cross_t, t); }
-      if (status == 1 && has_pred && k == pk) { atomicExch(&s->pred_f, fb); atomicExch(&s->pred_t, t); }
-      if (status == 2 && t == 1 && k == mk) atomicExch(&s->max_f, fb);
+      if (want_below && k < below && k > mx) mx = k;
+      if (want_above && k > above && k < mn) mn = k;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (mx) atomicMax(reinterpret_cast<unsigned long long*>(&s->slot[0].key), mx);
+    if (mn != ~0ull) atomicMin(reinterpret_cast<unsigned long long*>(&s->slot[3].key), mn);
+  }
+}
+
+__device__ void alloc_identify(const double* __restrict__ level, const float* __restrict__ F, uint32_t T,
+                               AllocState* s) {
+  uint64_t keys[4];
+  bool on[4];
+  for (int i = 0; i < 4; ++i) {
+    keys[i] = s->slot[i].key;
+    on[i] = s->slot[i].present != 0;
+  }
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < T; j += gridDim.x * blockDim.x) {
+    const double l = level[j];
+    if (l != l) continue;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const uint64_t k = dkey(__dsub_rn(t ? 8.0 : 4.0, l));
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (on[i] && k == keys[i]) {
+          atomicExch(&s->slot[i].fbits, __float_as_uint(F[j]));
+          atomicExch(&s->slot[i].type, static_cast<uint32_t>(t));
+        }
     }
   }
 }
 
-uint32_t alloc_blocks(uint32_t T) { return (T + 2047) / 2048; }
-
-// u and the thresholds on device (CUDA libm), mirroring fast_sample_points /
-// fast_threshold_* (allocation.cpp:170-224); the host re-derives them with glibc.
-__device__ void alloc_finish(AllocState* s, double alpha) {
-  auto flip = [&](uint32_t fbits, uint32_t type) {
-    return __dsub_rn(type ? 8.0 : 4.0, __dmul_rn(alpha, log2(static_cast<double>(__uint_as_float(fbits)))));
+// candidate samples L-1, L, L+1 (fast_sample_points, allocation.cpp:201-224) with
+// device-libm values; the host re-derives them with glibc and compares.
+__device__ void alloc_candidates(AllocState* s, double alpha) {
+  auto flip = [&](int i) {
+    return __dsub_rn(s->slot[i].type ? 8.0 : 4.0,
+                     __dmul_rn(alpha, log2(static_cast<double>(__uint_as_float(s->slot[i].fbits)))));
   };
-  double u = 0.0;
-  if (s->status == 2) u = __dadd_rn(flip(s->max_f, 1), 1.0);
-  else if (s->status == 1)
-    u = s->has_pred ? __dmul_rn(0.5, __dadd_rn(flip(s->pred_f, s->pred_t), flip(s->cross_f, s->cross_t)))
-                    : __dsub_rn(flip(s->cross_f, s->cross_t), 1.0);
-  u = u < -1e6 ? -1e6 : (u > 1e6 ? 1e6 : u);
-  s->u = u;
-  s->t24 = static_cast<float>(exp2(__ddiv_rn(__dsub_rn(4.0, u), alpha)));
-  s->t48 = static_cast<float>(exp2(__ddiv_rn(__dsub_rn(8.0, u), alpha)));
+  auto mid = [](double a, double b) { return __dmul_rn(0.5, __dadd_rn(a, b)); };
+  for (int c = 0; c < 3; ++c) {
+    s->cand_present[c] = 0;
+    s->cand_u[c] = 0.0;
+  }
+  if (s->status == 3) {
+    s->cand_present[1] = 1;
+    s->cand_u[1] = 0.0;
+  } else if (s->status == 2) {
+    const double f1 = flip(1);
+    s->cand_present[1] = 1;
+    s->cand_u[1] = __dadd_rn(f1, 1.0);
+    s->cand_present[0] = 1;
+    s->cand_u[0] = s->slot[0].present ? mid(flip(0), f1) : __dsub_rn(f1, 1.0);
+  } else if (s->status == 1) {
+    const double f2 = flip(2);
+    s->cand_present[1] = 1;
+    s->cand_u[1] = s->slot[1].present ? mid(flip(1), f2) : __dsub_rn(f2, 1.0);
+    if (s->slot[1].present) {
+      const double f1 = flip(1);
+      s->cand_present[0] = 1;
+      s->cand_u[0] = s->slot[0].present ? mid(flip(0), f1) : __dsub_rn(f1, 1.0);
+    }
+    s->cand_present[2] = 1;
+    s->cand_u[2] = s->slot[3].present ? mid(f2, flip(3)) : __dadd_rn(f2, 1.0);
+  }
+  for (int c = 0; c < 3; ++c) {
+    double u = s->cand_u[c];
+    u = u < -1e6 ? -1e6 : (u > 1e6 ? 1e6 : u);
+    s->cand_u[c] = u;
+    s->cand_t24[c] = static_cast<float>(exp2(__ddiv_rn(__dsub_rn(4.0, u), alpha)));
+    s->cand_t48[c] = static_cast<float>(exp2(__ddiv_rn(__dsub_rn(8.0, u), alpha)));
+    s->cand_n8[c] = 0;
+    s->cand_n48[c] = 0;
+  }
+}
+
+__device__ void alloc_count(const float* __restrict__ F, uint32_t T, AllocState* s) {
+  float t24[3], t48[3];
+  for (int c = 0; c < 3; ++c) {
+    t24[c] = s->cand_t24[c];
+    t48[c] = s->cand_t48[c];
+  }
+  unsigned long long n8[3] = {0, 0, 0}, n48[3] = {0, 0, 0};
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < T; j += gridDim.x * blockDim.x) {
+    const float f = F[j];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      n8[c] += f >= t48[c];
+      n48[c] += f >= t24[c];
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      n8[c] += __shfl_xor_sync(0xffffffffu, n8[c], o);
+      n48[c] += __shfl_xor_sync(0xffffffffu, n48[c], o);
+    }
+  if ((threadIdx.x & 31) == 0)
+    for (int c = 0; c < 3; ++c) {
+      atomicAdd(&s->cand_n8[c], n8[c]);
+      atomicAdd(&s->cand_n48[c], n48[c]);
+    }
+}
+
+// the reference's choice: the largest sample whose float-threshold payload fits
+__device__ void alloc_decide(AllocState* s, double budget, uint32_t S, uint32_t T) {
+  auto ok = [&](int c) {
+    const unsigned long long pay =
+        static_cast<unsigned long long>(S) * (2ull * T + 2ull * s->cand_n48[c] + 4ull * s->cand_n8[c]);
+    return s->cand_present[c] && static_cast<double>(pay) <= budget;
+  };
+  int ch;
+  if (ok(1)) ch = (s->cand_present[2] && ok(2)) ? -1 : 1;
+  else if (s->cand_present[0]) ch = ok(0) ? 0 : -1;
+  else ch = -2;
+  s->choice = ch;
+  const int c = ch >= 0 ? ch : 1;
+  s->u = s->cand_u[c];
+  s->t24 = s->cand_t24[c];
+  s->t48 = s->cand_t48[c];
 }
 
 // The whole search in one cooperative launch: prep -> up to kAllocMaxPasses x
-// (histogram on every CTA, scan on CTA 0) -> identify -> finish, with grid-wide
-// syncs in between (every CTA reads the same state after each sync, so the
-// early exit is uniform).
+// (histogram on every CTA, scan on CTA 0) -> neighbourhood -> identify -> candidate
+// counts -> decision, with grid-wide syncs in between (every CTA reads the same
+// state after each sync, so the early exit is uniform).
 __global__ void __launch_bounds__(kAllocBins) k_alloc_coop(const float* __restrict__ F, uint32_t T, double alpha,
-                                                           uint64_t wmax, AllocWork w) {
+                                                           uint64_t wmax, double budget, uint32_t S, AllocWork w) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   __shared__ HistSmem hs;
-  if (blockIdx.x == 0) alloc_init(w.state, w.bins, wmax);
+  AllocState* st = w.state;
+  if (blockIdx.x == 0) alloc_init(st, w.bins, wmax);
   grid.sync();
-  alloc_prep(F, T, alpha, w.level, w.state);
+  alloc_prep(F, T, alpha, w.level, st);
   grid.sync();
-  if (blockIdx.x == 0 && threadIdx.x == 0) alloc_start(w.state);
+  if (blockIdx.x == 0 && threadIdx.x == 0) alloc_start(st);
   grid.sync();
   for (int p = 0; p < kAllocMaxPasses; ++p) {
-    if (w.state->status != 0) break;
-    alloc_hist(w.level, T, w.state, w.bins, hs);
+    if (st->status != 0) break;
+    alloc_hist(w.level, T, st, w.bins, hs);
     grid.sync();
-    if (blockIdx.x == 0) alloc_scan(w.state, w.bins);
+    if (blockIdx.x == 0) alloc_scan(st, w.bins);
     grid.sync();
   }
-  alloc_identify(w.level, F, T, w.state);
+  if (blockIdx.x == 0 && threadIdx.x == 0) alloc_slots_init(st);
   grid.sync();
-  if (blockIdx.x == 0 && threadIdx.x == 0) alloc_finish(w.state, alpha);
+  alloc_neighbors(w.level, T, st);
+  grid.sync();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->slot[0].present = st->slot[1].present && st->slot[0].key != 0;
+    st->slot[3].present = st->status == 1 && st->slot[3].key != ~0ull;
+  }
+  grid.sync();
+  alloc_identify(w.level, F, T, st);
+  grid.sync();
+  if (blockIdx.x == 0 && threadIdx.x == 0) alloc_candidates(st, alpha);
+  grid.sync();
+  alloc_count(F, T, st);
+  grid.sync();
+  if (blockIdx.x == 0 && threadIdx.x == 0) alloc_decide(st, budget, S, T);
 }
 
-cudaError_t launch_alloc_search(const float* F, uint32_t T, double alpha, uint64_t wmax, AllocWork w,
-                                cudaStream_t st) {
+cudaError_t launch_alloc_search(const float* F, uint32_t T, double alpha, uint64_t wmax, double budget,
+                                uint32_t S, AllocWork w, cudaStream_t st) {
   static int max_blocks = 0;
   if (!max_blocks) {
     int dev = 0, sms = 0, per_sm = 0;
@@ -331,8 +469,70 @@ cudaError_t launch_alloc_search(const float* F, uint32_t T, double alpha, uint64
   }
   const uint32_t want = T ? (T + 4 * kAllocBins - 1) / (4 * kAllocBins) : 1;
   const uint32_t grid = want < static_cast<uint32_t>(max_blocks) ? want : static_cast<uint32_t>(max_blocks);
-  void* args[] = {const_cast<float**>(&F), &T, &alpha, &wmax, &w};
+  void* args[] = {const_cast<float**>(&F), &T, &alpha, &wmax, &budget, &S, &w};
   return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_alloc_coop), dim3(grid), dim3(kAllocBins), args, 0, st);
+}
+
+// ---- slow exact path helpers (rare: ambiguous neighbourhood or a libm mismatch)
+__global__ void k_flip_neighbor(const double* __restrict__ level, const float* __restrict__ F, uint32_t T,
+                                uint64_t key, int dir, FlipRec* rec) {
+  __shared__ unsigned long long best;
+  if (threadIdx.x == 0) best = dir < 0 ? 0ull : ~0ull;
+  __syncthreads();
+  unsigned long long b = dir < 0 ? 0ull : ~0ull;
+  for (uint32_t j = threadIdx.x; j < T; j += blockDim.x) {
+    const double l = level[j];
+    if (l != l) continue;
+    for (int t = 0; t < 2; ++t) {
+      const uint64_t k = dkey(__dsub_rn(t ? 8.0 : 4.0, l));
+      if (dir < 0 && k < key && k > b) b = k;
+      if (dir > 0 && k > key && k < b) b = k;
+    }
+  }
+  if (dir < 0) atomicMax(&best, b);
+  else atomicMin(&best, b);
+  __syncthreads();
+  const unsigned long long found = best;
+  if (threadIdx.x == 0) *rec = FlipRec{found, 0, 0, (dir < 0 ? found != 0ull : found != ~0ull) ? 1u : 0u, 0};
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < T; j += blockDim.x) {
+    const double l = level[j];
+    if (l != l) continue;
+    for (int t = 0; t < 2; ++t)
+      if (dkey(__dsub_rn(t ? 8.0 : 4.0, l)) == found) {
+        atomicExch(&rec->fbits, __float_as_uint(F[j]));
+        atomicExch(&rec->type, static_cast<uint32_t>(t));
+      }
+  }
+}
+
+void launch_flip_neighbor(const double* level, const float* F, uint32_t T, double alpha, uint64_t key, int dir,
+                          FlipRec* rec, cudaStream_t st) {
+  (void)alpha;
+  k_flip_neighbor<<<1, 1024, 0, st>>>(level, F, T, key, dir, rec);
+}
+
+__global__ void k_threshold_counts(const float* __restrict__ F, uint32_t T, float t24, float t48,
+                                   unsigned long long* counts) {
+  unsigned long long n8 = 0, n48 = 0;
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < T; j += gridDim.x * blockDim.x) {
+    n8 += F[j] >= t48;
+    n48 += F[j] >= t24;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    n8 += __shfl_xor_sync(0xffffffffu, n8, o);
+    n48 += __shfl_xor_sync(0xffffffffu, n48, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(counts, n8);
+    atomicAdd(counts + 1, n48);
+  }
+}
+
+void launch_threshold_counts(const float* F, uint32_t T, float t24, float t48, unsigned long long* counts,
+                             cudaStream_t st) {
+  cudaMemsetAsync(counts, 0, 2 * sizeof(unsigned long long), st);
+  k_threshold_counts<<<296, 512, 0, st>>>(F, T, t24, t48, counts);
 }
 
 // ---------------------------------------------------- width assignment

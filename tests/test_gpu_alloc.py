@@ -78,3 +78,19 @@ def test_allocate_fast_matches(dq, port, name, F, b):
 def test_allocate_infeasible(dq):
     with pytest.raises(dq.InfeasibleBudget):
         dq.allocate_fast(torch.ones(100, device="cuda"), 2.0)
+
+
+@pytest.mark.parametrize("seed", [5, 0])
+def test_allocate_fast_float_threshold_near_tie(dq, port, seed):
+    """At T = 2^22 a flip can sit within float rounding of the plateau's threshold, so the
+    exact-arithmetic crossing and the reference's float-threshold bisection disagree
+    (seed 5, found by /tmp search over seeds; seed 0 agrees).  The device must still
+    return the reference's allocation."""
+    rng = np.random.default_rng(seed)
+    F = (np.exp(8 * rng.standard_normal(1 << 22)) * 256).astype(np.float32)
+    w, p, u, pay = port.allocate_fast(F, 4.0)
+    got = dq.allocate_fast(torch.from_numpy(F).cuda(), 4.0)
+    assert got.u == u
+    assert got.payload_bits == pay
+    assert np.array_equal(got.widths.cpu().numpy(), w)
+    assert np.array_equal(got.permutation.cpu().numpy().astype(np.uint32), p)
