@@ -535,6 +535,8 @@ void launch_threshold_counts(const float* F, uint32_t T, float t24, float t48, u
   k_threshold_counts<<<296, 512, 0, st>>>(F, T, t24, t48, counts);
 }
 
+uint32_t alloc_blocks(uint32_t T) { return (T + 2047) / 2048; }
+
 // ---------------------------------------------------- width assignment
 // widths (proj/src/allocation.cpp:186-199) and the stable 8,4,2 partition
 // (allocation.cpp:302-310).  Block b owns super-groups [2048 b, 2048 b + 2048),

@@ -84,7 +84,7 @@ def test_allocate_infeasible(dq):
 def test_allocate_fast_float_threshold_near_tie(dq, port, seed):
     """At T = 2^22 a flip can sit within float rounding of the plateau's threshold, so the
     exact-arithmetic crossing and the reference's float-threshold bisection disagree
-    (seed 5, found by /tmp search over seeds; seed 0 agrees).  The device must still
+    (seed 5, found by tools/find_alloc_ties.py; seed 0 agrees).  The device must still
     return the reference's allocation."""
     rng = np.random.default_rng(seed)
     F = (np.exp(8 * rng.standard_normal(1 << 22)) * 256).astype(np.float32)
