@@ -123,7 +123,7 @@ def lib() -> C.CDLL:
     if _lib is None:
         if not os.path.exists(LIB_PATH):
             raise ImportError(f"{LIB_PATH} is not built; run paper_2602_08923_b200._lib.build()")
-        L = C.CDLL(LIB_PATH)
+        L = C.CDLL(LIB_PATH, mode=os.RTLD_NOW)  # resolve every symbol now: a broken build fails here
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(L, name)
             fn.restype = res

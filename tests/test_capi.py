@@ -42,6 +42,14 @@ def test_exports_every_declared_symbol(L):
         assert s in SIGNATURES, f"{s} missing from the ctypes signature table"
 
 
+def test_no_unresolved_internal_symbols():
+    """Every dq:: symbol the library references is defined in it (RTLD_NOW load in lib())."""
+    import subprocess
+    from paper_2602_08923_b200 import _lib
+    out = subprocess.run(["nm", "-D", "--undefined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "_ZN2dq" not in out, out
+
+
 def test_version_and_defaults(L):
     from paper_2602_08923_b200._lib import Config
     assert L.dq_version() >= 1
