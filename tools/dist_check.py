@@ -29,7 +29,7 @@ def main():
     results = {}
     ok = True
     cases = [("ring", 1 << 16, 4.0), ("ring", (1 << 20) + 300, 5.0), ("butterfly", 1 << 16, 4.0),
-             ("butterfly", (1 << 20) + 300, 3.0), ("ring", 1 << 24, 4.0)]
+             ("butterfly", (1 << 20) + 300, 3.0), ("ring", 1 << 24, 4.0), ("ring", 1 << 28, 4.0)]
     for topo, d, b in cases:
         if topo == "butterfly" and world & (world - 1):
             continue
