@@ -176,6 +176,17 @@ int dq_selftest(int which, uint64_t n, uint64_t seed, uint64_t* mismatches);
  * 128 bytes to every rank (e.g. torch.distributed), every rank joins. */
 int dq_comm_unique_id(uint8_t out[128]);
 int dq_comm_init(dq_ctx* ctx, int rank, int nranks, const uint8_t id[128]);
+/* Ring transport.  PEER (default): the fused hop kernels store compressed units
+ * straight into the neighbour's memory over NVLink (CUDA IPC mapping of one
+ * region per rank, per-unit flags; a flag missing for 20 s aborts the kernel),
+ * and the sink stores into every rank's gather slot.  NCCL: point-to-point
+ * sends of tile-aligned pieces on a communication stream.  Same bytes, same
+ * result.  Env DQ_TRANSPORT=nccl selects NCCL at context creation; if any rank
+ * cannot map its peers, all ranks switch to NCCL at the first round.  The
+ * butterfly topology always uses NCCL. */
+enum { DQ_TRANSPORT_PEER = 0, DQ_TRANSPORT_NCCL = 1 };
+int dq_comm_set_transport(dq_ctx* ctx, int transport);
+int dq_comm_get_transport(const dq_ctx* ctx, int* transport);
 /* [engine.hpp:63-64 run_round, distributed] d_in: this rank's gradient; d_out:
  * the SUM estimate over ranks (caller divides by n for a mean, as the
  * reference's caller does). */

@@ -409,12 +409,19 @@ def run_round_host(worker_values: Sequence[np.ndarray], config: PipelineConfig,
     return out, _info_dict(info)
 
 
+TRANSPORT_PEER, TRANSPORT_NCCL = 0, 1
+
+
 class Communicator:
-    """Distributed all-reduce: one process per GPU, NCCL over NVLink between the fused kernels.
+    """Distributed all-reduce: one process per GPU.
 
-    ``torch.distributed`` (any backend) only ships the 128-byte NCCL id."""
+    Ring transport ``"peer"`` (default): the fused hop kernels store compressed
+    units straight into the neighbour's HBM over NVLink (CUDA IPC, per-unit flags);
+    ``"nccl"``: NCCL point-to-point between the fused kernels.  ``torch.distributed``
+    (any backend) only ships the 128-byte NCCL id."""
 
-    def __init__(self, config: PipelineConfig, rank: int, world_size: int, group=None):
+    def __init__(self, config: PipelineConfig, rank: int, world_size: int, group=None,
+                 transport: Optional[str] = None):
         import torch.distributed as dist
         if config.n_workers != world_size:
             raise InvalidArgument(2, "config.n_workers must equal the world size")
@@ -426,7 +433,18 @@ class Communicator:
         dist.broadcast_object_list(obj, src=0, group=group)
         uid = np.frombuffer(obj[0], np.uint8).copy()
         check(lib().dq_comm_init(self.ctx.h, rank, world_size, uid.ctypes.data_as(C.POINTER(C.c_uint8))))
+        if transport is not None:
+            if transport not in ("peer", "nccl"):
+                raise InvalidArgument(2, f"unknown transport {transport!r}")
+            check(lib().dq_comm_set_transport(self.ctx.h, TRANSPORT_PEER if transport == "peer" else TRANSPORT_NCCL))
         self.rank, self.world_size = rank, world_size
+
+    @property
+    def transport(self) -> str:
+        """Active ring transport ("peer" or "nccl"; peer falls back to nccl if mapping fails)."""
+        t = C.c_int()
+        check(lib().dq_comm_get_transport(self.ctx.h, C.byref(t)))
+        return "peer" if t.value == TRANSPORT_PEER else "nccl"
 
     def allreduce(self, x: torch.Tensor, out: Optional[torch.Tensor] = None) -> tuple:
         """SUM estimate of every rank's ``x`` (caller divides by n for a mean)."""

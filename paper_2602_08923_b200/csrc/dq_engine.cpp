@@ -10,6 +10,7 @@
 // moves the compressed chunks over NVLink with NCCL point-to-point.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <stdexcept>
@@ -157,6 +158,25 @@ uint64_t fnv1a(const uint8_t* b, size_t n, uint64_t h) {
 
 using namespace dq;
 
+// Peer transport region of one rank (cudaMalloc'd, exported by CUDA IPC, mapped by
+// every other rank of the node): per round parity, n-1 ring inboxes (hop h's output
+// lands in the right neighbour's inbox h) and n gather slots (the sink of chunk c
+// stores its bytes into every rank's slot c), then one u32 flag per unit of each.
+struct PeerMem {
+  uint8_t* base = nullptr;
+  std::vector<uint8_t*> peer;  // rank q's region as mapped here (peer[me] == base)
+  size_t cap = 0;              // bytes per chunk slot
+  size_t cap_units = 0;        // flags per chunk slot
+  uint32_t n = 0, epoch = 0;
+  size_t slots() const { return 2ull * (n - 1) + 2ull * n; }
+  size_t inbox(uint32_t par, uint32_t h) const { return (static_cast<size_t>(par) * (n - 1) + h) * cap; }
+  size_t gather(uint32_t par, uint32_t c) const { return (2ull * (n - 1) + static_cast<size_t>(par) * n + c) * cap; }
+  size_t flags() const { return slots() * cap; }
+  size_t iflag(uint32_t par, uint32_t h) const { return flags() + 4 * cap_units * inbox(par, h) / cap; }
+  size_t gflag(uint32_t par, uint32_t c) const { return flags() + 4 * cap_units * gather(par, c) / cap; }
+  size_t total() const { return flags() + 4 * cap_units * slots(); }
+};
+
 struct dq_ctx {
   dq_config cfg{};
   int device = 0;
@@ -202,7 +222,17 @@ struct dq_ctx {
   cudaStream_t cs = nullptr;            // communication stream (NCCL p2p)
   std::vector<cudaEvent_t> pipe_ev;     // per (hop, piece) handshakes compute <-> comm
   int pieces = 4;                       // pipeline pieces per chunk
+  int transport = DQ_TRANSPORT_PEER;    // ring transport (butterfly always uses NCCL)
+  PeerMem pm;
+  DevBuf<uint8_t> ipc;                  // IPC handle exchange
+  void close_peers() {
+    for (size_t q = 0; q < pm.peer.size(); ++q)
+      if (pm.peer[q] && pm.peer[q] != pm.base) cudaIpcCloseMemHandle(pm.peer[q]);
+    pm.peer.clear();
+  }
   ~dq_ctx() {
+    close_peers();
+    if (pm.base) cudaFree(pm.base);
     if (h_state) cudaFreeHost(h_state);
     if (h_counts) cudaFreeHost(h_counts);
     if (h_vn) cudaFreeHost(h_vn);
@@ -929,6 +959,128 @@ uint8_t* ring_pipelined(dq_ctx* ctx, const Prepared& pr, const std::vector<Codec
   return sink;
 }
 
+// (Re)build the peer region when this round's chunks do not fit.  Collective: every
+// rank takes the same decision from round-global sizes at the same point of the
+// same round, after the stats all-gather has ordered all of every peer's previous
+// round (its last stores into this rank's region) before it.  If any rank cannot map
+// a peer, every rank falls back to the NCCL transport.
+bool peer_setup(dq_ctx* ctx, size_t mb, uint32_t max_nsg, cudaStream_t st) {
+  PeerMem& pm = ctx->pm;
+  const uint32_t n = ctx->cfg.n_workers, me = static_cast<uint32_t>(ctx->rank);
+  if (pm.base && pm.n == n && mb <= pm.cap && max_nsg <= pm.cap_units) return true;
+  DQ_CUDA(cudaStreamSynchronize(st));
+  ctx->close_peers();
+  uint8_t* old = pm.base;
+  pm.base = nullptr;
+  pm.n = n;
+  pm.cap = (mb + mb / 4 + 4095) & ~static_cast<size_t>(4095);
+  pm.cap_units = max_nsg + max_nsg / 4 + 64;
+  DQ_CUDA(cudaMalloc(&pm.base, pm.total()));
+  DQ_CUDA(cudaMemsetAsync(pm.base + pm.flags(), 0, pm.total() - pm.flags(), st));
+  ctx->ipc.reserve(static_cast<size_t>(n) * (sizeof(cudaIpcMemHandle_t) + 4));
+  cudaIpcMemHandle_t h;
+  DQ_CUDA(cudaIpcGetMemHandle(&h, pm.base));
+  const size_t hs = sizeof(h);
+  DQ_CUDA(cudaMemcpyAsync(ctx->ipc.p + me * hs, &h, hs, cudaMemcpyHostToDevice, st));
+  DQ_NCCL(ncclAllGather(ctx->ipc.p + me * hs, ctx->ipc.p, hs, ncclUint8, ctx->comm, st));
+  std::vector<uint8_t> all(n * hs);
+  DQ_CUDA(cudaMemcpyAsync(all.data(), ctx->ipc.p, n * hs, cudaMemcpyDeviceToHost, st));
+  DQ_CUDA(cudaStreamSynchronize(st));
+  if (old) DQ_CUDA(cudaFree(old));  // every rank closed its mapping before the all-gather
+  pm.peer.assign(n, nullptr);
+  int ok = 1;
+  for (uint32_t q = 0; q < n; ++q) {
+    if (q == me) {
+      pm.peer[q] = pm.base;
+      continue;
+    }
+    cudaIpcMemHandle_t hq;
+    std::memcpy(&hq, all.data() + q * hs, hs);
+    void* ptr = nullptr;
+    if (cudaIpcOpenMemHandle(&ptr, hq, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      ok = 0;
+      break;
+    }
+    pm.peer[q] = static_cast<uint8_t*>(ptr);
+  }
+  int* dok = reinterpret_cast<int*>(ctx->ipc.p + n * hs);
+  DQ_CUDA(cudaMemcpyAsync(dok, &ok, sizeof ok, cudaMemcpyHostToDevice, st));
+  DQ_NCCL(ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, ctx->comm, st));
+  DQ_CUDA(cudaMemcpyAsync(&ok, dok, sizeof ok, cudaMemcpyDeviceToHost, st));
+  DQ_CUDA(cudaStreamSynchronize(st));
+  if (!ok) {
+    ctx->close_peers();
+    DQ_CUDA(cudaFree(pm.base));
+    pm.base = nullptr;
+    ctx->transport = DQ_TRANSPORT_NCCL;
+    std::fprintf(stderr, "dynamiq_b200: peer mapping failed on some rank; ring uses NCCL p2p\n");
+  }
+  return ok != 0;
+}
+
+// Ring over peer memory: at hop h rank r runs the fused kernel on chunk r-1-h, reading
+// its inbox h-1 unit by unit as the left neighbour's hop h-1 kernel raises the unit
+// flags and storing its own output straight into the right neighbour's inbox h
+// (NVLink stores, no staging copy, no NCCL kernel); consecutive hops of neighbouring
+// ranks therefore overlap at unit granularity.  The sink (hop n-1) stores its chunk
+// into gather slot r of every rank - the all-gather - and one decode launch per rank
+// consumes all n gather slots as their units land.
+void ring_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>& bases,
+               const std::vector<Layout>& lays, float* out, size_t d, cudaStream_t st) {
+  const uint32_t n = ctx->cfg.n_workers, me = static_cast<uint32_t>(ctx->rank);
+  const uint32_t right = (me + 1) % n;
+  PeerMem& pm = ctx->pm;
+  const uint32_t epoch = ++pm.epoch, par = epoch & 1u;
+  for (uint32_t h = 0; h < n; ++h) {
+    const uint32_t ch = (me + 2 * n - 1 - h) % n;  // sink at h = n-1
+    CodecArgs a = bases[ch];
+    a.slot = h;
+    a.unit = peer_unit(lays[ch].nsg);
+    a.epoch = epoch;
+    if (h > 0) {
+      a.in = pm.base + pm.inbox(par, h - 1);
+      a.in_flags = reinterpret_cast<const uint32_t*>(pm.base + pm.iflag(par, h - 1));
+    }
+    if (h + 1 < n) {
+      a.outs[0] = pm.peer[right] + pm.inbox(par, h);
+      a.out_flags[0] = reinterpret_cast<uint32_t*>(pm.peer[right] + pm.iflag(par, h));
+      a.n_outs = 1;
+    } else {
+      for (uint32_t k = 0; k < n; ++k) {  // remote copies first, own slot last
+        const uint32_t q = (me + 1 + k) % n;
+        a.outs[k] = pm.peer[q] + pm.gather(par, me);
+        a.out_flags[k] = reinterpret_cast<uint32_t*>(pm.peer[q] + pm.gflag(par, me));
+      }
+      a.n_outs = static_cast<int>(n);
+    }
+    const bool dar = h > 0;
+    timed(ctx, dar ? K_DAR : K_LEAF, quant_bytes(lays[ch], dar), st, [&] { launch_quant_peer(a, dar, st); });
+  }
+  GatherArgs g{};
+  uint32_t max_nsg = 0;
+  double gbytes = 0;
+  for (uint32_t c = 0; c < n; ++c) {
+    g.in[c] = pm.base + pm.gather(par, c);
+    g.lo[c] = p.lo[c];
+    g.n8[c] = lays[c].n8;
+    g.n4[c] = lays[c].n4;
+    g.flags[c] = c == me ? nullptr : reinterpret_cast<const uint32_t*>(pm.base + pm.gflag(par, c));
+    g.unit[c] = peer_unit(lays[c].nsg);
+    max_nsg = std::max(max_nsg, lays[c].nsg);
+    gbytes += 1032.0 * lays[c].nsg + lays[c].bytes();
+  }
+  g.lo[n] = p.lo[n];
+  g.epoch = epoch;
+  g.perm = ctx->perm.p;
+  g.gmean = ctx->pmean.p;
+  g.out = out;
+  g.d = d;
+  g.n_workers_f = static_cast<float>(n);
+  g.uniform_books = ctx->cfg.non_uniform ? 0 : 1;
+  timed(ctx, K_DECODE, gbytes, st, [&] { launch_gather_decode(g, n, max_nsg, st); });
+}
+
 void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info* info, cudaStream_t st) {
   const dq_config& c = ctx->cfg;
   const uint32_t n = c.n_workers, me = static_cast<uint32_t>(ctx->rank);
@@ -971,7 +1123,7 @@ void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info
   uint32_t max_nsg = 0;
   for (uint32_t i = 0; i < n; ++i) max_nsg = std::max(max_nsg, p.lo[i + 1] - p.lo[i]);
   // per chunk: outgoing, incoming, held, gather; accumulators for butterfly receivers
-  ctx->msgs.reserve(4ull * n * mb);
+
   auto buf = [&](int kind, uint32_t ch) { return ctx->msgs.p + (static_cast<size_t>(kind) * n + ch) * mb; };
   const bool need_acc = c.topology == DQ_BUTTERFLY;
   if (need_acc) ctx->accs.reserve(static_cast<size_t>(n) * max_nsg * 256);
@@ -993,6 +1145,20 @@ void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info
     b.n_slots = plans[ch].n_slots;
     bases[ch] = b;
   }
+  if (c.topology == DQ_RING && ctx->transport == DQ_TRANSPORT_PEER && n <= static_cast<uint32_t>(kMaxPeers) &&
+      peer_setup(ctx, mb, max_nsg, st)) {
+    ring_peer(ctx, p, bases, lays, out, d, st);
+    for (uint32_t ch = 0; ch < n; ++ch) {
+      for (uint32_t g = 0; g < plans[ch].n_gat; ++g) account(info, lays[ch], g == 0);
+      for (size_t e = 0; e < plans[ch].red.size(); ++e) account(info, lays[ch], true);
+      info->stats_bits += static_cast<uint64_t>(plans[ch].red.size() + plans[ch].n_gat) * 64ull * lays[ch].nsg;
+    }
+    DQ_CUDA(cudaGetLastError());
+    DQ_CUDA(cudaEventRecord(ctx->ev1, st));
+    finish_async(ctx, info);
+    return;
+  }
+  ctx->msgs.reserve(4ull * n * mb);
   uint8_t* mysink = buf(3, me);
   if (c.topology == DQ_RING) {
     mysink = ring_pipelined(ctx, p, bases, lays, mb, info, st);
@@ -1185,6 +1351,8 @@ int dq_ctx_create(const dq_config* cfg, int device, dq_ctx** out) {
     auto* c = new dq_ctx;
     c->cfg = *cfg;
     c->device = device;
+    if (const char* t = std::getenv("DQ_TRANSPORT"))
+      if (std::strcmp(t, "nccl") == 0) c->transport = DQ_TRANSPORT_NCCL;
     *out = c;
   });
 }
@@ -1487,6 +1655,21 @@ int dq_comm_unique_id(uint8_t out[128]) {
     ncclUniqueId id;
     DQ_NCCL(ncclGetUniqueId(&id));
     std::memcpy(out, id.internal, 128);
+  });
+}
+
+int dq_comm_set_transport(dq_ctx* ctx, int transport) {
+  return guarded([&] {
+    if (!ctx) invalid("null context");
+    if (transport != DQ_TRANSPORT_PEER && transport != DQ_TRANSPORT_NCCL) invalid("unknown transport");
+    ctx->transport = transport;
+  });
+}
+
+int dq_comm_get_transport(const dq_ctx* ctx, int* transport) {
+  return guarded([&] {
+    if (!ctx || !transport) invalid("null argument");
+    *transport = ctx->transport;
   });
 }
 

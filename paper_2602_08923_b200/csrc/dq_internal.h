@@ -9,6 +9,8 @@
 namespace dq {
 
 // Arguments of every codec kernel (passed by value in the param space).
+constexpr int kMaxPeers = 8;  // peer transport: ring of up to 8 GPUs (one NVSwitch domain node)
+
 struct CodecArgs {
   Layout L;                 // geometry of the chunk being processed
   uint32_t first_sg;        // permuted index of the chunk's first super-group (RNG key, perm lookup)
@@ -26,6 +28,15 @@ struct CodecArgs {
   int correlated;
   int uniform_books;
   float est_c1, est_c2;     // width-8 codebook index estimator (see bracket())
+  // peer transport (k_quant_peer): the chunk is produced/consumed in flag units of
+  // `unit` consecutive super-groups; a unit of `in` may be read once in_flags[unit]
+  // == epoch, and every finished unit is stored to all n_outs destinations (peer
+  // memory over NVLink) before its out_flags[o][unit] is set to epoch.
+  const uint32_t* in_flags;
+  uint8_t* outs[kMaxPeers];
+  uint32_t* out_flags[kMaxPeers];
+  int n_outs;
+  uint32_t unit, epoch;
 };
 
 // All chunks of a round decoded into the output gradient in one launch.
@@ -41,10 +52,17 @@ struct GatherArgs {
   uint64_t d;
   float n_workers_f;
   int uniform_books;
+  // peer transport: chunk c's unit k may be decoded once flags[c][k] == epoch (null: ready)
+  const uint32_t* flags[64];
+  uint32_t unit[64];
+  uint32_t epoch;
 };
 void launch_gather_decode(const GatherArgs& g, uint32_t n_chunks, uint32_t max_nsg, cudaStream_t st);
 
 void launch_quant(const CodecArgs& a, int src, bool dar, cudaStream_t st);
+// one ring hop over peer memory (gather source, SRC = 0); see CodecArgs peer fields
+void launch_quant_peer(const CodecArgs& a, bool dar, cudaStream_t st);
+uint32_t peer_unit(uint32_t nsg);  // super-groups per flag unit of a chunk (same on every rank)
 void launch_da(const CodecArgs& a, int src, cudaStream_t st);
 void launch_decode(const CodecArgs& a, int out_mode, cudaStream_t st);
 cudaError_t upload_codebooks(const float* books);

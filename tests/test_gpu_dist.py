@@ -1,4 +1,5 @@
-"""Multi-GPU parity: dq_allreduce over NCCL == the simulated round == the oracle (bit-exact).
+"""Multi-GPU parity: dq_allreduce (peer-memory and NCCL ring transports, NCCL butterfly)
+== the simulated round == the oracle (bit-exact).
 
 Launches tools/dist_check.py with torchrun on every visible GPU (>= 2 needed)."""
 import json

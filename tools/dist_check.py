@@ -2,7 +2,7 @@
 """Distributed parity check (run under torchrun, one rank per GPU).
 
 Every rank builds the same n synthetic gradients (rank-keyed), all-reduces its
-own with dq_allreduce (NCCL over NVLink between the fused kernels), and rank 0
+own with dq_allreduce (peer-memory ring and NCCL transports), and rank 0
 compares the result bit for bit with the single-GPU simulated round over all n
 gradients (itself pinned to the oracle by tests/test_gpu_round.py) and, at small
 sizes, with the CPU oracle's run_round.  Prints one JSON line on rank 0;
@@ -28,9 +28,14 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     results = {}
     ok = True
-    cases = [("ring", 1 << 16, 4.0), ("ring", (1 << 20) + 300, 5.0), ("butterfly", 1 << 16, 4.0),
-             ("butterfly", (1 << 20) + 300, 3.0), ("ring", 1 << 24, 4.0), ("ring", 1 << 28, 4.0)]
-    for topo, d, b in cases:
+    only = os.environ.get("DIST_CHECK_TRANSPORTS", "peer,nccl").split(",")
+    cases = [("ring", 1 << 16, 4.0, t) for t in only]
+    cases += [("ring", (1 << 20) + 300, 5.0, t) for t in only]
+    cases += [("butterfly", 1 << 16, 4.0, "nccl"), ("butterfly", (1 << 20) + 300, 3.0, "nccl")]
+    cases += [("ring", 1 << 24, 4.0, t) for t in only] + [("ring", 1 << 28, 4.0, t) for t in only]
+    cases += [("ring", 3000, 6.0, "peer"), ("ring", 1 << 22, 2.6, "peer")]
+    comms = {}
+    for topo, d, b, transport in cases:
         if topo == "butterfly" and world & (world - 1):
             continue
         cfg = dq.PipelineConfig(n_workers=world, budget_bits=b, seed=dq.SharedSeed(3, 1),
@@ -40,7 +45,13 @@ def main():
         scale = torch.exp(4.0 * torch.randn(T, device="cuda", generator=g))
         ws = [(torch.randn(T, 256, device="cuda", generator=g) * scale[:, None]).reshape(-1)[:d].contiguous()
               for _ in range(world)]
-        comm = dq.Communicator(cfg, rank, world)
+        if rank == 0 and os.environ.get("DIST_CHECK_VERBOSE"):
+            print(f"case {topo} {transport} d={d} b={b}", file=sys.stderr, flush=True)
+        # peer-transport contexts are reused across sizes and budgets (region regrowth, epochs)
+        key = (topo, transport, b)
+        if key not in comms:
+            comms[key] = dq.Communicator(cfg, rank, world, transport=transport)
+        comm = comms[key]
         out, info = comm.allreduce(ws[rank])
         out2, _ = comm.allreduce(ws[rank])  # second round on the same context (buffer reuse)
         torch.cuda.synchronize()
@@ -52,7 +63,8 @@ def main():
         if rank == 0:
             sim = dq.run_round(ws, cfg, ctx=dq.Context(cfg))
             match_sim = bool(torch.equal(sim.synced, out))
-            rec = {"match_sim": match_sim, "ranks_agree": ranks_agree, "same_twice": same_twice,
+            rec = {"transport": comm.transport, "match_sim": match_sim, "ranks_agree": ranks_agree,
+                   "same_twice": same_twice,
                    "u_equal": info["u"] == sim.u, "vnmse": sim.vnmse, "n8_4_2": [info["n8"], info["n4"], info["n2"]]}
             if d <= (1 << 16):
                 from oracle.oracle import Oracle
@@ -61,9 +73,10 @@ def main():
                 rec["match_oracle"] = bool(np.array_equal(out.cpu().numpy().view(np.uint32),
                                                           want["synced"].view(np.uint32)))
             ok &= all(v for k, v in rec.items() if k.startswith("match") or k in ("ranks_agree", "same_twice"))
-            results[f"{topo}_d{d}_b{b}"] = rec
-        del comm
+            ok &= rec["transport"] == transport
+            results[f"{topo}_{transport}_d{d}_b{b}"] = rec
         dist.barrier()
+    comms.clear()
     if rank == 0:
         print(json.dumps({"world": world, "ok": ok, "cases": results}), flush=True)
     dist.barrier()

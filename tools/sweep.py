@@ -43,6 +43,7 @@ def main():
     ap.add_argument("--budgets", default="4")
     ap.add_argument("--topology", default="ring")
     ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--transport", default="peer", help="ring transport: peer | nccl")
     ap.add_argument("--sigma-log", type=float, default=4.0)
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -57,7 +58,7 @@ def main():
         for b in (float(x) for x in args.budgets.split(",")):
             cfg = dq.PipelineConfig(n_workers=world, budget_bits=b, seed=dq.SharedSeed(1, 0),
                                     topology=dq.BUTTERFLY if topo == "butterfly" else dq.RING)
-            comm = dq.Communicator(cfg, rank, world)
+            comm = dq.Communicator(cfg, rank, world, transport=args.transport)
             for e in range(lo, hi + 1):
                 d = 1 << e
                 g = torch.Generator(device="cuda").manual_seed(1)
@@ -66,7 +67,7 @@ def main():
                 g.manual_seed(1000 + rank)
                 x = (torch.randn(T, 256, device="cuda", generator=g) * scale[:, None]).reshape(-1)[:d].contiguous()
                 out = torch.empty_like(x)
-                rec = {"topology": topo, "budget": b, "n_gpus": world, "d": d, "bytes_fp32": 4 * d}
+                rec = {"topology": topo, "transport": comm.transport, "budget": b, "n_gpus": world, "d": d, "bytes_fp32": 4 * d}
                 try:
                     ms = timed(lambda: comm.allreduce(x, out), args.steps, st)
                 except dq.InfeasibleBudget as ex:
