@@ -127,6 +127,16 @@ int dq_to_reference_wire(const void* h_soa, uint32_t chunk_index, uint32_t n8, u
                          uint32_t n2, void* h_ref);
 int dq_from_reference_wire(const void* h_ref, size_t len, void* h_soa, size_t soa_cap,
                            uint32_t* chunk_index, uint32_t* n8, uint32_t* n4, uint32_t* n2);
+/* [codec.cpp:319-343 serialize_chunk] device buffers, stream-ordered: d_wire
+ * receives dq_chunk_bytes + 24 bytes (header + records), one warp per record. */
+int dq_serialize_chunk(const void* d_soa, uint32_t chunk_index, uint32_t n8, uint32_t n4, uint32_t n2,
+                       void* d_wire, void* stream);
+/* [codec.cpp:345-399 parse_chunk] device buffers: strict parse with the
+ * reference's checks and messages (DQ_EMALFORMED; width-16 bodies DQ_EINVAL).
+ * Reads the header and the validation verdict back, so it synchronizes `stream`.
+ * d_soa may be null (validate only); soa_cap < dq_chunk_bytes -> DQ_EINVAL. */
+int dq_parse_chunk(const void* d_wire, size_t len, void* d_soa, size_t soa_cap, uint32_t* chunk_index,
+                   uint32_t* n8, uint32_t* n4, uint32_t* n2, void* stream);
 
 /* ---- statistics and allocation ------------------------------------------ */
 /* [stats.hpp:19 compute_stats] per super-group fp64-sequential mean / sum of squares */

@@ -90,6 +90,9 @@ SIGNATURES = {
     "dq_decompress_chunk": (C.c_int, [_V, _V, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int, _V]),
     "dq_to_reference_wire": (C.c_int, [_V, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, _V]),
     "dq_from_reference_wire": (C.c_int, [_V, C.c_size_t, _V, C.c_size_t, _u32p, _u32p, _u32p, _u32p]),
+    "dq_serialize_chunk": (C.c_int, [_V, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, _V, _V]),
+    "dq_parse_chunk": (C.c_int, [_V, C.c_size_t, _V, C.c_size_t, _P(C.c_uint32), _P(C.c_uint32),
+                                 _P(C.c_uint32), _P(C.c_uint32), _V]),
     "dq_compute_stats": (C.c_int, [_V, C.c_size_t, _V, _V, _V]),
     "dq_reduce_stats": (C.c_int, [_V, _V, C.c_uint32, C.c_size_t, _V, _V, _V]),
     "dq_allocate_fast": (C.c_int, [_V, _V, C.c_size_t, C.c_double, _V, _V, _P(C.c_double), _P(C.c_uint64),

@@ -134,18 +134,21 @@ def _ptr(t: Optional[torch.Tensor]) -> C.c_void_p:
 def _runs(widths) -> tuple:
     """Run lengths of a width-sorted body; unsorted bodies are rejected like serialize_chunk
     (proj/src/codec.cpp:298-315)."""
-    w = np.asarray(widths, np.uint8).ravel()
-    rank = {8: 0, 4: 1, 2: 2}
-    cls = []
-    for x in w.tolist():
-        if x not in rank:
-            if x == 16:
-                raise InvalidArgument(2, "width-16 passthrough is not supported by the device codec")
-            raise InvalidArgument(2, f"unsupported codec width {x}")
-        cls.append(rank[x])
-    if any(b < a for a, b in zip(cls, cls[1:])):
+    w = np.asarray(widths).astype(np.int64, copy=False).ravel()
+    lut = np.full(256, -1, np.int64)
+    lut[[8, 4, 2]] = [0, 1, 2]
+    ok = (w >= 0) & (w < 256)
+    cls = np.where(ok, lut[np.clip(w, 0, 255)], -1)
+    bad = np.flatnonzero(cls < 0)
+    if bad.size:
+        x = int(w[bad[0]])
+        if x == 16:
+            raise InvalidArgument(2, "width-16 passthrough is not supported by the device codec")
+        raise InvalidArgument(2, f"unsupported codec width {x}")
+    if np.any(np.diff(cls) < 0):
         raise InvalidArgument(2, "chunk body must be ordered by width class 8,4,2,16")
-    return cls.count(0), cls.count(1), cls.count(2)
+    cnt = np.bincount(cls, minlength=3)
+    return int(cnt[0]), int(cnt[1]), int(cnt[2])
 
 
 def _f32(t: torch.Tensor, n: int, what: str) -> torch.Tensor:
@@ -215,8 +218,15 @@ def decompress_chunk(chunk: DeviceChunk, cfg: CodecConfig, out: Optional[torch.T
     return out
 
 
-def serialize_chunk(chunk: DeviceChunk) -> bytes:
-    """Reference wire bytes (proj/src/codec.cpp:319-343)."""
+def serialize_chunk(chunk: DeviceChunk, device: bool = False):
+    """Reference wire bytes (proj/src/codec.cpp:319-343): host ``bytes``, or with
+    ``device=True`` a CUDA uint8 tensor serialized on the GPU (dq_serialize_chunk)."""
+    if device:
+        out = torch.empty(chunk_bytes(chunk.n8, chunk.n4, chunk.n2) + 24, dtype=torch.uint8,
+                          device=chunk.data.device)
+        check(lib().dq_serialize_chunk(_ptr(chunk.data), chunk.chunk_index, chunk.n8, chunk.n4, chunk.n2,
+                                       _ptr(out), _stream()))
+        return out
     soa = chunk.data.cpu().numpy()
     out = np.zeros(chunk_bytes(chunk.n8, chunk.n4, chunk.n2) + 24, np.uint8)
     check(lib().dq_to_reference_wire(soa.ctypes.data_as(C.c_void_p), chunk.chunk_index, chunk.n8, chunk.n4,
@@ -235,8 +245,20 @@ def soa_from_reference(buf: bytes):
     return ci.value, n8.value, n4.value, n2.value, soa[: chunk_bytes(n8.value, n4.value, n2.value)]
 
 
-def parse_chunk(buf: bytes, device="cuda") -> DeviceChunk:
-    """proj/src/codec.cpp:345-399 — raises MalformedBuffer on any malformed buffer."""
+def parse_chunk(buf, device="cuda") -> DeviceChunk:
+    """proj/src/codec.cpp:345-399 — raises MalformedBuffer on any malformed buffer.
+
+    ``buf``: host bytes (parsed on the host), or a CUDA uint8 tensor (parsed and
+    validated on the GPU by dq_parse_chunk)."""
+    if isinstance(buf, torch.Tensor):
+        if not (buf.is_cuda and buf.dtype == torch.uint8 and buf.is_contiguous()):
+            raise InvalidArgument(2, "device wire buffer must be a contiguous CUDA uint8 tensor")
+        ci, n8, n4, n2 = C.c_uint32(), C.c_uint32(), C.c_uint32(), C.c_uint32()
+        # a valid body is exactly the device layout's size: len - 24
+        data = torch.empty(max(buf.numel() - 24, 1), dtype=torch.uint8, device=buf.device)
+        check(lib().dq_parse_chunk(_ptr(buf), buf.numel(), _ptr(data), data.numel(), C.byref(ci), C.byref(n8),
+                                   C.byref(n4), C.byref(n2), _stream()))
+        return DeviceChunk(ci.value, n8.value, n4.value, n2.value, data)
     ci, n8, n4, n2, soa = soa_from_reference(buf)
     data = torch.from_numpy(soa.copy() if soa.size else np.zeros(1, np.uint8)).to(device)
     return DeviceChunk(ci, n8, n4, n2, data)

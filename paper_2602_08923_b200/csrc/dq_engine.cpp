@@ -1455,6 +1455,68 @@ int dq_to_reference_wire(const void* h_soa, uint32_t chunk_index, uint32_t n8, u
   });
 }
 
+int dq_serialize_chunk(const void* d_soa, uint32_t chunk_index, uint32_t n8, uint32_t n4, uint32_t n2,
+                       void* d_wire, void* stream) {
+  return guarded([&] {
+    if (!d_wire || (!d_soa && n8 + n4 + n2)) invalid("null argument");
+    if (reinterpret_cast<uintptr_t>(d_wire) % 4 || reinterpret_cast<uintptr_t>(d_soa) % 2)
+      invalid("wire buffer must be 4-byte aligned, chunk 2-byte aligned");
+    const Layout L{n8 + n4 + n2, n8, n4};
+    launch_to_wire(static_cast<const uint8_t*>(d_soa), L, chunk_index, static_cast<uint8_t*>(d_wire), S(stream));
+    DQ_CUDA(cudaGetLastError());
+  });
+}
+
+int dq_parse_chunk(const void* d_wire, size_t len, void* d_soa, size_t soa_cap, uint32_t* chunk_index,
+                   uint32_t* n8, uint32_t* n4, uint32_t* n2, void* stream) {
+  return guarded([&] {
+    if (!chunk_index || !n8 || !n4 || !n2 || (!d_wire && len)) invalid("null argument");
+    if (reinterpret_cast<uintptr_t>(d_wire) % 2 || reinterpret_cast<uintptr_t>(d_soa) % 2)
+      invalid("buffers must be 2-byte aligned");
+    auto mal = [](const char* m) { throw Error(DQ_EMALFORMED, std::string("malformed compressed buffer: ") + m); };
+    if (len < 24) mal("truncated header");
+    const cudaStream_t st = S(stream);
+    const uint8_t* b = static_cast<const uint8_t*>(d_wire);
+    uint32_t h[6];
+    DQ_CUDA(cudaMemcpyAsync(h, b, 24, cudaMemcpyDeviceToHost, st));
+    DQ_CUDA(cudaStreamSynchronize(st));
+    const uint32_t count = h[1], r8 = h[2], r4 = h[3], r2 = h[4], r16 = h[5];
+    if (static_cast<uint64_t>(r8) + r4 + r2 + r16 != count) mal("width run-lengths do not sum to the super-group count");
+    if (r16) invalid("width-16 passthrough is not supported by the device codec");
+    const Layout L{count, r8, r4};
+    // super-groups whose record fits in len (codec.cpp:380-383 checks each before reading it)
+    const uint64_t body = len - 24;
+    uint32_t fit = count;
+    if (L.pay_prefix(count) + static_cast<uint64_t>(kMetaBytes) * count > body) {
+      uint32_t lo = 0, hi = count;  // largest k with record_end(k) <= body
+      while (lo < hi) {
+        const uint32_t mid = lo + (hi - lo + 1) / 2;
+        if (L.pay_prefix(mid) + static_cast<uint64_t>(kMetaBytes) * mid <= body) lo = mid;
+        else hi = mid - 1;
+      }
+      fit = lo;
+    }
+    const bool write = d_soa && soa_cap >= L.bytes();
+    unsigned long long* bad = nullptr;
+    DQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bad), sizeof(*bad), st));
+    DQ_CUDA(cudaMemsetAsync(bad, 0xff, sizeof(*bad), st));
+    launch_from_wire(b, L, fit, write ? static_cast<uint8_t*>(d_soa) : nullptr, bad, st);
+    DQ_CUDA(cudaGetLastError());
+    unsigned long long hb = 0;
+    DQ_CUDA(cudaMemcpyAsync(&hb, bad, sizeof hb, cudaMemcpyDeviceToHost, st));
+    DQ_CUDA(cudaFreeAsync(bad, st));
+    DQ_CUDA(cudaStreamSynchronize(st));
+    if (hb != ~0ull) mal(hb & 1 ? "zero super-group scale with nonzero payload" : "zero super-group scale with nonzero group scale");
+    if (fit < count) mal("truncated super-group body");
+    if (24 + L.bytes() != len) mal("trailing bytes after chunk body");
+    if (d_soa && !write) invalid("output capacity");
+    *chunk_index = h[0];
+    *n8 = r8;
+    *n4 = r4;
+    *n2 = r2;
+  });
+}
+
 int dq_from_reference_wire(const void* h_ref, size_t len, void* h_soa, size_t soa_cap,
                            uint32_t* chunk_index, uint32_t* n8, uint32_t* n4, uint32_t* n2) {
   // strict parser with the reference's checks (codec.cpp:345-399), S=256, s=16, hierarchical

@@ -60,6 +60,12 @@ struct GatherArgs {
 void launch_gather_decode(const GatherArgs& g, uint32_t n_chunks, uint32_t max_nsg, cudaStream_t st);
 
 void launch_quant(const CodecArgs& a, int src, bool dar, cudaStream_t st);
+// reference wire format on the device (dq_wire.cu): SoA chunk -> header + records, and
+// records [0, fit) -> SoA (soa may be null: validate only) with the first malformed
+// super-group as min(i << 1 | kind) in *bad (initialised to ~0 by the caller)
+void launch_to_wire(const uint8_t* soa, const Layout& L, uint32_t chunk, uint8_t* out, cudaStream_t st);
+void launch_from_wire(const uint8_t* in, const Layout& L, uint32_t fit, uint8_t* soa, unsigned long long* bad,
+                      cudaStream_t st);
 // one ring hop over peer memory (gather source, SRC = 0); see CodecArgs peer fields
 void launch_quant_peer(const CodecArgs& a, bool dar, cudaStream_t st);
 uint32_t peer_unit(uint32_t nsg);  // super-groups per flag unit of a chunk (same on every rank)

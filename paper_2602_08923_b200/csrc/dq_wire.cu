@@ -1,0 +1,98 @@
+// dq_wire.cu — device-side reference wire format (proj/src/codec.cpp:319-399).
+//
+// The reference serializes a chunk as a 24-byte header {chunk, count, n8, n4, n2,
+// n16} (u32 little-endian) followed by one record per super-group in chunk order:
+// bf16 sg_scale | 16 u8 group codes | 32*w payload bytes.  The device layout is
+// the tiled SoA of dq_device.cuh; both are closed-form, so each super-group maps
+// record <-> SoA independently: one warp per super-group, 16-bit moves (every
+// record and SoA field starts at an even offset).  Parsing validates like the
+// reference's strict parser: the first offending super-group in chunk order
+// decides the message (codec.cpp:380-395), truncation and trailing bytes are
+// decided from the header on the host.
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+#include "dq_device.cuh"
+#include "dq_internal.h"
+
+namespace dq {
+
+namespace {
+
+constexpr int kWireThreads = 256;
+constexpr int kWireWarps = kWireThreads / 32;
+
+// byte offset of super-group i's record after the 24-byte header
+__device__ __forceinline__ uint64_t record_offset(const Layout& L, uint32_t i) {
+  return L.pay_prefix(i) + static_cast<uint64_t>(kMetaBytes) * i;
+}
+
+// SoA offset of halfword k of super-group i's record (k = 0 scale, 1..8 codes, 9.. payload)
+__device__ __forceinline__ uint64_t soa_half(const Layout::SG& g, uint32_t k) {
+  return k == 0 ? g.scale : (k < 9 ? g.codes + 2 * (k - 1) : g.payload + 2 * (k - 9));
+}
+
+__global__ void __launch_bounds__(kWireThreads) k_to_wire(const uint8_t* __restrict__ soa, Layout L, uint32_t chunk,
+                                                          uint8_t* __restrict__ out) {
+  if (blockIdx.x == 0 && threadIdx.x < 6) {
+    const uint32_t v[6] = {chunk, L.nsg, L.n8, L.n4, L.n2(), 0u};
+    reinterpret_cast<uint32_t*>(out)[threadIdx.x] = v[threadIdx.x];  // little-endian like BitWriter
+  }
+  const uint32_t lane = threadIdx.x & 31;
+  uint16_t* rec_base = reinterpret_cast<uint16_t*>(out + 24);
+  for (uint32_t i = blockIdx.x * kWireWarps + (threadIdx.x >> 5); i < L.nsg; i += gridDim.x * kWireWarps) {
+    const Layout::SG g = L.locate(i);
+    uint16_t* rec = rec_base + record_offset(L, i) / 2;
+    const uint32_t halves = (kMetaBytes + 32 * g.width) / 2;
+    for (uint32_t k = lane; k < halves; k += 32)
+      rec[k] = *reinterpret_cast<const uint16_t*>(soa + soa_half(g, k));
+  }
+}
+
+// Copies (soa != nullptr) and validates super-groups [0, fit): bad = min over
+// offending super-groups of (i << 1 | kind), kind 0 = zero sg_scale with a
+// nonzero group code, 1 = zero sg_scale with a nonzero payload byte.
+__global__ void __launch_bounds__(kWireThreads) k_from_wire(const uint8_t* __restrict__ in, Layout L, uint32_t fit,
+                                                            uint8_t* __restrict__ soa,
+                                                            unsigned long long* __restrict__ bad) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint16_t* rec_base = reinterpret_cast<const uint16_t*>(in + 24);
+  for (uint32_t i = blockIdx.x * kWireWarps + (threadIdx.x >> 5); i < fit; i += gridDim.x * kWireWarps) {
+    const Layout::SG g = L.locate(i);
+    const uint16_t* rec = rec_base + record_offset(L, i) / 2;
+    const uint32_t halves = (kMetaBytes + 32 * g.width) / 2;
+    uint32_t codes_or = 0, pay_or = 0;
+    for (uint32_t k = lane; k < halves; k += 32) {
+      const uint16_t v = rec[k];
+      if (soa) *reinterpret_cast<uint16_t*>(soa + soa_half(g, k)) = v;
+      if (k >= 1 && k < 9) codes_or |= v;
+      else if (k >= 9) pay_or |= v;
+    }
+    const bool zero_scale = rec[0] == 0;  // both scale bytes zero
+    const bool codes_nz = __any_sync(0xffffffffu, codes_or != 0);
+    const bool pay_nz = __any_sync(0xffffffffu, pay_or != 0);
+    if (lane == 0 && zero_scale && (codes_nz || pay_nz))
+      atomicMin(bad, (static_cast<unsigned long long>(i) << 1) | (codes_nz ? 0ull : 1ull));
+  }
+}
+
+uint32_t wire_grid(uint32_t nsg) {
+  const uint32_t want = (nsg + kWireWarps - 1) / kWireWarps;
+  const uint32_t cap = 148u * 16;
+  return want == 0 ? 1 : (want < cap ? want : cap);
+}
+
+}  // namespace
+
+void launch_to_wire(const uint8_t* soa, const Layout& L, uint32_t chunk, uint8_t* out, cudaStream_t st) {
+  k_to_wire<<<wire_grid(L.nsg), kWireThreads, 0, st>>>(soa, L, chunk, out);
+}
+
+void launch_from_wire(const uint8_t* in, const Layout& L, uint32_t fit, uint8_t* soa, unsigned long long* bad,
+                      cudaStream_t st) {
+  if (fit == 0) return;
+  k_from_wire<<<wire_grid(fit), kWireThreads, 0, st>>>(in, L, fit, soa, bad);
+}
+
+}  // namespace dq
