@@ -517,16 +517,14 @@ static int cmp_dbl(const void* a, const void* b) {
   double x = *(const double*)a, y = *(const double*)b;
   return x < y ? -1 : x > y;
 }
-/* proj/src/allocation.cpp:302-310: stable class order 8,4,2,16 */
+/* proj/src/allocation.cpp:302-310: stable sort by rank(w) = 16 - w, width 16 last
+ * (0x100): class order 8,4,2,1,16 (counting sort over the 513 possible ranks) */
+static int perm_rank(uint8_t w) { return (w == 16 ? 0x100 : 16 - (int)w) + 256; }
 int dqo_build_permutation(const uint8_t* widths, size_t nsg, uint32_t* perm) {
-  size_t cnt[4] = {0, 0, 0, 0};
-  for (size_t i = 0; i < nsg; ++i) {
-    int c = cls_of(widths[i]);
-    if (c < 0) return fail(DQO_EINVAL, "unsupported width");
-    cnt[c]++;
-  }
-  size_t start[4] = {0, cnt[0], cnt[0] + cnt[1], cnt[0] + cnt[1] + cnt[2]};
-  for (size_t i = 0; i < nsg; ++i) perm[start[cls_of(widths[i])]++] = (uint32_t)i;
+  size_t cnt[514] = {0};
+  for (size_t i = 0; i < nsg; ++i) cnt[perm_rank(widths[i]) + 1]++;
+  for (int r = 0; r < 513; ++r) cnt[r + 1] += cnt[r];
+  for (size_t i = 0; i < nsg; ++i) perm[cnt[perm_rank(widths[i])]++] = (uint32_t)i;
   return 0;
 }
 /* proj/src/allocation.cpp:45-58 */
@@ -608,6 +606,176 @@ int dqo_allocate_fast(const float* F, size_t nsg, double b, uint32_t s, uint32_t
   return 0;
 }
 
+/* general allocator: proj/src/allocation.cpp:14-33 (widths), 44-58 (budget),
+ * 60-90 (threshold ratios), 92-115 (chain, widths at a base), 121-168 (search) */
+static long long ipow4(int e) {
+  long long r = 1;
+  for (int i = 0; i < e; ++i) r *= 4;
+  return r;
+}
+static long long gcdll(long long a, long long b) {
+  while (b) {
+    long long t = a % b;
+    a = b;
+    b = t;
+  }
+  return a < 0 ? -a : a;
+}
+static int gen_level(double f, const double* chain, int nc, double base) {
+  int level = 0;
+  for (int k = 0; k < nc; ++k)
+    if (f >= base * chain[k]) level = k + 1;
+  return level;
+}
+int dqo_allocate_general(const float* F, size_t nsg, double b, uint32_t s, uint32_t S, int hier, const int* W,
+                         int n_w, uint8_t* widths, uint32_t* perm, double* u_out, uint64_t* payload_out) {
+  static const int allowed[] = {1, 2, 4, 8, 16};
+  if (n_w <= 0) return fail(DQO_EINVAL, "width set is empty");
+  for (int i = 0; i < n_w; ++i) {
+    int ok = 0;
+    for (int k = 0; k < 5; ++k) ok |= W[i] == allowed[k];
+    if (!ok) return fail(DQO_EINVAL, "unsupported width");
+    if (i > 0 && W[i] <= W[i - 1]) return fail(DQO_EINVAL, "width set must be strictly ascending");
+  }
+  if (!s || S % s) return fail(DQO_EINVAL, "invalid group sizes");
+  const double bbar = b - (hier ? 8.0 / s + 16.0 / S : 16.0 / s);
+  if (!(bbar > W[0])) return fail(DQO_EINFEASIBLE, "payload budget does not exceed the minimum width");
+  const double budget = (double)((uint64_t)nsg * S) * bbar;
+  for (size_t j = 0; j < nsg; ++j)
+    if (!(F[j] >= 0.0f)) return fail(DQO_EINVAL, "squared norms must be non-negative");
+  double u = 0.0;
+  if (n_w == 1) {
+    for (size_t j = 0; j < nsg; ++j) widths[j] = (uint8_t)W[0];
+  } else {
+    const int nc = n_w - 1;
+    double chain[4];
+    chain[0] = 1.0;
+    for (int k = 0; k + 1 < nc; ++k) {
+      const int a = W[k], bb = W[k + 1], c = W[k + 2];
+      long long num = (ipow4(c - bb) - 1) * (bb - a);
+      long long den = ipow4(c - bb) * (c - bb) * (ipow4(bb - a) - 1);
+      const long long g = gcdll(num, den);
+      num /= g;
+      den /= g;
+      chain[k + 1] = chain[k] / ((double)num / (double)den);
+    }
+    double* pts = (double*)malloc(sizeof(double) * (nsg * (size_t)nc + 1));
+    size_t np = 0;
+    for (size_t j = 0; j < nsg; ++j) {
+      if (F[j] <= 0.0f) continue;
+      for (int k = 0; k < nc; ++k) pts[np++] = (double)F[j] / chain[k];
+    }
+    qsort(pts, np, sizeof(double), cmp_dbl);
+    size_t nu = 0;
+    for (size_t i = 0; i < np; ++i)
+      if (nu == 0 || pts[i] != pts[nu - 1]) pts[nu++] = pts[i];
+    pts[nu] = nu ? pts[nu - 1] * 2.0 + 1.0 : 1.0; /* all-min plateau */
+    const size_t M = nu + 1;
+#define GEN_PAYLOAD(base, res)                                                   \
+  do {                                                                           \
+    uint64_t p_ = 0;                                                             \
+    for (size_t j_ = 0; j_ < nsg; ++j_)                                          \
+      p_ += (uint64_t)W[gen_level((double)F[j_], chain, nc, (base))] * S;        \
+    res = p_;                                                                    \
+  } while (0)
+    size_t lo = 0, hi = M - 1;
+    uint64_t p;
+    GEN_PAYLOAD(pts[lo], p);
+    if ((double)p > budget) {
+      while (lo + 1 < hi) {
+        const size_t mid = (lo + hi) / 2;
+        GEN_PAYLOAD(pts[mid], p);
+        if ((double)p <= budget) hi = mid; else lo = mid;
+      }
+      lo = hi;
+    }
+#undef GEN_PAYLOAD
+    u = pts[lo];
+    free(pts);
+    for (size_t j = 0; j < nsg; ++j) widths[j] = (uint8_t)W[gen_level((double)F[j], chain, nc, u)];
+  }
+  uint64_t pay = 0;
+  for (size_t j = 0; j < nsg; ++j) pay += (uint64_t)widths[j] * S;
+  if ((double)pay > budget) return fail(DQO_EINFEASIBLE, "bit allocation infeasible within budget");
+  *u_out = u;
+  *payload_out = pay;
+  if (perm) dqo_build_permutation(widths, nsg, perm);
+  return 0;
+}
+
+/* cross-round fast allocator: proj/src/allocation.cpp:262-300.  state = {lo, hi, u}
+ * (FastAllocatorState, allocation.hpp:75-79), updated in place. */
+int dqo_allocate_fast_stateful(const float* F, size_t nsg, double b, uint32_t s, uint32_t S, int hier,
+                               double state[3], uint8_t* widths, uint32_t* perm, double* u_out,
+                               uint64_t* payload_out) {
+  double bbar;
+  int rc = bbar_of(b, s, S, hier, &bbar);
+  if (rc) return rc;
+  const double alpha = 4.0 / log2(512.0 / 17.0);
+  const double budget = (double)nsg * S * bbar;
+#define FAST_AT(uu, wout, res)                                                   \
+  do {                                                                           \
+    const float t24_ = (float)exp2((4.0 - (uu)) / alpha);                        \
+    const float t48_ = (float)exp2((8.0 - (uu)) / alpha);                        \
+    uint64_t p_ = 0;                                                             \
+    for (size_t j_ = 0; j_ < nsg; ++j_) {                                        \
+      const uint8_t w_ = F[j_] >= t48_ ? 8 : F[j_] >= t24_ ? 4 : 2;              \
+      if (wout) ((uint8_t*)(wout))[j_] = w_;                                     \
+      p_ += (uint64_t)w_ * S;                                                    \
+    }                                                                            \
+    res = p_;                                                                    \
+  } while (0)
+  uint64_t pay;
+  FAST_AT(state[2], widths, pay);
+  const int over = (double)pay > budget;
+  if (over) {
+    /* largest in-budget plateau sample at or below the carried u, scanning down */
+    double* flips = (double*)malloc(sizeof(double) * (2 * nsg + 1));
+    size_t nf = 0;
+    for (size_t j = 0; j < nsg; ++j) {
+      if (F[j] <= 0.0f) continue;
+      const double l = alpha * log2((double)F[j]);
+      flips[nf++] = 4.0 - l;
+      flips[nf++] = 8.0 - l;
+    }
+    qsort(flips, nf, sizeof(double), cmp_dbl);
+    size_t nu = 0;
+    for (size_t i = 0; i < nf; ++i)
+      if (nu == 0 || flips[i] != flips[nu - 1]) flips[nu++] = flips[i];
+    size_t ns = nu ? nu + 1 : 1;
+    double* samp = (double*)malloc(sizeof(double) * ns);
+    if (!nu) samp[0] = 0.0;
+    else {
+      samp[0] = flips[0] - 1.0;
+      for (size_t i = 0; i + 1 < nu; ++i) samp[i + 1] = 0.5 * (flips[i] + flips[i + 1]);
+      samp[nu] = flips[nu - 1] + 1.0;
+      for (size_t i = 0; i < ns; ++i) samp[i] = samp[i] < -1e6 ? -1e6 : samp[i] > 1e6 ? 1e6 : samp[i];
+    }
+    free(flips);
+    double chosen = -1e6;
+    for (size_t i = ns; i-- > 0;) {
+      if (samp[i] > state[2]) continue;
+      uint64_t p;
+      FAST_AT(samp[i], (uint8_t*)NULL, p);
+      if ((double)p <= budget) {
+        chosen = samp[i];
+        break;
+      }
+    }
+    free(samp);
+    FAST_AT(chosen, widths, pay);
+    if ((double)pay > budget) return fail(DQO_EINFEASIBLE, "bit allocation infeasible within budget");
+  }
+#undef FAST_AT
+  *u_out = state[2];
+  *payload_out = pay;
+  if (perm) dqo_build_permutation(widths, nsg, perm);
+  if (over) state[1] = state[2];
+  else state[0] = state[2];
+  state[2] = 0.5 * (state[0] + state[1]);
+  return 0;
+}
+
 /* ------------------------------------------------------------ schedules   */
 typedef struct { uint32_t snd, rcv, slot; } rev_t;
 typedef struct {
@@ -663,8 +831,6 @@ int dqo_run_round(const float* const* workers, size_t d, const dqo_round_cfg* cf
     return fail(DQO_EINVAL, "fixed-width allocator requires variable_width off and vice versa");
   if (cfg->topology == 1 && (n & (n - 1))) return fail(DQO_EINVAL, "butterfly topology requires a power-of-two worker count");
   if (!d) return fail(DQO_EINVAL, "empty gradient");
-  if (cfg->allocator == 0 && cfg->variable_width && cfg->codec == 0)
-    return fail(DQO_EINVAL, "restatement covers the fast and fixed allocators only");
 
   double* exact = (double*)calloc(d, sizeof(double));
   for (uint32_t r = 0; r < n; ++r)
@@ -695,6 +861,10 @@ int dqo_run_round(const float* const* workers, size_t d, const dqo_round_cfg* cf
     if (!rc && cfg->fixed_width > bbar) rc = fail(DQO_EINFEASIBLE, "fixed width exceeds the payload budget");
     memset(widths, cfg->fixed_width, T);
     out->payload_bits = (uint64_t)T * S * cfg->fixed_width;
+  } else if (cfg->allocator == 0) {
+    static const int W248[3] = {2, 4, 8};  /* engine.cpp:306-307 */
+    rc = dqo_allocate_general(gs, T, cfg->budget_bits, s, S, cfg->hierarchical, W248, 3, widths, NULL, &out->u,
+                              &out->payload_bits);
   } else {
     rc = dqo_allocate_fast(gs, T, cfg->budget_bits, s, S, cfg->hierarchical, widths, NULL, &out->u,
                            &out->payload_bits);

@@ -101,6 +101,13 @@ typedef struct {
   int P##allocate_fast(const float* sq_norms, size_t nsg, double budget_bits, uint32_t s,   \
                        uint32_t S, int hierarchical, uint8_t* widths, uint32_t* perm,       \
                        double* u, uint64_t* payload_bits);                                  \
+  int P##allocate_general(const float* sq_norms, size_t nsg, double budget_bits, uint32_t s,\
+                          uint32_t S, int hierarchical, const int* W, int n_w,              \
+                          uint8_t* widths, uint32_t* perm, double* u, uint64_t* payload_bits);\
+  int P##allocate_fast_stateful(const float* sq_norms, size_t nsg, double budget_bits,      \
+                                uint32_t s, uint32_t S, int hierarchical, double state[3],  \
+                                uint8_t* widths, uint32_t* perm, double* u,                 \
+                                uint64_t* payload_bits);                                    \
   int P##build_permutation(const uint8_t* widths, size_t nsg, uint32_t* perm);              \
   int P##run_round(const float* const* workers, size_t d, const dqo_round_cfg* cfg,         \
                    float* synced, uint8_t* widths, uint32_t* perm, dqo_round_out* out);     \

@@ -102,6 +102,10 @@ class Oracle:
         f("reduce_stats", i32, [P(C.c_float), P(C.c_float), u32, sz, P(C.c_float), P(C.c_float)])
         f("allocate_fast", i32, [P(C.c_float), sz, dbl, u32, u32, i32, P(C.c_uint8), P(u32),
                                  P(dbl), P(u64)])
+        f("allocate_general", i32, [P(C.c_float), sz, dbl, u32, u32, i32, P(i32), i32, P(C.c_uint8),
+                                    P(u32), P(dbl), P(u64)])
+        f("allocate_fast_stateful", i32, [P(C.c_float), sz, dbl, u32, u32, i32, P(dbl), P(C.c_uint8),
+                                          P(u32), P(dbl), P(u64)])
         f("build_permutation", i32, [P(C.c_uint8), sz, P(u32)])
         f("run_round", i32, [P(P(C.c_float)), sz, P(RoundCfg), P(C.c_float), P(C.c_uint8),
                              P(u32), P(RoundOut)])
@@ -216,6 +220,33 @@ class Oracle:
         self._check(self._allocate_fast(_p(f, C.c_float), f.size, budget_bits, s, S, int(hierarchical),
                                         _p(w, C.c_uint8), _p(p, C.c_uint32), C.byref(u), C.byref(pay)))
         return w[: f.size], p[: f.size], u.value, pay.value
+
+    def allocate_general(self, F, budget_bits, widths=(2, 4, 8), s=16, S=256, hierarchical=True):
+        """proj/src/allocation.cpp:121-168 -> (widths, permutation, u = resolved base threshold, payload)"""
+        f = np.ascontiguousarray(F, np.float32)
+        W = np.ascontiguousarray(widths, np.int32)
+        w = np.zeros(max(f.size, 1), np.uint8)
+        p = np.zeros(max(f.size, 1), np.uint32)
+        u = C.c_double()
+        pay = C.c_uint64()
+        self._check(self._allocate_general(_p(f, C.c_float), f.size, budget_bits, s, S, int(hierarchical),
+                                           _p(W, C.c_int), W.size, _p(w, C.c_uint8), _p(p, C.c_uint32),
+                                           C.byref(u), C.byref(pay)))
+        return w[: f.size], p[: f.size], u.value, pay.value
+
+    def allocate_fast_stateful(self, F, budget_bits, state, s=16, S=256, hierarchical=True):
+        """proj/src/allocation.cpp:262-300; state = [lo, hi, u] (FastAllocatorState) ->
+        (widths, permutation, u used this round, payload, next state)"""
+        f = np.ascontiguousarray(F, np.float32)
+        st = np.array(state, np.float64)
+        w = np.zeros(max(f.size, 1), np.uint8)
+        p = np.zeros(max(f.size, 1), np.uint32)
+        u = C.c_double()
+        pay = C.c_uint64()
+        self._check(self._allocate_fast_stateful(_p(f, C.c_float), f.size, budget_bits, s, S, int(hierarchical),
+                                                 _p(st, C.c_double), _p(w, C.c_uint8), _p(p, C.c_uint32),
+                                                 C.byref(u), C.byref(pay)))
+        return w[: f.size], p[: f.size], u.value, pay.value, [float(x) for x in st]
 
     def build_permutation(self, widths):
         w = np.ascontiguousarray(widths, np.uint8)

@@ -167,6 +167,33 @@ int dqref_allocate_fast(const float* F, size_t nsg, double b, uint32_t s, uint32
     *payload_bits = a.payload_bits;
   });
 }
+int dqref_allocate_general(const float* F, size_t nsg, double b, uint32_t s, uint32_t S, int hier, const int* W,
+                           int n_w, uint8_t* widths, uint32_t* perm, double* u, uint64_t* payload_bits) {
+  return guarded([&] {
+    BudgetSpec spec{b, s, S, std::vector<int>(W, W + (n_w > 0 ? n_w : 0)), hier != 0};
+    BitAllocation a = allocate_general({F, nsg}, spec);
+    std::memcpy(widths, a.widths.data(), nsg);
+    if (perm) std::memcpy(perm, a.permutation.data(), nsg * sizeof(uint32_t));
+    *u = a.u;
+    *payload_bits = a.payload_bits;
+  });
+}
+int dqref_allocate_fast_stateful(const float* F, size_t nsg, double b, uint32_t s, uint32_t S, int hier,
+                                 double state[3], uint8_t* widths, uint32_t* perm, double* u,
+                                 uint64_t* payload_bits) {
+  return guarded([&] {
+    BudgetSpec spec{b, s, S, {2, 4, 8}, hier != 0};
+    FastAllocatorState st{state[0], state[1], state[2]};
+    BitAllocation a = allocate_fast_stateful({F, nsg}, spec, st);
+    std::memcpy(widths, a.widths.data(), nsg);
+    if (perm) std::memcpy(perm, a.permutation.data(), nsg * sizeof(uint32_t));
+    *u = a.u;
+    *payload_bits = a.payload_bits;
+    state[0] = st.lo;
+    state[1] = st.hi;
+    state[2] = st.u;
+  });
+}
 int dqref_build_permutation(const uint8_t* widths, size_t nsg, uint32_t* perm) {
   return guarded([&] {
     auto p = build_permutation({widths, nsg});

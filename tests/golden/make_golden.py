@@ -92,14 +92,23 @@ def main():
             al.append({"name": name, "b": b, "F_sha": f32sha(F), "widths_sha": sha(w.tobytes()),
                        "perm_sha": sha(p.astype(np.uint32).tobytes()), "u": u.hex(), "payload_bits": pay})
     g["allocation"] = al
+    ga = []
+    for name, F in Fs.items():
+        for W in ((2, 4, 8), (1, 2, 4, 8, 16)):
+            for b in (3, 5):
+                w, p, u, pay = R.allocate_general(F, b, W)
+                ga.append({"name": name, "b": b, "W": list(W), "widths_sha": sha(w.tobytes()),
+                           "perm_sha": sha(p.astype(np.uint32).tobytes()), "u": u.hex(), "payload_bits": pay})
+    g["allocation_general"] = ga
     g["allocation_inputs"] = {"rng_seed": 5, "note": "F arrays regenerated by the same numpy calls"}
     rounds = []
-    for (n, d, b, topo, seed) in [(4, 1 << 14, 4, "ring", 1), (4, (1 << 13) + 77, 5, "ring", 2),
-                                  (8, 1 << 14, 4, "butterfly", 1), (3, 1 << 13, 6, "ring", 3),
-                                  (2, 1 << 13, 3, "butterfly", 4)]:
+    for (n, d, b, topo, seed, alloc) in [(4, 1 << 14, 4, "ring", 1, "fast"), (4, (1 << 13) + 77, 5, "ring", 2, "fast"),
+                                         (8, 1 << 14, 4, "butterfly", 1, "fast"), (3, 1 << 13, 6, "ring", 3, "fast"),
+                                         (2, 1 << 13, 3, "butterfly", 4, "fast"),
+                                         (4, 1 << 14, 4, "ring", 5, "general")]:
         ws = [R.generate_worker(d, seed=seed, sigma_log=4.0, rank=r) for r in range(n)]
-        res = R.run_round(ws, R.round_cfg(n, b, topo, seed=seed))
-        rounds.append({"n": n, "d": d, "b": b, "topology": topo, "seed": seed,
+        res = R.run_round(ws, R.round_cfg(n, b, topo, seed=seed, allocator=alloc))
+        rounds.append({"n": n, "d": d, "b": b, "topology": topo, "seed": seed, "allocator": alloc,
                        "inputs_sha": sha(b"".join(w.tobytes() for w in ws)),
                        "wire_hash": f"{res['wire_hash']:016x}", "synced_sha": f32sha(res["synced"]),
                        "widths_sha": sha(res["widths"].tobytes()), "perm_sha": sha(res["perm"].tobytes()),

@@ -126,11 +126,20 @@ def test_golden_allocation(port):
         assert u.hex() == a["u"] and pay == a["payload_bits"]
 
 
+def test_golden_general_allocation(port):
+    Fs = golden_F()
+    for a in GOLD["allocation_general"]:
+        w, p, u, pay = port.allocate_general(Fs[a["name"]], a["b"], tuple(a["W"]))
+        assert sha(w.tobytes()) == a["widths_sha"] and sha(p.astype(np.uint32).tobytes()) == a["perm_sha"]
+        assert u.hex() == a["u"] and pay == a["payload_bits"]
+
+
 def test_golden_rounds(port):
     for g in GOLD["rounds"]:
         ws = [port.generate_worker(g["d"], seed=g["seed"], sigma_log=4.0, rank=r) for r in range(g["n"])]
         assert sha(b"".join(w.tobytes() for w in ws)) == g["inputs_sha"]
-        res = port.run_round(ws, port.round_cfg(g["n"], g["b"], g["topology"], seed=g["seed"]))
+        res = port.run_round(ws, port.round_cfg(g["n"], g["b"], g["topology"], seed=g["seed"],
+                                                allocator=g.get("allocator", "fast")))
         assert f"{res['wire_hash']:016x}" == g["wire_hash"]
         assert f32sha(res["synced"]) == g["synced_sha"]
         assert sha(res["widths"].tobytes()) == g["widths_sha"] and sha(res["perm"].tobytes()) == g["perm_sha"]
@@ -187,6 +196,79 @@ def test_live_allocation_vs_reference(port, ref):
             got = port.allocate_fast(F, b)
             for a, c in zip(got, want):
                 assert np.array_equal(a, c)
+
+
+def _general_cases():
+    rng = np.random.default_rng(11)
+    yield np.exp(6 * rng.standard_normal(3000)).astype(np.float32)
+    yield np.zeros(10, np.float32)
+    yield np.array([1e-30, 5e-31, 0.0], np.float32)
+    yield np.repeat(np.float32(7.0), 33)
+    f = np.exp(3 * rng.standard_normal(2000)).astype(np.float32)
+    yield np.concatenate([f, f * np.float32(512 / 17), f])  # points colliding across the chain
+
+
+@pytest.mark.parametrize("W", [(2, 4, 8), (1, 2, 4, 8, 16), (4,), (2, 8), (1, 2), (2, 4, 8, 16)])
+def test_live_general_allocation_vs_reference(port, ref, W):
+    """proj/src/allocation.cpp:121-168 (allocate_general), every width set it accepts."""
+    for F in _general_cases():
+        for b in (2.2, 3, 4.5, 8, 17):
+            for hier in (True, False):
+                try:
+                    want = ref.allocate_general(F, b, W, hierarchical=hier)
+                except OracleError as e:
+                    with pytest.raises(OracleError) as e2:
+                        port.allocate_general(F, b, W, hierarchical=hier)
+                    assert e2.value.code == e.code
+                    continue
+                got = port.allocate_general(F, b, W, hierarchical=hier)
+                for a, c in zip(got, want):
+                    assert np.array_equal(a, c)
+
+
+def test_general_allocation_rejects_like_reference(port, ref):
+    F = np.ones(8, np.float32)
+    for W, Fx in [((2, 4, 3), F), ((3,), F), ((), F), ((2, 4, 8), np.array([1, -1], np.float32)),
+                  ((2, 4, 8), np.array([np.nan], np.float32))]:
+        with pytest.raises(OracleError) as a:
+            ref.allocate_general(Fx, 5, W)
+        with pytest.raises(OracleError) as c:
+            port.allocate_general(Fx, 5, W)
+        assert a.value.code == c.value.code == 2
+
+
+def test_live_stateful_fast_vs_reference(port, ref):
+    """proj/src/allocation.cpp:262-300: the carried u, its projection and the bisection step."""
+    rng = np.random.default_rng(5)
+    for b in (3, 4, 6):
+        s_port = s_ref = [-1e6, 1e6, 0.0]
+        for rnd in range(12):
+            F = np.exp((4 + rnd % 3) * rng.standard_normal(1500)).astype(np.float32)
+            try:
+                want = ref.allocate_fast_stateful(F, b, s_ref)
+            except OracleError as e:
+                with pytest.raises(OracleError) as e2:
+                    port.allocate_fast_stateful(F, b, s_port)
+                assert e2.value.code == e.code
+                continue
+            got = port.allocate_fast_stateful(F, b, s_port)
+            for a, c in zip(got[:4], want[:4]):
+                assert np.array_equal(a, c)
+            assert got[4] == want[4]
+            s_port, s_ref = got[4], want[4]
+
+
+@pytest.mark.parametrize("topo,n,b", [("ring", 4, 4), ("butterfly", 4, 3)])
+def test_live_round_general_allocator_vs_reference(port, ref, topo, n, b):
+    d = 3 * (1 << 12) + 5
+    ws = [ref.generate_worker(d, seed=n, sigma_log=2.0, rank=r) for r in range(n)]
+    cfg = port.round_cfg(n, b, topo, seed=2, allocator="general")
+    x, y = port.run_round(ws, cfg), ref.run_round(ws, cfg)
+    for k in x:
+        if isinstance(x[k], np.ndarray):
+            assert np.array_equal(x[k], y[k]), k
+        else:
+            assert x[k] == y[k], k
 
 
 # ------------------------------------- 4. reference property tests on the port
