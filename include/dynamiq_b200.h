@@ -48,8 +48,8 @@ enum dq_allocator { DQ_ALLOC_GENERAL = 0, DQ_ALLOC_FAST = 1, DQ_ALLOC_FIXED = 2 
 
 /* [proj/include/dynamiq/engine.hpp:22-43 PipelineConfig] — same fields and
  * defaults (dq_config_default).  Supported on device: group_size 16,
- * super_group_size 256, hierarchical scales, quantized codec, fast or fixed
- * allocator; non_uniform and correlated may be toggled. */
+ * super_group_size 256, hierarchical scales, quantized codec, fast, general
+ * or fixed allocator; non_uniform and correlated may be toggled. */
 typedef struct dq_config {
   uint32_t n_workers;
   uint32_t group_size;
@@ -149,6 +149,19 @@ int dq_reduce_stats(const float* d_means, const float* d_sqs, uint32_t n_workers
 int dq_allocate_fast(dq_ctx* ctx, const float* d_sq_norms, size_t n_sg, double budget_bits,
                      uint8_t* d_widths, uint32_t* d_perm, double* u, uint64_t* payload_bits,
                      uint32_t counts[3], void* stream);
+/* [allocation.hpp:57 allocate_general], W = {2,4,8} (the width set run_round uses,
+ * engine.cpp:306-307): crossing points sorted on the device, the reference's
+ * bisection driven from the host (one probe kernel + sync per step).  u = the
+ * resolved base threshold.  DQ_EINVAL for negative/NaN norms. */
+int dq_allocate_general(dq_ctx* ctx, const float* d_sq_norms, size_t n_sg, double budget_bits,
+                        uint8_t* d_widths, uint32_t* d_perm, double* u, uint64_t* payload_bits,
+                        uint32_t counts[3], void* stream);
+/* [allocation.hpp:75-81 allocate_fast_stateful + FastAllocatorState] state =
+ * {lo, hi, u} (defaults {-1e6, 1e6, 0}), updated in place by one bisection step;
+ * *u = the carried u this round used. */
+int dq_allocate_fast_stateful(dq_ctx* ctx, const float* d_sq_norms, size_t n_sg, double budget_bits,
+                              double state[3], uint8_t* d_widths, uint32_t* d_perm, double* u,
+                              uint64_t* payload_bits, uint32_t counts[3], void* stream);
 
 /* ---- the all-reduce ------------------------------------------------------ */
 /* [engine.hpp:63-64 run_round] all cfg.n_workers gradients resident on this

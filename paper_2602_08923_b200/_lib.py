@@ -97,6 +97,10 @@ SIGNATURES = {
     "dq_reduce_stats": (C.c_int, [_V, _V, C.c_uint32, C.c_size_t, _V, _V, _V]),
     "dq_allocate_fast": (C.c_int, [_V, _V, C.c_size_t, C.c_double, _V, _V, _P(C.c_double), _P(C.c_uint64),
                                    _u32p, _V]),
+    "dq_allocate_general": (C.c_int, [_V, _V, C.c_size_t, C.c_double, _V, _V, _P(C.c_double), _P(C.c_uint64),
+                                      _P(C.c_uint32), _V]),
+    "dq_allocate_fast_stateful": (C.c_int, [_V, _V, C.c_size_t, C.c_double, _P(C.c_double), _V, _V,
+                                            _P(C.c_double), _P(C.c_uint64), _P(C.c_uint32), _V]),
     "dq_sim_round": (C.c_int, [_V, _P(_V), C.c_size_t, _V, C.c_int, _P(RoundInfo), _V]),
     "dq_run_round_host": (C.c_int, [_V, _P(_V), C.c_size_t, _V, _P(RoundInfo), _V]),
     "dq_round_allocation": (C.c_int, [_V, _u8p, _u32p, C.c_size_t]),

@@ -360,6 +360,47 @@ def allocate_fast(sq_norms: torch.Tensor, budget_bits: float, ctx: Optional[Cont
     return BitAllocation(widths[:T], perm[:T], pay.value, u.value, tuple(counts))
 
 
+def allocate_general(sq_norms: torch.Tensor, budget_bits: float, ctx: Optional[Context] = None) -> BitAllocation:
+    """proj/src/allocation.cpp:121-168 (W = {2,4,8}, the set run_round uses) + build_permutation;
+    ``u`` is the resolved base threshold."""
+    ctx = ctx or _ctx_for(PipelineConfig())
+    F = _f32(sq_norms, sq_norms.numel(), "sq_norms")
+    T = F.numel()
+    widths = torch.empty(max(T, 1), dtype=torch.uint8, device=F.device)
+    perm = torch.empty(max(T, 1), dtype=torch.int32, device=F.device)
+    u, pay = C.c_double(), C.c_uint64()
+    counts = (C.c_uint32 * 3)()
+    check(lib().dq_allocate_general(ctx.h, _ptr(F), T, float(budget_bits), _ptr(widths), _ptr(perm), C.byref(u),
+                                    C.byref(pay), counts, _stream()))
+    return BitAllocation(widths[:T], perm[:T], pay.value, u.value, tuple(counts))
+
+
+@dataclass
+class FastAllocatorState:
+    """proj/include/dynamiq/allocation.hpp:75-79"""
+    lo: float = -1e6
+    hi: float = 1e6
+    u: float = 0.0
+
+
+def allocate_fast_stateful(sq_norms: torch.Tensor, budget_bits: float, state: FastAllocatorState,
+                           ctx: Optional[Context] = None) -> BitAllocation:
+    """proj/src/allocation.cpp:262-300: widths at the carried ``state.u`` (projected to the
+    largest in-budget plateau when over budget); ``state`` takes one bisection step."""
+    ctx = ctx or _ctx_for(PipelineConfig())
+    F = _f32(sq_norms, sq_norms.numel(), "sq_norms")
+    T = F.numel()
+    widths = torch.empty(max(T, 1), dtype=torch.uint8, device=F.device)
+    perm = torch.empty(max(T, 1), dtype=torch.int32, device=F.device)
+    st = (C.c_double * 3)(state.lo, state.hi, state.u)
+    u, pay = C.c_double(), C.c_uint64()
+    counts = (C.c_uint32 * 3)()
+    check(lib().dq_allocate_fast_stateful(ctx.h, _ptr(F), T, float(budget_bits), st, _ptr(widths), _ptr(perm),
+                                          C.byref(u), C.byref(pay), counts, _stream()))
+    state.lo, state.hi, state.u = st[0], st[1], st[2]
+    return BitAllocation(widths[:T], perm[:T], pay.value, u.value, tuple(counts))
+
+
 @dataclass
 class RoundResult:
     """proj/include/dynamiq/engine.hpp:45-54 (exact fp64 sum not materialized)."""

@@ -190,6 +190,10 @@ struct dq_ctx {
   DevBuf<uint32_t> blockcnt, counts;
   DevBuf<FlipRec> nrec;                 // slow allocation path scratch
   DevBuf<unsigned long long> tcount;
+  DevBuf<uint64_t> gkeys, gsorted;       // general allocator: crossing points
+  DevBuf<uint8_t> gtemp;                 // CUB scratch
+  DevBuf<int> gnum;
+  DevBuf<double> gbase;
   DevBuf<const float*> xptrs;
   DevBuf<double> vn;
   DevBuf<uint8_t> msgs;   // message pool
@@ -342,7 +346,8 @@ void validate(const dq_config& c) {  // engine.cpp:243-255 + device coverage
     invalid("device codec supports group_size 16 and super_group_size 256");
   if (!c.hierarchical_scales) invalid("device codec supports hierarchical scales only");
   if (c.codec != 0) invalid("device codec supports the quantized codec only");
-  if (c.variable_width && c.allocator != DQ_ALLOC_FAST) invalid("device supports the fast allocator");
+  if (c.variable_width && c.allocator != DQ_ALLOC_FAST && c.allocator != DQ_ALLOC_GENERAL)
+    invalid("unknown allocator");
 }
 
 double payload_budget(const dq_config& c) {  // allocation.cpp:45-58
@@ -375,9 +380,93 @@ struct AllocResult {
   uint32_t n8 = 0, n4 = 0, n2 = 0, passes = 0;
 };
 
-// allocate_fast (allocation.cpp:228-260) + build_permutation; see dq_stats_alloc.cu
+// allocate_general for W = {2,4,8} (allocation.cpp:121-168), the round path's general
+// allocator (engine.cpp:306-307,322-323): crossing points sorted on the device, then the
+// reference's bisection over them driven from the host, one probe kernel per step.
+AllocResult allocate_general(dq_ctx* ctx, const dq_config& c, const float* dF, uint32_t T, uint8_t* dW,
+                             uint32_t* dP, cudaStream_t st) {
+  AllocResult r;
+  const uint32_t S = c.super_group_size;
+  AllocWork w = work_of(ctx, T);
+  const double bbar = payload_budget(c);
+  const double budget = static_cast<double>(static_cast<uint64_t>(T) * S) * bbar;
+  // threshold_chain({2,4,8}) (allocation.cpp:60-90): ratio (4^4-1)(4-2) / (4^4 4 (4^2-1)) = 17/512
+  const double c1 = 1.0 / (17.0 / 512.0);
+  ctx->gkeys.reserve(2ull * T + 1);
+  ctx->gsorted.reserve(2ull * T + 1);
+  const size_t tb = general_temp_bytes(T);
+  ctx->gtemp.reserve(tb + 1);
+  ctx->gnum.reserve(1);
+  ctx->gbase.reserve(1);
+  ctx->tcount.reserve(2);
+  unsigned long long* d_bad = ctx->tcount.p;
+  DQ_CUDA(launch_general_points(dF, T, c1, ctx->gkeys.p, ctx->gsorted.p, ctx->gtemp.p, tb, ctx->gnum.p, d_bad, st));
+  int nu = 0;
+  unsigned long long bad = 0;
+  DQ_CUDA(cudaMemcpyAsync(&nu, ctx->gnum.p, sizeof nu, cudaMemcpyDeviceToHost, st));
+  DQ_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof bad, cudaMemcpyDeviceToHost, st));
+  DQ_CUDA(cudaStreamSynchronize(st));
+  if (bad) invalid("squared norms must be non-negative");
+  uint32_t M = static_cast<uint32_t>(nu);
+  if (M) {
+    uint64_t last = 0;
+    DQ_CUDA(cudaMemcpy(&last, ctx->gkeys.p + M - 1, sizeof last, cudaMemcpyDeviceToHost));
+    if (last == ~0ull) --M;  // the non-positive F_j
+  }
+  // points[0..M) unique ascending, points[M] = the all-min plateau (allocation.cpp:146-147)
+  struct Probe {
+    double base;
+    uint64_t payload;
+  };
+  auto probe = [&](uint32_t idx) {
+    launch_general_counts(dF, T, ctx->gkeys.p, M, idx, c1, ctx->tcount.p, ctx->gbase.p, st);
+    unsigned long long cnt[2];
+    Probe p;
+    DQ_CUDA(cudaMemcpyAsync(cnt, ctx->tcount.p, sizeof cnt, cudaMemcpyDeviceToHost, st));
+    DQ_CUDA(cudaMemcpyAsync(&p.base, ctx->gbase.p, sizeof p.base, cudaMemcpyDeviceToHost, st));
+    DQ_CUDA(cudaStreamSynchronize(st));
+    p.payload = static_cast<uint64_t>(S) * (2ull * T + 2ull * cnt[1] + 4ull * cnt[0]);
+    return p;
+  };
+  uint32_t lo = 0, hi = M;
+  Probe p = probe(lo);
+  if (static_cast<double>(p.payload) > budget) {
+    while (lo + 1 < hi) {
+      const uint32_t mid = lo + (hi - lo) / 2;  // == (lo + hi) / 2 without overflow
+      if (static_cast<double>(probe(mid).payload) <= budget) hi = mid;
+      else lo = mid;
+    }
+    lo = hi;
+    p = probe(lo);
+  }
+  const double base = p.base;
+  timed(ctx, K_ALLOC_ASSIGN, 13.0 * T, st, [&] { launch_general_assign(dF, T, base, base * c1, w, dW, dP, st); });
+  DQ_CUDA(cudaGetLastError());
+  DQ_CUDA(cudaMemcpyAsync(ctx->h_counts, w.counts, 3 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  DQ_CUDA(cudaStreamSynchronize(st));
+  harvest(ctx);
+  r.u = base;
+  r.n8 = ctx->h_counts[0];
+  r.n4 = ctx->h_counts[1];
+  r.n2 = ctx->h_counts[2];
+  r.payload = static_cast<uint64_t>(S) * (8ull * r.n8 + 4ull * r.n4 + 2ull * r.n2);
+  if (static_cast<double>(r.payload) > budget) throw Error(DQ_EINFEASIBLE, "bit allocation infeasible within budget");
+  return r;
+}
+
+AllocResult allocate_fast(dq_ctx* ctx, const dq_config& c, const float* dF, uint32_t T, uint8_t* dW,
+                          uint32_t* dP, cudaStream_t st);
+
+// allocate_fast / allocate_general / fixed width (engine.cpp:308-326) + build_permutation
 AllocResult allocate(dq_ctx* ctx, const dq_config& c, const float* dF, uint32_t T, uint8_t* dW,
                      uint32_t* dP, cudaStream_t st) {
+  if (c.variable_width && c.allocator == DQ_ALLOC_GENERAL) return allocate_general(ctx, c, dF, T, dW, dP, st);
+  return allocate_fast(ctx, c, dF, T, dW, dP, st);
+}
+
+// allocate_fast (allocation.cpp:228-260) + build_permutation; see dq_stats_alloc.cu
+AllocResult allocate_fast(dq_ctx* ctx, const dq_config& c, const float* dF, uint32_t T, uint8_t* dW,
+                          uint32_t* dP, cudaStream_t st) {
   AllocResult r;
   const uint32_t S = c.super_group_size;
   AllocWork w = work_of(ctx, T);
@@ -1602,6 +1691,79 @@ int dq_allocate_fast(dq_ctx* ctx, const float* d_F, size_t nsg, double b, uint8_
       counts[1] = r.n4;
       counts[2] = r.n2;
     }
+  });
+}
+
+int dq_allocate_general(dq_ctx* ctx, const float* d_F, size_t nsg, double b, uint8_t* d_widths,
+                        uint32_t* d_perm, double* u, uint64_t* payload, uint32_t counts[3], void* stream) {
+  return guarded([&] {
+    if (!ctx) invalid("null context");
+    DQ_CUDA(cudaSetDevice(ctx->device));
+    dq_config c = ctx->cfg;
+    c.budget_bits = b;
+    c.variable_width = 1;
+    c.allocator = DQ_ALLOC_GENERAL;
+    AllocResult r = allocate_general(ctx, c, d_F, static_cast<uint32_t>(nsg), d_widths, d_perm, S(stream));
+    if (u) *u = r.u;
+    if (payload) *payload = r.payload;
+    if (counts) {
+      counts[0] = r.n8;
+      counts[1] = r.n4;
+      counts[2] = r.n2;
+    }
+  });
+}
+
+int dq_allocate_fast_stateful(dq_ctx* ctx, const float* d_F, size_t nsg, double b, double state[3],
+                              uint8_t* d_widths, uint32_t* d_perm, double* u, uint64_t* payload, uint32_t counts[3],
+                              void* stream) {
+  // allocation.cpp:262-300: widths at the carried u; when over budget, the largest
+  // in-budget plateau sample at or below it - payload(u) is non-decreasing, so that is
+  // allocate_fast's sample (every sample above the carried u is over budget too)
+  return guarded([&] {
+    if (!ctx || !state) invalid("null argument");
+    DQ_CUDA(cudaSetDevice(ctx->device));
+    const cudaStream_t st = S(stream);
+    dq_config c = ctx->cfg;
+    c.budget_bits = b;
+    c.variable_width = 1;
+    c.allocator = DQ_ALLOC_FAST;
+    const uint32_t T = static_cast<uint32_t>(nsg);
+    const uint32_t Sg = c.super_group_size;
+    const double budget = static_cast<double>(T) * Sg * payload_budget(c);
+    AllocWork w = work_of(ctx, T);
+    const float t24 = static_cast<float>(std::exp2((4.0 - state[2]) / kAlpha));
+    const float t48 = static_cast<float>(std::exp2((8.0 - state[2]) / kAlpha));
+    ctx->tcount.reserve(2);
+    launch_threshold_counts(d_F, T, t24, t48, ctx->tcount.p, st);
+    unsigned long long cnt[2];
+    DQ_CUDA(cudaMemcpyAsync(cnt, ctx->tcount.p, sizeof cnt, cudaMemcpyDeviceToHost, st));
+    DQ_CUDA(cudaStreamSynchronize(st));
+    const uint64_t pay_u = static_cast<uint64_t>(Sg) * (2ull * T + 2ull * cnt[1] + 4ull * cnt[0]);
+    const bool over = static_cast<double>(pay_u) > budget;
+    AllocResult r;
+    if (over) {
+      r = allocate_fast(ctx, c, d_F, T, d_widths, d_perm, st);
+    } else {
+      launch_alloc_assign(d_F, T, t24, t48, false, w, d_widths, d_perm, st);
+      DQ_CUDA(cudaGetLastError());
+      DQ_CUDA(cudaMemcpyAsync(ctx->h_counts, w.counts, 3 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+      DQ_CUDA(cudaStreamSynchronize(st));
+      r.n8 = ctx->h_counts[0];
+      r.n4 = ctx->h_counts[1];
+      r.n2 = ctx->h_counts[2];
+      r.payload = pay_u;
+    }
+    if (u) *u = state[2];
+    if (payload) *payload = r.payload;
+    if (counts) {
+      counts[0] = r.n8;
+      counts[1] = r.n4;
+      counts[2] = r.n2;
+    }
+    if (over) state[1] = state[2];
+    else state[0] = state[2];
+    state[2] = 0.5 * (state[0] + state[1]);
   });
 }
 

@@ -142,6 +142,17 @@ void launch_threshold_counts(const float* F, uint32_t T, float t24, float t48, u
 // otherwise the given host values are used.
 void launch_alloc_assign(const float* F, uint32_t T, float t24, float t48, bool from_state, AllocWork w,
                          uint8_t* widths, uint32_t* perm, cudaStream_t st);
+// general allocator, W = {2,4,8} (see dq_stats_alloc.cu): widths by double thresholds
+// g0 = base, g1 = base * 512/17; crossing points -> sorted unique u64 keys (back in
+// `keys`, count in *n_unique; trailing ~0 = non-positive F); payload counts at a probe.
+void launch_general_assign(const float* F, uint32_t T, double g0, double g1, AllocWork w, uint8_t* widths,
+                           uint32_t* perm, cudaStream_t st);
+size_t general_temp_bytes(uint32_t T);
+cudaError_t launch_general_points(const float* F, uint32_t T, double c1, uint64_t* keys, uint64_t* sorted,
+                                  void* temp, size_t temp_bytes, int* n_unique, unsigned long long* invalid,
+                                  cudaStream_t st);
+void launch_general_counts(const float* F, uint32_t T, const uint64_t* pts, uint32_t M, uint32_t idx, double c1,
+                           unsigned long long* counts, double* base_out, cudaStream_t st);
 void launch_fixed_assign(uint32_t T, int width, AllocWork w, uint8_t* widths, uint32_t* perm,
                          cudaStream_t st);
 

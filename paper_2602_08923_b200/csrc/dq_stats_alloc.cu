@@ -22,6 +22,7 @@
 #include <cstdint>
 
 #include <cooperative_groups.h>
+#include <cub/cub.cuh>
 
 #include "dq_internal.h"
 
@@ -566,10 +567,22 @@ __device__ __forceinline__ uint64_t block_excl_scan_u64(uint64_t v, uint64_t* to
   return off + incl - v;
 }
 
-template <bool FIXED>
+// MODE 0: fast allocator (float thresholds, from params or the search state);
+// 1: fixed width; 2: general allocator (level by double compares, allocation.cpp:100-105)
+template <int MODE>
+__device__ __forceinline__ int class_of(const float* F, uint32_t j, float t24, float t48, int fixed_cls, double g0,
+                                        double g1) {
+  if constexpr (MODE == 1) return fixed_cls;
+  else if constexpr (MODE == 2) {
+    const double f = static_cast<double>(F[j]);
+    return f >= g1 ? 0 : (f >= g0 ? 1 : 2);
+  } else return cls_of(F[j], t24, t48);
+}
+
+template <int MODE>
 __global__ void __launch_bounds__(256) k_assign_count(const float* __restrict__ F, uint32_t T, float t24,
                                                       float t48, const AllocState* st_thr, int fixed_cls,
-                                                      uint8_t* widths, uint32_t* blockcnt) {
+                                                      double g0, double g1, uint8_t* widths, uint32_t* blockcnt) {
   if (st_thr) {
     t24 = st_thr->t24;
     t48 = st_thr->t48;
@@ -579,7 +592,7 @@ __global__ void __launch_bounds__(256) k_assign_count(const float* __restrict__ 
   for (int k = 0; k < 8; ++k) {
     const uint32_t j = j0 + k;
     if (j >= T) break;
-    const int c = FIXED ? fixed_cls : cls_of(F[j], t24, t48);
+    const int c = class_of<MODE>(F, j, t24, t48, fixed_cls, g0, g1);
     widths[j] = static_cast<uint8_t>(c == 0 ? 8 : (c == 1 ? 4 : 2));
     packed += 1ull << (16 * c);
   }
@@ -630,9 +643,10 @@ __global__ void __launch_bounds__(1024) k_assign_scan(uint32_t nb, uint32_t* blo
   }
 }
 
-template <bool FIXED>
+template <int MODE>
 __global__ void __launch_bounds__(256) k_assign_scatter(const float* __restrict__ F, uint32_t T, float t24,
                                                         float t48, const AllocState* st_thr, int fixed_cls,
+                                                        double g0, double g1,
                                                         const uint32_t* blockcnt, const uint32_t* counts,
                                                         uint32_t* perm, const float* gmean, float* pmean) {
   if (st_thr) {
@@ -644,7 +658,7 @@ __global__ void __launch_bounds__(256) k_assign_scatter(const float* __restrict_
   uint64_t packed = 0;
   for (int k = 0; k < 8; ++k) {
     const uint32_t j = j0 + k;
-    cls[k] = j < T ? (FIXED ? fixed_cls : cls_of(F[j], t24, t48)) : 3;
+    cls[k] = j < T ? class_of<MODE>(F, j, t24, t48, fixed_cls, g0, g1) : 3;
     if (cls[k] < 3) packed += 1ull << (16 * cls[k]);
   }
   uint64_t tot;
@@ -661,27 +675,116 @@ __global__ void __launch_bounds__(256) k_assign_scatter(const float* __restrict_
     }
 }
 
-static void assign_impl(const float* F, uint32_t T, float t24, float t48, const AllocState* thr, int fixed_cls,
-                        bool fixed, AllocWork w, uint8_t* widths, uint32_t* perm, cudaStream_t st) {
+static void assign_impl(int mode, const float* F, uint32_t T, float t24, float t48, const AllocState* thr,
+                        int fixed_cls, double g0, double g1, AllocWork w, uint8_t* widths, uint32_t* perm,
+                        cudaStream_t st) {
   const uint32_t nb = alloc_blocks(T);
   if (nb == 0) return;
-  if (fixed) k_assign_count<true><<<nb, 256, 0, st>>>(F, T, t24, t48, thr, fixed_cls, widths, w.blockcnt);
-  else k_assign_count<false><<<nb, 256, 0, st>>>(F, T, t24, t48, thr, fixed_cls, widths, w.blockcnt);
-  k_assign_scan<<<1, 1024, 0, st>>>(nb, w.blockcnt, w.counts);
-  if (fixed)
-    k_assign_scatter<true><<<nb, 256, 0, st>>>(F, T, t24, t48, thr, fixed_cls, w.blockcnt, w.counts, perm, w.gmean, w.pmean);
-  else
-    k_assign_scatter<false><<<nb, 256, 0, st>>>(F, T, t24, t48, thr, fixed_cls, w.blockcnt, w.counts, perm, w.gmean, w.pmean);
+#define DQ_ASSIGN(M)                                                                                     \
+  do {                                                                                                   \
+    k_assign_count<M><<<nb, 256, 0, st>>>(F, T, t24, t48, thr, fixed_cls, g0, g1, widths, w.blockcnt);    \
+    k_assign_scan<<<1, 1024, 0, st>>>(nb, w.blockcnt, w.counts);                                         \
+    k_assign_scatter<M><<<nb, 256, 0, st>>>(F, T, t24, t48, thr, fixed_cls, g0, g1, w.blockcnt, w.counts, \
+                                            perm, w.gmean, w.pmean);                                     \
+  } while (0)
+  if (mode == 1) DQ_ASSIGN(1);
+  else if (mode == 2) DQ_ASSIGN(2);
+  else DQ_ASSIGN(0);
+#undef DQ_ASSIGN
 }
 
 void launch_alloc_assign(const float* F, uint32_t T, float t24, float t48, bool from_state, AllocWork w,
                          uint8_t* widths, uint32_t* perm, cudaStream_t st) {
-  assign_impl(F, T, t24, t48, from_state ? w.state : nullptr, 0, false, w, widths, perm, st);
+  assign_impl(0, F, T, t24, t48, from_state ? w.state : nullptr, 0, 0.0, 0.0, w, widths, perm, st);
 }
 
 void launch_fixed_assign(uint32_t T, int width, AllocWork w, uint8_t* widths, uint32_t* perm,
                          cudaStream_t st) {
-  assign_impl(nullptr, T, 0.f, 0.f, nullptr, width == 8 ? 0 : (width == 4 ? 1 : 2), true, w, widths, perm, st);
+  assign_impl(1, nullptr, T, 0.f, 0.f, nullptr, width == 8 ? 0 : (width == 4 ? 1 : 2), 0.0, 0.0, w, widths, perm,
+              st);
+}
+
+void launch_general_assign(const float* F, uint32_t T, double g0, double g1, AllocWork w, uint8_t* widths,
+                           uint32_t* perm, cudaStream_t st) {
+  assign_impl(2, F, T, 0.f, 0.f, nullptr, 0, g0, g1, w, widths, perm, st);
+}
+
+// ----------------------------------------------------- general allocator
+// allocate_general for W = {2,4,8} (allocation.cpp:121-168; the round path's W,
+// engine.cpp:306-307): crossing points F_j / chain[k] (chain = {1, 512/17}) of
+// every F_j > 0 as order-preserving u64 keys (positive doubles), sorted and
+// de-duplicated with CUB; the host then bisects over the sorted points exactly
+// like the reference, evaluating each probe with k_general_counts.  Non-positive
+// F_j emit ~0 keys (dropped after the sort); negative or NaN F_j are counted as
+// invalid (allocation.cpp:127-128).
+__global__ void k_general_points(const float* __restrict__ F, uint32_t T, double c1, uint64_t* keys,
+                                 unsigned long long* invalid) {
+  unsigned long long bad = 0;
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < T; j += gridDim.x * blockDim.x) {
+    const float f = F[j];
+    bad += !(f >= 0.0f);
+    uint64_t k0 = ~0ull, k1 = ~0ull;
+    if (f > 0.0f) {
+      k0 = static_cast<uint64_t>(__double_as_longlong(__ddiv_rn(static_cast<double>(f), 1.0)));
+      k1 = static_cast<uint64_t>(__double_as_longlong(__ddiv_rn(static_cast<double>(f), c1)));
+    }
+    keys[2ull * j] = k0;
+    keys[2ull * j + 1] = k1;
+  }
+  if (bad) atomicAdd(invalid, bad);
+}
+
+// payload terms at the probe points[idx] (the all-min plateau 2 * back + 1 at idx == M)
+__global__ void k_general_counts(const float* __restrict__ F, uint32_t T, const uint64_t* __restrict__ pts,
+                                 uint32_t M, uint32_t idx, double c1, unsigned long long* counts, double* base_out) {
+  double base;
+  if (idx < M) base = __longlong_as_double(static_cast<long long>(pts[idx]));
+  else base = M ? __dadd_rn(__dmul_rn(__longlong_as_double(static_cast<long long>(pts[M - 1])), 2.0), 1.0) : 1.0;
+  const double g1 = __dmul_rn(base, c1);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *base_out = base;
+  unsigned long long n8 = 0, n48 = 0;
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < T; j += gridDim.x * blockDim.x) {
+    const double f = static_cast<double>(F[j]);
+    n8 += f >= g1;
+    n48 += f >= base;  // base * chain[0] == base
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    n8 += __shfl_xor_sync(0xffffffffu, n8, o);
+    n48 += __shfl_xor_sync(0xffffffffu, n48, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(counts, n8);
+    atomicAdd(counts + 1, n48);
+  }
+}
+
+size_t general_temp_bytes(uint32_t T) {
+  size_t a = 0, b = 0;
+  const int n = static_cast<int>(2 * T);
+  cub::DeviceRadixSort::SortKeys(nullptr, a, static_cast<const uint64_t*>(nullptr), static_cast<uint64_t*>(nullptr), n);
+  cub::DeviceSelect::Unique(nullptr, b, static_cast<const uint64_t*>(nullptr), static_cast<uint64_t*>(nullptr),
+                            static_cast<int*>(nullptr), n);
+  return a > b ? a : b;
+}
+
+cudaError_t launch_general_points(const float* F, uint32_t T, double c1, uint64_t* keys, uint64_t* sorted,
+                                  void* temp, size_t temp_bytes, int* n_unique, unsigned long long* invalid,
+                                  cudaStream_t st) {
+  cudaMemsetAsync(invalid, 0, sizeof(*invalid), st);
+  if (T == 0) return cudaMemsetAsync(n_unique, 0, sizeof(int), st);
+  k_general_points<<<(T + 255) / 256 < 148u * 8 ? (T + 255) / 256 : 148u * 8, 256, 0, st>>>(F, T, c1, keys, invalid);
+  const int n = static_cast<int>(2 * T);
+  size_t tb = temp_bytes;
+  cudaError_t e = cub::DeviceRadixSort::SortKeys(temp, tb, keys, sorted, n, 0, 64, st);
+  if (e != cudaSuccess) return e;
+  tb = temp_bytes;
+  return cub::DeviceSelect::Unique(temp, tb, sorted, keys, n_unique, n, st);  // unique points back into keys
+}
+
+void launch_general_counts(const float* F, uint32_t T, const uint64_t* pts, uint32_t M, uint32_t idx, double c1,
+                           unsigned long long* counts, double* base_out, cudaStream_t st) {
+  cudaMemsetAsync(counts, 0, 2 * sizeof(unsigned long long), st);
+  k_general_counts<<<296, 512, 0, st>>>(F, T, pts, M, idx, c1, counts, base_out);
 }
 
 // ------------------------------------------------------------------ vNMSE

@@ -94,3 +94,58 @@ def test_allocate_fast_float_threshold_near_tie(dq, port, seed):
     assert got.payload_bits == pay
     assert np.array_equal(got.widths.cpu().numpy(), w)
     assert np.array_equal(got.permutation.cpu().numpy().astype(np.uint32), p)
+
+
+@pytest.mark.parametrize("b", [2.6, 3, 4, 6, 12])
+@pytest.mark.parametrize("name,F", list(_F_cases()), ids=[c[0] for c in _F_cases()])
+def test_allocate_general_matches(dq, port, name, F, b):
+    """allocate_general (allocation.cpp:121-168), W = {2,4,8}: widths, permutation,
+    resolved base threshold and payload identical to the oracle."""
+    from oracle.oracle import OracleError
+    try:
+        w, p, u, pay = port.allocate_general(F, b)
+    except OracleError as e:
+        assert e.code == 3
+        with pytest.raises(dq.InfeasibleBudget):
+            dq.allocate_general(torch.from_numpy(F).cuda(), b)
+        return
+    got = dq.allocate_general(torch.from_numpy(F).cuda(), b)
+    assert np.array_equal(got.widths.cpu().numpy(), w)
+    assert np.array_equal(got.permutation.cpu().numpy().astype(np.uint32), p)
+    assert got.u == u
+    assert got.payload_bits == pay
+
+
+def test_allocate_general_large_and_collisions(dq, port):
+    rng = np.random.default_rng(9)
+    f = (np.exp(5 * rng.standard_normal(1 << 18)) * 64).astype(np.float32)
+    F = np.concatenate([f, (f.astype(np.float64) * (512 / 17)).astype(np.float32), f[:1000]])
+    for b in (3.3, 4, 5.5):
+        w, p, u, pay = port.allocate_general(F, b)
+        got = dq.allocate_general(torch.from_numpy(F).cuda(), b)
+        assert got.u == u and got.payload_bits == pay
+        assert np.array_equal(got.widths.cpu().numpy(), w)
+        assert np.array_equal(got.permutation.cpu().numpy().astype(np.uint32), p)
+
+
+def test_allocate_general_rejects_negative(dq):
+    for bad in (np.array([1.0, -1.0], np.float32), np.array([np.nan, 1.0], np.float32)):
+        with pytest.raises(dq.InvalidArgument):
+            dq.allocate_general(torch.from_numpy(bad).cuda(), 5.0)
+
+
+def test_allocate_fast_stateful_sequence(dq, port):
+    """allocate_fast_stateful (allocation.cpp:262-300) over 12 rounds with the state carried:
+    widths, permutation, reported u, payload and the next state identical to the oracle."""
+    rng = np.random.default_rng(5)
+    for b in (3, 4, 6):
+        st = dq.FastAllocatorState()
+        ost = [-1e6, 1e6, 0.0]
+        for rnd in range(12):
+            F = np.exp((4 + rnd % 3) * rng.standard_normal(1500)).astype(np.float32)
+            w, p, u, pay, ost = port.allocate_fast_stateful(F, b, ost)
+            got = dq.allocate_fast_stateful(torch.from_numpy(F).cuda(), b, st)
+            assert np.array_equal(got.widths.cpu().numpy(), w)
+            assert np.array_equal(got.permutation.cpu().numpy().astype(np.uint32), p)
+            assert got.u == u and got.payload_bits == pay
+            assert [st.lo, st.hi, st.u] == ost

@@ -90,6 +90,15 @@ def test_round_ablation_toggles(dq, port):
         _check_round(dq, port, ws, _cfg(dq, 4, 6, "ring", **kw), port.round_cfg(4, 6, "ring", **okw))
 
 
+@pytest.mark.parametrize("topo,n,b", [("ring", 4, 4), ("butterfly", 8, 3), ("ring", 5, 6)])
+def test_round_general_allocator(dq, port, topo, n, b):
+    """AllocatorKind::kGeneral in run_round (engine.cpp:322-323), W = {2,4,8}."""
+    d = (1 << 15) + 3
+    ws = _workers(port, n, d, seed=40 + n)
+    _check_round(dq, port, ws, _cfg(dq, n, b, topo, seed=2, allocator=dq.KIND_GENERAL),
+                 port.round_cfg(n, b, topo, seed=2, allocator="general"))
+
+
 def test_round_known_answer_c1(dq, port):
     """SURVEY Appendix A round pins at d = 2^20 (n=4 ring b=4, b=5; n=8 ring/butterfly b=4)."""
     d = 1 << 20
