@@ -9,7 +9,7 @@ from ._lib import (CudaError, DqError, InfeasibleBudget, InvalidArgument, Malfor
                    NcclError, build, lib)
 from .api import (BUTTERFLY, KIND_FAST, KIND_FIXED, KIND_GENERAL, RING, BitAllocation, CodecConfig,  # noqa: F401
                   Communicator, Context, DeviceChunk, FastAllocatorState, PipelineConfig, QuantContext,
-                  RoundResult, SharedSeed, allocate_fast, allocate_fast_stateful, allocate_general, chunk_bytes, compress_chunk, compressed_size_bits, compute_stats,
+                  RoundResult, SharedSeed, ablation_ladder, allocate_fast, allocate_fast_stateful, allocate_general, chunk_bytes, compress_chunk, compressed_size_bits, compute_stats,
                   decompress_accumulate, decompress_accumulate_recompress, decompress_chunk, parse_chunk,
                   reduce_stats, run_round, run_round_host, serialize_chunk, soa_from_reference)
 

@@ -401,6 +401,21 @@ def allocate_fast_stateful(sq_norms: torch.Tensor, budget_bits: float, state: Fa
     return BitAllocation(widths[:T], perm[:T], pay.value, u.value, tuple(counts))
 
 
+def ablation_ladder(base: PipelineConfig) -> list:
+    """proj/src/engine.cpp:420-450: the Table-6 ladder of configs, each rung adding one
+    ingredient: uniform -> non_uniform -> variable_width -> hierarchical -> correlated."""
+    from dataclasses import replace
+    uniform = replace(base, non_uniform=False, variable_width=False, allocator=KIND_FIXED, fixed_width=4,
+                      hierarchical_scales=False, correlated=False, group_size=32)
+    non_uniform = replace(uniform, non_uniform=True)
+    variable = replace(non_uniform, variable_width=True,
+                       allocator=KIND_FAST if base.allocator == KIND_FIXED else base.allocator)
+    hierarchical = replace(variable, hierarchical_scales=True, group_size=16)
+    correlated = replace(hierarchical, correlated=True)
+    return [("uniform", uniform), ("non_uniform", non_uniform), ("variable_width", variable),
+            ("hierarchical", hierarchical), ("correlated", correlated)]
+
+
 @dataclass
 class RoundResult:
     """proj/include/dynamiq/engine.hpp:45-54 (exact fp64 sum not materialized)."""

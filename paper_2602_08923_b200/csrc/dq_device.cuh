@@ -17,7 +17,7 @@ constexpr int kS = 256;            // super-group size S (entries)
 constexpr int kG = 16;             // group size s (entries)
 constexpr int kGroups = kS / kG;   // groups per super-group
 constexpr int kTileSG = 64;        // super-groups per layout tile
-constexpr int kMetaBytes = 18;     // per-SG scale bytes: 16 u8 codes + bf16 sg_scale
+constexpr int kMetaBytes = 18;     // per-SG scale bytes of the default format: 16 u8 codes + bf16 sg_scale
 constexpr uint64_t kGolden = 0x9e3779b97f4a7c15ULL;
 constexpr uint64_t kSeedSalt = 0x6a09e667f3bcc909ULL;
 
@@ -78,12 +78,19 @@ __device__ __forceinline__ uint16_t bf16_round_up(float v) {
 // ---------------------------------------------------------------- layout
 // A chunk of nsg super-groups in body order: n8 width-8, then n4 width-4, then
 // n2 width-2 super-groups (the reference's wire run order 8,4,2).  Super-groups
-// are packed in tiles of 64: [payloads][16 u8 codes x cnt][bf16 sg_scale x cnt].
+// are packed in tiles of 64: [payloads][group scales x cnt][bf16 sg_scale x cnt].
 // Every tile starts 64-byte aligned (payloads are 64/128/256 B, metadata is
-// 18 x 64 = 1152 B for full tiles) and a run of whole tiles is one contiguous
+// (gs + ss) x 64 B for full tiles) and a run of whole tiles is one contiguous
 // byte range, which is what the transport pipelines on.
+// Scale format (codec.cpp:92-116, the record fields of serialize_chunk):
+//   hierarchical (default, s = 16): gs = 256/s u8 codes, ss = 2 (bf16 sg_scale);
+//   flat bf16 (ablation): gs = 2 * 256/s bytes (one bf16 per group), ss = 0.
+// gshift = log2(s / 8): lanes per group when a warp holds a super-group 8 entries per lane.
 struct Layout {
   uint32_t nsg, n8, n4;
+  uint32_t gs = 16, ss = 2, gshift = 1;
+  __host__ __device__ bool hierarchical() const { return ss != 0; }
+  __host__ __device__ bool default_format() const { return gs == 16 && ss == 2 && gshift == 1; }
   __host__ __device__ uint32_t n2() const { return nsg - n8 - n4; }
   __host__ __device__ uint32_t width(uint32_t i) const { return i < n8 ? 8 : (i < n8 + n4 ? 4 : 2); }
   // payload bytes of super-groups [0, k)
@@ -96,7 +103,7 @@ struct Layout {
   }
   __host__ __device__ uint64_t tile_offset(uint32_t t) const {
     const uint32_t k = t * kTileSG < nsg ? t * kTileSG : nsg;
-    return pay_prefix(k) + static_cast<uint64_t>(kMetaBytes) * k;
+    return pay_prefix(k) + static_cast<uint64_t>(gs + ss) * k;
   }
   __host__ __device__ uint32_t tiles() const { return (nsg + kTileSG - 1) / kTileSG; }
   __host__ __device__ uint64_t bytes() const { return tile_offset(tiles()); }
@@ -112,8 +119,8 @@ struct Layout {
     const uint64_t tp = pay_prefix(last) - pay_prefix(first);
     SG s;
     s.payload = base + (pay_prefix(i) - pay_prefix(first));
-    s.codes = base + tp + 16ull * (i - first);
-    s.scale = base + tp + 16ull * cnt + 2ull * (i - first);
+    s.codes = base + tp + static_cast<uint64_t>(gs) * (i - first);
+    s.scale = base + tp + static_cast<uint64_t>(gs) * cnt + static_cast<uint64_t>(ss) * (i - first);
     s.width = width(i);
     return s;
   }

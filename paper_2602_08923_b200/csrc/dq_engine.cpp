@@ -342,16 +342,17 @@ void validate(const dq_config& c) {  // engine.cpp:243-255 + device coverage
   if (c.topology == DQ_BUTTERFLY && (c.n_workers & (c.n_workers - 1)) != 0)
     invalid("butterfly topology requires a power-of-two worker count");
   if (c.topology != DQ_RING && c.topology != DQ_BUTTERFLY) invalid("unknown topology");
-  if (c.group_size != 16 || c.super_group_size != 256)
-    invalid("device codec supports group_size 16 and super_group_size 256");
-  if (!c.hierarchical_scales) invalid("device codec supports hierarchical scales only");
+  if (c.super_group_size != 256) invalid("device codec supports super_group_size 256");
+  if (c.group_size != 8 && c.group_size != 16 && c.group_size != 32 && c.group_size != 64 && c.group_size != 128)
+    invalid("device codec supports group_size 8, 16, 32, 64 or 128");
   if (c.codec != 0) invalid("device codec supports the quantized codec only");
   if (c.variable_width && c.allocator != DQ_ALLOC_FAST && c.allocator != DQ_ALLOC_GENERAL)
     invalid("unknown allocator");
 }
 
 double payload_budget(const dq_config& c) {  // allocation.cpp:45-58
-  const double bbar = c.budget_bits - (8.0 / c.group_size + 16.0 / c.super_group_size);
+  const double over = c.hierarchical_scales ? 8.0 / c.group_size + 16.0 / c.super_group_size : 16.0 / c.group_size;
+  const double bbar = c.budget_bits - over;
   if (!(bbar > 2.0)) {
     char m[160];
     std::snprintf(m, sizeof m, "payload budget %f does not exceed the minimum width 2", bbar);
@@ -375,6 +376,7 @@ AllocWork work_of(dq_ctx* ctx, uint32_t T) {
 }
 
 struct AllocResult {
+  uint32_t gs = 16, ss = 2, gshift = 1;  // scale format of the round's chunks (Layout)
   double u = 0.0;
   uint64_t payload = 0;
   uint32_t n8 = 0, n4 = 0, n2 = 0, passes = 0;
@@ -651,6 +653,17 @@ AllocResult allocate_fast(dq_ctx* ctx, const dq_config& c, const float* dF, uint
   return r;
 }
 
+// scale format of the codec config (codec.cpp:88-116): s = 8 << gshift entries per
+// group; hierarchical: 256/s u8 codes + bf16 sg_scale, flat: 256/s bf16 per super-group
+template <class T>
+void set_format(T& f, const dq_config& c) {
+  uint32_t sh = 0;
+  while ((8u << sh) < c.group_size) ++sh;
+  f.gshift = sh;
+  f.gs = c.hierarchical_scales ? 256 / c.group_size : 2 * 256 / c.group_size;
+  f.ss = c.hierarchical_scales ? 2 : 0;
+}
+
 Layout chunk_layout(const AllocResult& a, uint32_t lo, uint32_t hi) {
   auto overlap = [](uint32_t a0, uint32_t a1, uint32_t b0, uint32_t b1) {
     const uint32_t l = a0 > b0 ? a0 : b0, h = a1 < b1 ? a1 : b1;
@@ -660,6 +673,9 @@ Layout chunk_layout(const AllocResult& a, uint32_t lo, uint32_t hi) {
   L.nsg = hi - lo;
   L.n8 = overlap(lo, hi, 0, a.n8);
   L.n4 = overlap(lo, hi, a.n8, a.n8 + a.n4);
+  L.gs = a.gs;
+  L.ss = a.ss;
+  L.gshift = a.gshift;
   return L;
 }
 
@@ -692,10 +708,10 @@ void to_reference(const uint8_t* soa, uint32_t chunk, const Layout& L, uint8_t* 
   size_t at = 24;
   for (uint32_t i = 0; i < L.nsg; ++i) {
     const Layout::SG g = L.locate(i);
-    std::memcpy(out + at, soa + g.scale, 2);
-    std::memcpy(out + at + 2, soa + g.codes, 16);
-    std::memcpy(out + at + 18, soa + g.payload, 32 * g.width);
-    at += 18 + 32 * g.width;
+    std::memcpy(out + at, soa + g.scale, L.ss);
+    std::memcpy(out + at + L.ss, soa + g.codes, L.gs);
+    std::memcpy(out + at + L.ss + L.gs, soa + g.payload, 32 * g.width);
+    at += L.ss + L.gs + 32 * g.width;
   }
 }
 
@@ -703,7 +719,7 @@ void to_reference(const uint8_t* soa, uint32_t chunk, const Layout& L, uint8_t* 
 void account(dq_round_info* info, const Layout& L, bool fresh) {
   const uint64_t coords = static_cast<uint64_t>(L.nsg) * 256;
   const uint64_t pay = 256ull * (8ull * L.n8 + 4ull * L.n4 + 2ull * L.n2());
-  const uint64_t scl = static_cast<uint64_t>(L.nsg) * (16 + 16 * 8);
+  const uint64_t scl = static_cast<uint64_t>(L.nsg) * 8 * (L.gs + L.ss);  // supergroup_scale_bits (codec.cpp:274-279)
   info->transmitted_coordinates += coords;
   info->header_bits += 192;
   info->wire_payload_bits += pay;
@@ -727,6 +743,7 @@ Prepared prepare(dq_ctx* ctx, uint32_t T, cudaStream_t st) {
   p.T = T;
   const dq_config& c = ctx->cfg;
   p.a = allocate(ctx, c, ctx->gsq.p, T, ctx->widths.p, ctx->perm.p, st);
+  set_format(p.a, c);
   const uint32_t n = c.n_workers;
   p.lo.resize(n + 1);
   for (uint32_t i = 0; i <= n; ++i) p.lo[i] = static_cast<uint32_t>(static_cast<uint64_t>(T) * i / n);
@@ -895,6 +912,7 @@ void sim_round(dq_ctx* ctx, const float* const* xs, size_t d, float* out, int fl
   if (collect_wire) info->wire_hash = H;
   {
     GatherArgs g{};
+    set_format(g, ctx->cfg);
     uint32_t max_nsg_g = 0;
     for (uint32_t ch = 0; ch < n; ++ch) {
       const Layout L = chunk_layout(p.a, p.lo[ch], p.lo[ch + 1]);
@@ -1147,6 +1165,7 @@ void ring_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>& bas
     timed(ctx, dar ? K_DAR : K_LEAF, quant_bytes(lays[ch], dar), st, [&] { launch_quant_peer(a, dar, st); });
   }
   GatherArgs g{};
+  set_format(g, ctx->cfg);
   uint32_t max_nsg = 0;
   double gbytes = 0;
   for (uint32_t c = 0; c < n; ++c) {
@@ -1234,8 +1253,9 @@ void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info
     b.n_slots = plans[ch].n_slots;
     bases[ch] = b;
   }
+  // peer transport: default scale format (the ablation formats run their generic kernels over NCCL)
   if (c.topology == DQ_RING && ctx->transport == DQ_TRANSPORT_PEER && n <= static_cast<uint32_t>(kMaxPeers) &&
-      peer_setup(ctx, mb, max_nsg, st)) {
+      lays[0].default_format() && peer_setup(ctx, mb, max_nsg, st)) {
     ring_peer(ctx, p, bases, lays, out, d, st);
     for (uint32_t ch = 0; ch < n; ++ch) {
       for (uint32_t g = 0; g < plans[ch].n_gat; ++g) account(info, lays[ch], g == 0);
@@ -1343,6 +1363,7 @@ void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info
   cudaEvent_t* gev = ctx->pipe_ev.data() + 2ull * n * ctx->pieces + 4;
   auto decode_one = [&](uint32_t ch, const uint8_t* src) {
     GatherArgs g{};
+    set_format(g, ctx->cfg);
     g.in[0] = src;
     g.lo[0] = p.lo[ch];
     g.lo[1] = p.lo[ch + 1];
@@ -1372,6 +1393,7 @@ void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info
   DQ_CUDA(cudaStreamWaitEvent(st, gev[1], 0));
   {
     GatherArgs g{};
+    set_format(g, ctx->cfg);
     uint32_t k = 0, max_nsg_g = 0;
     double gbytes = 0;
     for (uint32_t ch = 0; ch < n; ++ch) {
@@ -1576,11 +1598,11 @@ int dq_parse_chunk(const void* d_wire, size_t len, void* d_soa, size_t soa_cap, 
     // super-groups whose record fits in len (codec.cpp:380-383 checks each before reading it)
     const uint64_t body = len - 24;
     uint32_t fit = count;
-    if (L.pay_prefix(count) + static_cast<uint64_t>(kMetaBytes) * count > body) {
+    if (L.pay_prefix(count) + static_cast<uint64_t>(L.gs + L.ss) * count > body) {
       uint32_t lo = 0, hi = count;  // largest k with record_end(k) <= body
       while (lo < hi) {
         const uint32_t mid = lo + (hi - lo + 1) / 2;
-        if (L.pay_prefix(mid) + static_cast<uint64_t>(kMetaBytes) * mid <= body) lo = mid;
+        if (L.pay_prefix(mid) + static_cast<uint64_t>(L.gs + L.ss) * mid <= body) lo = mid;
         else hi = mid - 1;
       }
       fit = lo;

@@ -52,6 +52,7 @@ struct GatherArgs {
   uint64_t d;
   float n_workers_f;
   int uniform_books;
+  uint32_t gs = 16, ss = 2, gshift = 1;  // scale format of every chunk (see Layout)
   // peer transport: chunk c's unit k may be decoded once flags[c][k] == epoch (null: ready)
   const uint32_t* flags[64];
   uint32_t unit[64];

@@ -25,12 +25,14 @@ constexpr int kWireWarps = kWireThreads / 32;
 
 // byte offset of super-group i's record after the 24-byte header
 __device__ __forceinline__ uint64_t record_offset(const Layout& L, uint32_t i) {
-  return L.pay_prefix(i) + static_cast<uint64_t>(kMetaBytes) * i;
+  return L.pay_prefix(i) + static_cast<uint64_t>(L.gs + L.ss) * i;
 }
 
-// SoA offset of halfword k of super-group i's record (k = 0 scale, 1..8 codes, 9.. payload)
-__device__ __forceinline__ uint64_t soa_half(const Layout::SG& g, uint32_t k) {
-  return k == 0 ? g.scale : (k < 9 ? g.codes + 2 * (k - 1) : g.payload + 2 * (k - 9));
+// SoA offset of halfword k of super-group i's record: [sg_scale (ss bytes)]
+// [group scales (gs bytes)][payload] (codec.cpp:331-337)
+__device__ __forceinline__ uint64_t soa_half(const Layout& L, const Layout::SG& g, uint32_t k) {
+  const uint32_t h0 = L.ss / 2, h1 = (L.ss + L.gs) / 2;
+  return k < h0 ? g.scale + 2 * k : (k < h1 ? g.codes + 2 * (k - h0) : g.payload + 2 * (k - h1));
 }
 
 __global__ void __launch_bounds__(kWireThreads) k_to_wire(const uint8_t* __restrict__ soa, Layout L, uint32_t chunk,
@@ -44,9 +46,9 @@ __global__ void __launch_bounds__(kWireThreads) k_to_wire(const uint8_t* __restr
   for (uint32_t i = blockIdx.x * kWireWarps + (threadIdx.x >> 5); i < L.nsg; i += gridDim.x * kWireWarps) {
     const Layout::SG g = L.locate(i);
     uint16_t* rec = rec_base + record_offset(L, i) / 2;
-    const uint32_t halves = (kMetaBytes + 32 * g.width) / 2;
+    const uint32_t halves = (L.gs + L.ss + 32 * g.width) / 2;
     for (uint32_t k = lane; k < halves; k += 32)
-      rec[k] = *reinterpret_cast<const uint16_t*>(soa + soa_half(g, k));
+      rec[k] = *reinterpret_cast<const uint16_t*>(soa + soa_half(L, g, k));
   }
 }
 
@@ -61,15 +63,16 @@ __global__ void __launch_bounds__(kWireThreads) k_from_wire(const uint8_t* __res
   for (uint32_t i = blockIdx.x * kWireWarps + (threadIdx.x >> 5); i < fit; i += gridDim.x * kWireWarps) {
     const Layout::SG g = L.locate(i);
     const uint16_t* rec = rec_base + record_offset(L, i) / 2;
-    const uint32_t halves = (kMetaBytes + 32 * g.width) / 2;
+    const uint32_t h0 = L.ss / 2, h1 = (L.ss + L.gs) / 2;
+    const uint32_t halves = (L.gs + L.ss + 32 * g.width) / 2;
     uint32_t codes_or = 0, pay_or = 0;
     for (uint32_t k = lane; k < halves; k += 32) {
       const uint16_t v = rec[k];
-      if (soa) *reinterpret_cast<uint16_t*>(soa + soa_half(g, k)) = v;
-      if (k >= 1 && k < 9) codes_or |= v;
-      else if (k >= 9) pay_or |= v;
+      if (soa) *reinterpret_cast<uint16_t*>(soa + soa_half(L, g, k)) = v;
+      if (k >= h0 && k < h1) codes_or |= v;
+      else if (k >= h1) pay_or |= v;
     }
-    const bool zero_scale = rec[0] == 0;  // both scale bytes zero
+    const bool zero_scale = L.hierarchical() && rec[0] == 0;  // both sg_scale bytes zero (flat: no check)
     const bool codes_nz = __any_sync(0xffffffffu, codes_or != 0);
     const bool pay_nz = __any_sync(0xffffffffu, pay_or != 0);
     if (lane == 0 && zero_scale && (codes_nz || pay_nz))

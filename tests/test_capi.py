@@ -144,5 +144,8 @@ def test_invalid_config_rejected(L):
     h = C.c_void_p()
     assert L.dq_ctx_create(C.byref(c), 0, C.byref(h)) == 2
     L.dq_config_default(C.byref(c))
-    c.group_size = 32
+    c.group_size = 12  # not a power of two in 8..128 (the device codec's group sizes)
+    assert L.dq_ctx_create(C.byref(c), 0, C.byref(h)) == 2
+    L.dq_config_default(C.byref(c))
+    c.super_group_size = 512
     assert L.dq_ctx_create(C.byref(c), 0, C.byref(h)) == 2

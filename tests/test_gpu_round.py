@@ -99,6 +99,38 @@ def test_round_general_allocator(dq, port, topo, n, b):
                  port.round_cfg(n, b, topo, seed=2, allocator="general"))
 
 
+@pytest.mark.parametrize("topo", ["ring", "butterfly"])
+@pytest.mark.parametrize("s,hier", [(16, False), (32, False), (8, True), (32, True), (64, False), (128, True)])
+def test_round_scale_formats(dq, port, s, hier, topo):
+    """CodecConfig ablations on the device: group size s and flat bf16 group scales
+    (codec.cpp:88-116,146-149; wire records without sg_scale, engine accounting 16/s)."""
+    d = (1 << 14) + 9
+    ws = _workers(port, 4, d, seed=60 + s)
+    _check_round(dq, port, ws, _cfg(dq, 4, 5, topo, seed=3, group_size=s, hierarchical_scales=hier),
+                 port.round_cfg(4, 5, topo, seed=3, s=s, hierarchical=hier))
+
+
+def test_ablation_ladder(dq, port):
+    """proj/tests/test_engine.cpp:241-260 on the device: every rung of ablation_ladder
+    (engine.cpp:420-450) bit-identical to the oracle, mean vNMSE strictly decreasing."""
+    ladder = dq.ablation_ladder(dq.PipelineConfig(n_workers=4, seed=dq.SharedSeed(0, 0)))
+    assert [name for name, _ in ladder] == ["uniform", "non_uniform", "variable_width", "hierarchical", "correlated"]
+    means = [0.0] * 5
+    for smp in range(3):
+        ws = _workers(port, 4, 1 << 16, seed=50 + smp)
+        for v, (name, cfg) in enumerate(ladder):
+            from dataclasses import replace
+            cfg = replace(cfg, seed=dq.SharedSeed(70 + smp, 0))
+            ocfg = port.round_cfg(4, cfg.budget_bits, "ring", seed=70 + smp, s=cfg.group_size,
+                                  non_uniform=cfg.non_uniform, variable_width=cfg.variable_width,
+                                  hierarchical=cfg.hierarchical_scales, correlated=cfg.correlated,
+                                  fixed_width=cfg.fixed_width,
+                                  allocator={0: "general", 1: "fast", 2: "fixed"}[cfg.allocator])
+            got, _ = _check_round(dq, port, ws, cfg, ocfg)
+            means[v] += got.vnmse
+    assert all(means[v] < means[v - 1] for v in range(1, 5)), means
+
+
 def test_round_known_answer_c1(dq, port):
     """SURVEY Appendix A round pins at d = 2^20 (n=4 ring b=4, b=5; n=8 ring/butterfly b=4)."""
     d = 1 << 20
