@@ -159,18 +159,19 @@ uint64_t fnv1a(const uint8_t* b, size_t n, uint64_t h) {
 using namespace dq;
 
 // Peer transport region of one rank (cudaMalloc'd, exported by CUDA IPC, mapped by
-// every other rank of the node): per round parity, n-1 ring inboxes (hop h's output
-// lands in the right neighbour's inbox h) and n gather slots (the sink of chunk c
+// every other rank of the node): per round parity, `ninbox` inboxes (ring: hop h's
+// output lands in the right neighbour's inbox h; butterfly: stage s's message for
+// chunk c in the receiver's inbox s * n + c) and n gather slots (the sink of chunk c
 // stores its bytes into every rank's slot c), then one u32 flag per unit of each.
 struct PeerMem {
   uint8_t* base = nullptr;
   std::vector<uint8_t*> peer;  // rank q's region as mapped here (peer[me] == base)
   size_t cap = 0;              // bytes per chunk slot
   size_t cap_units = 0;        // flags per chunk slot
-  uint32_t n = 0, epoch = 0;
-  size_t slots() const { return 2ull * (n - 1) + 2ull * n; }
-  size_t inbox(uint32_t par, uint32_t h) const { return (static_cast<size_t>(par) * (n - 1) + h) * cap; }
-  size_t gather(uint32_t par, uint32_t c) const { return (2ull * (n - 1) + static_cast<size_t>(par) * n + c) * cap; }
+  uint32_t n = 0, ninbox = 0, epoch = 0;
+  size_t slots() const { return 2ull * ninbox + 2ull * n; }
+  size_t inbox(uint32_t par, uint32_t h) const { return (static_cast<size_t>(par) * ninbox + h) * cap; }
+  size_t gather(uint32_t par, uint32_t c) const { return (2ull * ninbox + static_cast<size_t>(par) * n + c) * cap; }
   size_t flags() const { return slots() * cap; }
   size_t iflag(uint32_t par, uint32_t h) const { return flags() + 4 * cap_units * inbox(par, h) / cap; }
   size_t gflag(uint32_t par, uint32_t c) const { return flags() + 4 * cap_units * gather(par, c) / cap; }
@@ -1071,15 +1072,16 @@ uint8_t* ring_pipelined(dq_ctx* ctx, const Prepared& pr, const std::vector<Codec
 // same round, after the stats all-gather has ordered all of every peer's previous
 // round (its last stores into this rank's region) before it.  If any rank cannot map
 // a peer, every rank falls back to the NCCL transport.
-bool peer_setup(dq_ctx* ctx, size_t mb, uint32_t max_nsg, cudaStream_t st) {
+bool peer_setup(dq_ctx* ctx, size_t mb, uint32_t max_nsg, uint32_t ninbox, cudaStream_t st) {
   PeerMem& pm = ctx->pm;
   const uint32_t n = ctx->cfg.n_workers, me = static_cast<uint32_t>(ctx->rank);
-  if (pm.base && pm.n == n && mb <= pm.cap && max_nsg <= pm.cap_units) return true;
+  if (pm.base && pm.n == n && pm.ninbox == ninbox && mb <= pm.cap && max_nsg <= pm.cap_units) return true;
   DQ_CUDA(cudaStreamSynchronize(st));
   ctx->close_peers();
   uint8_t* old = pm.base;
   pm.base = nullptr;
   pm.n = n;
+  pm.ninbox = ninbox;
   pm.cap = (mb + mb / 4 + 4095) & ~static_cast<size_t>(4095);
   pm.cap_units = max_nsg + max_nsg / 4 + 64;
   DQ_CUDA(cudaMalloc(&pm.base, pm.total()));
@@ -1133,6 +1135,9 @@ bool peer_setup(dq_ctx* ctx, size_t mb, uint32_t max_nsg, cudaStream_t st) {
 // ranks therefore overlap at unit granularity.  The sink (hop n-1) stores its chunk
 // into gather slot r of every rank - the all-gather - and one decode launch per rank
 // consumes all n gather slots as their units land.
+void peer_gather_decode(dq_ctx* ctx, const Prepared& p, const std::vector<Layout>& lays, float* out, size_t d,
+                        uint32_t epoch, cudaStream_t st);
+
 void ring_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>& bases,
                const std::vector<Layout>& lays, float* out, size_t d, cudaStream_t st) {
   const uint32_t n = ctx->cfg.n_workers, me = static_cast<uint32_t>(ctx->rank);
@@ -1162,8 +1167,18 @@ void ring_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>& bas
       a.n_outs = static_cast<int>(n);
     }
     const bool dar = h > 0;
-    timed(ctx, dar ? K_DAR : K_LEAF, quant_bytes(lays[ch], dar), st, [&] { launch_quant_peer(a, dar, st); });
+    timed(ctx, dar ? K_DAR : K_LEAF, quant_bytes(lays[ch], dar), st, [&] { launch_quant_peer(a, 0, dar, st); });
   }
+  peer_gather_decode(ctx, p, lays, out, d, epoch, st);
+}
+
+// Every rank decodes all n gather slots of this round's parity into the output, unit by
+// unit as the sinks' stores land (its own slot is complete: its sink ran earlier on st).
+void peer_gather_decode(dq_ctx* ctx, const Prepared& p, const std::vector<Layout>& lays, float* out, size_t d,
+                        uint32_t epoch, cudaStream_t st) {
+  const uint32_t n = ctx->cfg.n_workers, me = static_cast<uint32_t>(ctx->rank);
+  const uint32_t par = epoch & 1u;
+  PeerMem& pm = ctx->pm;
   GatherArgs g{};
   set_format(g, ctx->cfg);
   uint32_t max_nsg = 0;
@@ -1187,6 +1202,100 @@ void ring_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>& bas
   g.n_workers_f = static_cast<float>(n);
   g.uniform_books = ctx->cfg.non_uniform ? 0 : 1;
   timed(ctx, K_DECODE, gbytes, st, [&] { launch_gather_decode(g, n, max_nsg, st); });
+}
+
+// halving stage of a butterfly reduce event (topology.cpp:46-54): partner bit n >> (stage + 1)
+uint32_t butterfly_stage(uint32_t n, const Event& ev) {
+  const uint32_t bit = ev.snd ^ ev.rcv;
+  uint32_t l = 0;
+  while ((n >> (l + 1)) != bit) ++l;
+  return l;
+}
+
+// Butterfly over peer memory: at stage s every sender's fused kernel stores its chunk
+// message into the receiver's inbox s * n + c unit by unit; a receiver's last parent is
+// "held" (read in place, unit by unit, by its own later DAR), earlier parents are
+// decompress-accumulated as their units land (k_da_peer), and the sink's final DAR
+// stores into every rank's gather slot c.  Same events, slots and association order as
+// the reference schedule (topology.cpp:32-70, engine.cpp:162-216).
+void butterfly_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>& bases,
+                    const std::vector<Layout>& lays, const std::vector<Plan>& plans, uint32_t max_nsg, float* out,
+                    size_t d, cudaStream_t st) {
+  const uint32_t n = ctx->cfg.n_workers, me = static_cast<uint32_t>(ctx->rank);
+  uint32_t stages = 0;
+  while ((1u << stages) < n) ++stages;
+  PeerMem& pm = ctx->pm;
+  const uint32_t epoch = ++pm.epoch, par = epoch & 1u;
+  ctx->accs.reserve(static_cast<size_t>(n) * max_nsg * 256);
+  auto acc_ptr = [&](uint32_t ch) { return ctx->accs.p + static_cast<size_t>(ch) * max_nsg * 256; };
+  std::vector<int> held(n, -1);
+  std::vector<char> has_acc(n, 0);
+  auto prep = [&](uint32_t ch) {
+    CodecArgs a = bases[ch];
+    a.unit = peer_unit(lays[ch].nsg);
+    a.epoch = epoch;
+    return a;
+  };
+  auto operand = [&](uint32_t ch, CodecArgs& a) {
+    if (!has_acc[ch]) return 0;
+    a.acc_in = acc_ptr(ch);
+    return 1;
+  };
+  auto inbox_in = [&](CodecArgs& a, uint32_t k) {
+    a.in = pm.base + pm.inbox(par, k);
+    a.in_flags = reinterpret_cast<const uint32_t*>(pm.base + pm.iflag(par, k));
+  };
+  for (uint32_t s = 0; s < stages; ++s) {
+    for (uint32_t ch = 0; ch < n; ++ch)
+      for (size_t e = 0; e < plans[ch].red.size(); ++e) {
+        const Event& ev = plans[ch].red[e];
+        if (ev.snd != me || butterfly_stage(n, ev) != s) continue;
+        CodecArgs a = prep(ch);
+        a.slot = ev.slot;
+        const int src = operand(ch, a);
+        const bool dar = held[ch] >= 0;
+        if (dar) inbox_in(a, static_cast<uint32_t>(held[ch]));
+        const uint32_t k = s * n + ch;
+        a.outs[0] = pm.peer[ev.rcv] + pm.inbox(par, k);
+        a.out_flags[0] = reinterpret_cast<uint32_t*>(pm.peer[ev.rcv] + pm.iflag(par, k));
+        a.n_outs = 1;
+        timed(ctx, dar ? K_DAR : K_LEAF, quant_bytes(lays[ch], dar), st, [&] { launch_quant_peer(a, src, dar, st); });
+        held[ch] = -1;
+      }
+    for (uint32_t ch = 0; ch < n; ++ch) {
+      const Plan& pl = plans[ch];
+      size_t last = 0;
+      for (size_t e = 0; e < pl.red.size(); ++e)
+        if (pl.red[e].rcv == me) last = e;
+      for (size_t e = 0; e < pl.red.size(); ++e) {
+        const Event& ev = pl.red[e];
+        if (ev.rcv != me || butterfly_stage(n, ev) != s) continue;
+        const uint32_t k = s * n + ch;
+        if (e == last && me != pl.sink) {
+          held[ch] = static_cast<int>(k);  // consumed in place by this rank's next send of ch
+          continue;
+        }
+        CodecArgs a = prep(ch);
+        inbox_in(a, k);
+        const int src = operand(ch, a);
+        if (e == last) {  // sink: final DAR straight into every rank's gather slot ch
+          a.slot = pl.sink_slot;
+          for (uint32_t j = 0; j < n; ++j) {
+            const uint32_t q = (me + 1 + j) % n;
+            a.outs[j] = pm.peer[q] + pm.gather(par, ch);
+            a.out_flags[j] = reinterpret_cast<uint32_t*>(pm.peer[q] + pm.gflag(par, ch));
+          }
+          a.n_outs = static_cast<int>(n);
+          timed(ctx, K_DAR, quant_bytes(lays[ch], true), st, [&] { launch_quant_peer(a, src, true, st); });
+        } else {
+          a.acc_out = acc_ptr(ch);
+          timed(ctx, K_DA, 2048.0 * lays[ch].nsg + lays[ch].bytes(), st, [&] { launch_da_peer(a, src, st); });
+          has_acc[ch] = 1;
+        }
+      }
+    }
+  }
+  peer_gather_decode(ctx, p, lays, out, d, epoch, st);
 }
 
 void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info* info, cudaStream_t st) {
@@ -1254,9 +1363,13 @@ void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info
     bases[ch] = b;
   }
   // peer transport: default scale format (the ablation formats run their generic kernels over NCCL)
-  if (c.topology == DQ_RING && ctx->transport == DQ_TRANSPORT_PEER && n <= static_cast<uint32_t>(kMaxPeers) &&
-      lays[0].default_format() && peer_setup(ctx, mb, max_nsg, st)) {
-    ring_peer(ctx, p, bases, lays, out, d, st);
+  uint32_t stages = 0;
+  while ((1u << stages) < n) ++stages;
+  const uint32_t ninbox = c.topology == DQ_RING ? n - 1 : stages * n;
+  if (ctx->transport == DQ_TRANSPORT_PEER && n <= static_cast<uint32_t>(kMaxPeers) && lays[0].default_format() &&
+      peer_setup(ctx, mb, max_nsg, ninbox, st)) {
+    if (c.topology == DQ_RING) ring_peer(ctx, p, bases, lays, out, d, st);
+    else butterfly_peer(ctx, p, bases, lays, plans, max_nsg, out, d, st);
     for (uint32_t ch = 0; ch < n; ++ch) {
       for (uint32_t g = 0; g < plans[ch].n_gat; ++g) account(info, lays[ch], g == 0);
       for (size_t e = 0; e < plans[ch].red.size(); ++e) account(info, lays[ch], true);

@@ -67,8 +67,10 @@ void launch_quant(const CodecArgs& a, int src, bool dar, cudaStream_t st);
 void launch_to_wire(const uint8_t* soa, const Layout& L, uint32_t chunk, uint8_t* out, cudaStream_t st);
 void launch_from_wire(const uint8_t* in, const Layout& L, uint32_t fit, uint8_t* soa, unsigned long long* bad,
                       cudaStream_t st);
-// one ring hop over peer memory (gather source, SRC = 0); see CodecArgs peer fields
-void launch_quant_peer(const CodecArgs& a, bool dar, cudaStream_t st);
+// one hop over peer memory (src 0: raw gradient, 1: acc_in); see CodecArgs peer fields
+void launch_quant_peer(const CodecArgs& a, int src, bool dar, cudaStream_t st);
+// decompress-accumulate of a peer-delivered message (waits per unit) into acc_out
+void launch_da_peer(const CodecArgs& a, int src, cudaStream_t st);
 uint32_t peer_unit(uint32_t nsg);  // super-groups per flag unit of a chunk (same on every rank)
 void launch_da(const CodecArgs& a, int src, cudaStream_t st);
 void launch_decode(const CodecArgs& a, int out_mode, cudaStream_t st);

@@ -31,7 +31,8 @@ def main():
     only = os.environ.get("DIST_CHECK_TRANSPORTS", "peer,nccl").split(",")
     cases = [("ring", 1 << 16, 4.0, t) for t in only]
     cases += [("ring", (1 << 20) + 300, 5.0, t) for t in only]
-    cases += [("butterfly", 1 << 16, 4.0, "nccl"), ("butterfly", (1 << 20) + 300, 3.0, "nccl")]
+    cases += [("butterfly", 1 << 16, 4.0, t) for t in only] + [("butterfly", (1 << 20) + 300, 3.0, t) for t in only]
+    cases += [("butterfly", 1 << 24, 4.0, "peer"), ("butterfly", 3000, 6.0, "peer")]
     cases += [("ring", 1 << 24, 4.0, t) for t in only] + [("ring", 1 << 28, 4.0, t) for t in only]
     cases += [("ring", 3000, 6.0, "peer"), ("ring", 1 << 22, 2.6, "peer")]
     comms = {}
