@@ -47,7 +47,8 @@ def parse():
     p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--d", type=int, default=0, help="entries per worker (default 2^26 at N=1, 2^28 at N>1)")
+    p.add_argument("--entries", "--d", dest="d", type=int, default=0,
+                   help="entries per worker (default 2^26 at N=1, 2^28 at N>1)")
     p.add_argument("--n-sim", type=int, default=4, help="simulated workers at N=1")
     p.add_argument("--budget", type=float, default=4.0)
     p.add_argument("--topology", default="ring", choices=["ring", "butterfly"])

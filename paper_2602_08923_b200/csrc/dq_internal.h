@@ -37,6 +37,10 @@ struct CodecArgs {
   uint32_t* out_flags[kMaxPeers];
   int n_outs;
   uint32_t unit, epoch;
+  // simulated round only: per-entry Fisher-Yates permutations of this chunk
+  // (u8 per entry for n <= 4, u32 for n <= 8); pc_mode 1 = compute + store, 2 = read
+  uint8_t* pcache;
+  int pc_mode;
 };
 
 // All chunks of a round decoded into the output gradient in one launch.
