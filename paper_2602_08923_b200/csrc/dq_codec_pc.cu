@@ -1,0 +1,39 @@
+// dq_codec_pc.cu — simulated-round hop kernels with the per-chunk permutation cache
+// (dq_sim_round): the chunk's first compression stores every entry's Fisher-Yates
+// permutation, later simulated hops read their slot.  Worker counts 2..8, gather operand.
+#include "dq_codec.cuh"
+
+namespace dq {
+namespace {
+template <int NS>
+bool launch_pc_ns(const CodecArgs& a, bool dar, cudaStream_t st) {
+  const uint32_t per_warp = per_warp_sgs(a.L.nsg);
+  const dim3 grid(persistent_grid((a.L.nsg + per_warp - 1) / per_warp, 64));
+  if (a.pc_mode == 1 && !dar) {
+    k_quant<NS, true, 0, false, false, 1><<<grid, kThreads, 0, st>>>(a);
+    return true;
+  }
+  if (a.pc_mode == 2) {
+    if (dar) k_quant<NS, true, 0, true, false, 2><<<grid, kThreads, 0, st>>>(a);
+    else k_quant<NS, true, 0, false, false, 2><<<grid, kThreads, 0, st>>>(a);
+    return true;
+  }
+  return false;
+}
+}  // namespace
+
+bool launch_quant_pc(const CodecArgs& a, int src, bool dar, cudaStream_t st) {
+  if (!a.pcache || src != 0 || !a.correlated) return false;
+  switch (a.n_slots) {
+    case 2: return launch_pc_ns<2>(a, dar, st);
+    case 3: return launch_pc_ns<3>(a, dar, st);
+    case 4: return launch_pc_ns<4>(a, dar, st);
+    case 5: return launch_pc_ns<5>(a, dar, st);
+    case 6: return launch_pc_ns<6>(a, dar, st);
+    case 7: return launch_pc_ns<7>(a, dar, st);
+    case 8: return launch_pc_ns<8>(a, dar, st);
+    default: return false;
+  }
+}
+
+}  // namespace dq

@@ -1,0 +1,49 @@
+// dq_codec_peer.cu — peer-transport kernels (fused hop with NVLink peer stores and
+// per-unit flags; DA of a peer-delivered message).
+#include "dq_codec.cuh"
+
+namespace dq {
+namespace {
+template <int NS, bool CORR>
+void launch_peer_ns(const CodecArgs& a, int src, bool dar, cudaStream_t st) {
+  const uint32_t units = (a.L.nsg + a.unit - 1) / a.unit;
+  const dim3 grid(persistent_grid(units, 64));  // one unit per warp (not persistent: see per_warp_sgs)
+  if (src == 0) {
+    if (dar) k_quant_peer<NS, CORR, 0, true><<<grid, kThreads, 0, st>>>(a);
+    else k_quant_peer<NS, CORR, 0, false><<<grid, kThreads, 0, st>>>(a);
+  } else {
+    if (dar) k_quant_peer<NS, CORR, 1, true><<<grid, kThreads, 0, st>>>(a);
+    else k_quant_peer<NS, CORR, 1, false><<<grid, kThreads, 0, st>>>(a);
+  }
+}
+template <bool CORR>
+void launch_peer_corr(const CodecArgs& a, int src, bool dar, cudaStream_t st) {
+  switch (CORR ? a.n_slots : 1) {
+    case 1: return launch_peer_ns<1, CORR>(a, src, dar, st);
+    case 2: return launch_peer_ns<2, CORR>(a, src, dar, st);
+    case 3: return launch_peer_ns<3, CORR>(a, src, dar, st);
+    case 4: return launch_peer_ns<4, CORR>(a, src, dar, st);
+    case 5: return launch_peer_ns<5, CORR>(a, src, dar, st);
+    case 6: return launch_peer_ns<6, CORR>(a, src, dar, st);
+    case 7: return launch_peer_ns<7, CORR>(a, src, dar, st);
+    case 8: return launch_peer_ns<8, CORR>(a, src, dar, st);
+    default: return launch_peer_ns<0, CORR>(a, src, dar, st);
+  }
+}
+}  // namespace
+
+void launch_da_peer(const CodecArgs& a, int src, cudaStream_t st) {
+  if (a.L.nsg == 0) return;
+  const uint32_t units = (a.L.nsg + a.unit - 1) / a.unit;
+  const dim3 grid(persistent_grid(units, 64));
+  if (src == 0) k_da_peer<0><<<grid, kThreads, 0, st>>>(a);
+  else k_da_peer<1><<<grid, kThreads, 0, st>>>(a);
+}
+
+void launch_quant_peer(const CodecArgs& a, int src, bool dar, cudaStream_t st) {
+  if (a.L.nsg == 0) return;
+  if (a.correlated) launch_peer_corr<true>(a, src, dar, st);
+  else launch_peer_corr<false>(a, src, dar, st);
+}
+
+}  // namespace dq
