@@ -163,6 +163,17 @@ int dq_allocate_fast_stateful(dq_ctx* ctx, const float* d_sq_norms, size_t n_sg,
                               double state[3], uint8_t* d_widths, uint32_t* d_perm, double* u,
                               uint64_t* payload_bits, uint32_t counts[3], void* stream);
 
+/* ---- schedule ------------------------------------------------------------ */
+/* [topology.hpp:15-46 ring_schedule / butterfly_schedule, ChunkPlan] the reduce
+ * events of chunk `chunk` in execution order (sender, receiver, hop slot, and the
+ * stage the multi-GPU executor runs it in: ring = hop index, butterfly = halving
+ * stage), the sink's compression slot and the slot count.  Host only (no device). */
+typedef struct dq_event {
+  uint32_t sender, receiver, slot, stage;
+} dq_event;
+int dq_schedule(uint32_t n_workers, int topology, uint32_t chunk, dq_event* events, uint32_t cap,
+                uint32_t* n_events, uint32_t* sink_slot, uint32_t* n_slots, uint32_t* n_gather);
+
 /* ---- the all-reduce ------------------------------------------------------ */
 /* [engine.hpp:63-64 run_round] all cfg.n_workers gradients resident on this
  * GPU (simulated hops, BASELINE config 2).  d_workers: host array of n device

@@ -811,6 +811,28 @@ static void butterfly_plan(uint32_t n, uint32_t c, plan_t* p) {
   p->n_slots = slot + 1;
 }
 
+/* the plans above through the oracle interface: events as (sender, receiver, slot) */
+int dqo_schedule(uint32_t n, int topology, uint32_t chunk, uint32_t* events, uint32_t cap, uint32_t* n_events,
+                 uint32_t* sink_slot, uint32_t* n_slots, uint32_t* n_gather) {
+  if (!n || n > 64 || chunk >= n) return fail(DQO_EINVAL, "bad schedule arguments");
+  if (topology == 1 && (n & (n - 1))) return fail(DQO_EINVAL, "butterfly topology requires a power-of-two worker count");
+  plan_t p;
+  if (topology == 0) ring_plan(n, chunk, &p); else butterfly_plan(n, chunk, &p);
+  *n_events = p.n_red;
+  *sink_slot = p.sink_slot;
+  *n_slots = p.n_slots;
+  *n_gather = p.n_gat;
+  if (events) {
+    if (cap < p.n_red) return fail(DQO_EINVAL, "event capacity");
+    for (uint32_t e = 0; e < p.n_red; ++e) {
+      events[3 * e] = p.red[e].snd;
+      events[3 * e + 1] = p.red[e].rcv;
+      events[3 * e + 2] = p.red[e].slot;
+    }
+  }
+  return 0;
+}
+
 /* --------------------------------------------------------------- engine   */
 static uint64_t fnv(const uint8_t* b, size_t n, uint64_t h) {
   for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 0x100000001b3ULL;

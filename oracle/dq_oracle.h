@@ -109,6 +109,9 @@ typedef struct {
                                 uint8_t* widths, uint32_t* perm, double* u,                 \
                                 uint64_t* payload_bits);                                    \
   int P##build_permutation(const uint8_t* widths, size_t nsg, uint32_t* perm);              \
+  int P##schedule(uint32_t n, int topology, uint32_t chunk, uint32_t* events, uint32_t cap,  \
+                  uint32_t* n_events, uint32_t* sink_slot, uint32_t* n_slots,                \
+                  uint32_t* n_gather);                                                       \
   int P##run_round(const float* const* workers, size_t d, const dqo_round_cfg* cfg,         \
                    float* synced, uint8_t* widths, uint32_t* perm, dqo_round_out* out);     \
   int P##generate_worker(int kind, size_t d, uint64_t seed, double sigma_log, uint32_t S,   \

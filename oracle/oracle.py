@@ -107,6 +107,7 @@ class Oracle:
         f("allocate_fast_stateful", i32, [P(C.c_float), sz, dbl, u32, u32, i32, P(dbl), P(C.c_uint8),
                                           P(u32), P(dbl), P(u64)])
         f("build_permutation", i32, [P(C.c_uint8), sz, P(u32)])
+        f("schedule", i32, [u32, i32, u32, P(u32), u32, P(u32), P(u32), P(u32), P(u32)])
         f("run_round", i32, [P(P(C.c_float)), sz, P(RoundCfg), P(C.c_float), P(C.c_uint8),
                              P(u32), P(RoundOut)])
         f("generate_worker", i32, [i32, sz, u64, dbl, u32, u32, P(C.c_float)])
@@ -253,6 +254,14 @@ class Oracle:
         p = np.zeros(max(w.size, 1), np.uint32)
         self._check(self._build_permutation(_p(w, C.c_uint8), w.size, _p(p, C.c_uint32)))
         return p[: w.size]
+
+    def schedule(self, n, topology, chunk):
+        """topology.cpp:8-70 -> (events [(sender, receiver, slot)], sink_slot, n_slots, n_gather)"""
+        ev = np.zeros(3 * 64 * 8, np.uint32)
+        ne, ss, ns, ng = C.c_uint32(), C.c_uint32(), C.c_uint32(), C.c_uint32()
+        self._check(self._schedule(n, {"ring": 0, "butterfly": 1}[topology], chunk, _p(ev, C.c_uint32), 64 * 8,
+                                   C.byref(ne), C.byref(ss), C.byref(ns), C.byref(ng)))
+        return [tuple(int(x) for x in ev[3 * e:3 * e + 3]) for e in range(ne.value)], ss.value, ns.value, ng.value
 
     # ---- engine
     @staticmethod

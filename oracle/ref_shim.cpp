@@ -18,6 +18,7 @@
 #include "dynamiq/codec.hpp"
 #include "dynamiq/engine.hpp"
 #include "dynamiq/random.hpp"
+#include "dynamiq/topology.hpp"
 #include "dynamiq/stats.hpp"
 #include "dynamiq/synth.hpp"
 
@@ -192,6 +193,27 @@ int dqref_allocate_fast_stateful(const float* F, size_t nsg, double b, uint32_t 
     state[0] = st.lo;
     state[1] = st.hi;
     state[2] = st.u;
+  });
+}
+int dqref_schedule(uint32_t n, int topology, uint32_t chunk, uint32_t* events, uint32_t cap, uint32_t* n_events,
+                   uint32_t* sink_slot, uint32_t* n_slots, uint32_t* n_gather) {
+  return guarded([&] {
+    Schedule s = topology == 0 ? ring_schedule(n) : butterfly_schedule(n);
+    if (chunk >= s.chunks.size()) throw std::invalid_argument("chunk out of range");
+    const ChunkPlan& p = s.chunks[chunk];
+    *n_events = static_cast<uint32_t>(p.reduce_events.size());
+    *sink_slot = p.sink_compress_slot;
+    *n_slots = p.n_slots;
+    *n_gather = static_cast<uint32_t>(p.gather_events.size());
+    if (events) {
+      if (cap < p.reduce_events.size()) throw std::invalid_argument("event capacity");
+      for (size_t e = 0; e < p.reduce_events.size(); ++e) {
+        events[3 * e] = p.reduce_events[e].sender;
+        events[3 * e + 1] = p.reduce_events[e].receiver;
+        events[3 * e + 2] = p.reduce_events[e].hop_slot;
+      }
+    }
+    if (!validate_schedule(s).ok) throw std::runtime_error("reference schedule failed validation");
   });
 }
 int dqref_build_permutation(const uint8_t* widths, size_t nsg, uint32_t* perm) {

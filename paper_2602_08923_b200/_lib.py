@@ -107,6 +107,8 @@ SIGNATURES = {
     "dq_selftest": (C.c_int, [C.c_int, C.c_uint64, C.c_uint64, _P(C.c_uint64)]),
     "dq_profile_enable": (C.c_int, [_V, C.c_int]),
     "dq_profile_read": (C.c_int, [_V, _P(KernelProfile), C.c_int, _P(C.c_int), C.c_int]),
+    "dq_schedule": (C.c_int, [C.c_uint32, C.c_int, C.c_uint32, _V, C.c_uint32, _P(C.c_uint32), _P(C.c_uint32),
+                              _P(C.c_uint32), _P(C.c_uint32)]),
     "dq_comm_unique_id": (C.c_int, [_u8p]),
     "dq_comm_init": (C.c_int, [_V, C.c_int, C.c_int, _u8p]),
     "dq_allreduce": (C.c_int, [_V, _V, _V, C.c_size_t, _P(RoundInfo), _V]),

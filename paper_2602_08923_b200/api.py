@@ -487,6 +487,20 @@ def run_round_host(worker_values: Sequence[np.ndarray], config: PipelineConfig,
     return out, _info_dict(info)
 
 
+class Event(C.Structure):
+    _fields_ = [("sender", C.c_uint32), ("receiver", C.c_uint32), ("slot", C.c_uint32), ("stage", C.c_uint32)]
+
+
+def schedule(n_workers: int, topology: int, chunk: int) -> dict:
+    """proj/include/dynamiq/topology.hpp ChunkPlan of `chunk`: reduce events (sender, receiver,
+    hop slot, executor stage), sink compression slot, slot count, gather message count."""
+    ev = (Event * 512)()
+    ne, ss, ns, ng = C.c_uint32(), C.c_uint32(), C.c_uint32(), C.c_uint32()
+    check(lib().dq_schedule(n_workers, topology, chunk, ev, 512, C.byref(ne), C.byref(ss), C.byref(ns), C.byref(ng)))
+    return {"events": [(ev[i].sender, ev[i].receiver, ev[i].slot, ev[i].stage) for i in range(ne.value)],
+            "sink_slot": ss.value, "n_slots": ns.value, "n_gather": ng.value}
+
+
 TRANSPORT_PEER, TRANSPORT_NCCL = 0, 1
 
 

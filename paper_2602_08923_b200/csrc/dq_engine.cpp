@@ -2028,6 +2028,28 @@ int dq_profile_read(dq_ctx* ctx, dq_kernel_profile* out, int cap, int* count, in
   });
 }
 
+int dq_schedule(uint32_t n_workers, int topology, uint32_t chunk, dq_event* events, uint32_t cap,
+                uint32_t* n_events, uint32_t* sink_slot, uint32_t* n_slots, uint32_t* n_gather) {
+  return guarded([&] {
+    if (!n_events || !sink_slot || !n_slots || !n_gather) invalid("null argument");
+    if (topology != DQ_RING && topology != DQ_BUTTERFLY) invalid("unknown topology");
+    if (n_workers < 2) invalid(topology == DQ_RING ? "ring schedule requires n >= 2" : "butterfly schedule requires n >= 2");
+    if (n_workers > 64) invalid("n_workers must be at most 64");
+    if (topology == DQ_BUTTERFLY && (n_workers & (n_workers - 1)))
+      invalid("butterfly topology requires a power-of-two worker count");
+    if (chunk >= n_workers) invalid("chunk out of range");
+    const Plan pl = make_plan(n_workers, chunk, topology);
+    *n_events = static_cast<uint32_t>(pl.red.size());
+    *sink_slot = pl.sink_slot;
+    *n_slots = pl.n_slots;
+    *n_gather = pl.n_gat;
+    if (events && cap < pl.red.size()) invalid("event capacity");
+    for (size_t e = 0; events && e < pl.red.size(); ++e)
+      events[e] = dq_event{pl.red[e].snd, pl.red[e].rcv, pl.red[e].slot,
+                           topology == DQ_RING ? static_cast<uint32_t>(e) : butterfly_stage(n_workers, pl.red[e])};
+  });
+}
+
 int dq_comm_unique_id(uint8_t out[128]) {
   return guarded([&] {
     ncclUniqueId id;
