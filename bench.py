@@ -190,7 +190,8 @@ def bench_sim(args):
     for _ in range(args.warmup):
         r = dq.run_round(ws, cfg, out=out, ctx=ctx, metrics=False)
     torch.cuda.synchronize()
-    ctx.profile(True)
+    # timed region: K rounds back to back, no per-launch instrumentation (value)
+    ctx.profile(False)
     ctx.read_profile(reset=True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     per_step = []
@@ -202,12 +203,23 @@ def bench_sim(args):
             per_step.append(r.info["ms_total"])
         e1.record(st)
         torch.cuda.synchronize()
+    launch_counts = ctx.read_profile(reset=True)
+    ms = e0.elapsed_time(e1) / args.steps
+    # the same K rounds again with CUDA events around every launch (per-kernel times,
+    # roofline); the extra event records cost host time, so this region runs slower
+    ctx.profile(True)
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(st)
+    for _ in range(args.steps):
+        dq.run_round(ws, cfg, out=out, ctx=ctx, metrics=False)
+    p1.record(st)
+    torch.cuda.synchronize()
     prof = ctx.read_profile(reset=True)
     ctx.profile(False)
-    ms = e0.elapsed_time(e1) / args.steps
+    prof_ms = p0.elapsed_time(p1) / args.steps
     value = n * 4 * d / (ms * 1e-3) / 1e9
     peak, pk = peaks()
-    launches = sum(p["launches"] for p in prof.values())
+    launches = sum(p["launches"] for p in launch_counts.values())
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
@@ -220,6 +232,8 @@ def bench_sim(args):
         "round_device_ms_median": round(statistics.median(per_step), 4),
         "kernels": {k: {"launches": v["launches"], "ms_per_step": round(v["ms"] / args.steps, 4),
                         "GBps": round(v["bytes"] / max(v["ms"], 1e-9) / 1e6, 1)} for k, v in prof.items()},
+        "kernels_region": {"steps": args.steps, "ms_per_step": round(prof_ms, 4),
+                           "note": "second timed region, CUDA events around every launch"},
         "roofline": roofline_of(prof, peak, pk), "gpu_launches": launches,
         "clocks": clk.summary(),
     }
@@ -282,7 +296,9 @@ def bench_dist(args):
     dist.all_reduce(truth)
     err = float(((out.double() - truth.double()) ** 2).sum())
     ref = float((truth.double() ** 2).sum())
-    comm.ctx.profile(True)
+    # timed region without per-launch instrumentation (value), then the same K rounds
+    # with CUDA events around every launch (per-kernel times, roofline)
+    comm.ctx.profile(False)
     comm.ctx.read_profile(reset=True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
@@ -294,11 +310,24 @@ def bench_dist(args):
         e1.record(st)
         torch.cuda.synchronize()
         dist.barrier()
-    prof = comm.ctx.read_profile(reset=True)
-    comm.ctx.profile(False)
+    launch_counts = comm.ctx.read_profile(reset=True)
     ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = float(ms)
+    comm.ctx.profile(True)
+    dist.barrier()
+    torch.cuda.synchronize()
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(st)
+    for _ in range(args.steps):
+        comm.allreduce(x, out)
+    p1.record(st)
+    torch.cuda.synchronize()
+    prof = comm.ctx.read_profile(reset=True)
+    comm.ctx.profile(False)
+    prof_ms = torch.tensor([p0.elapsed_time(p1) / args.steps], device="cuda")
+    dist.all_reduce(prof_ms, op=dist.ReduceOp.MAX)
+    prof_ms = float(prof_ms)
     # NCCL bf16 all-reduce baseline on the same d
     xb = x.to(torch.bfloat16)
     for _ in range(3):
@@ -318,7 +347,7 @@ def bench_dist(args):
     line = None
     if rank == 0:
         value = world * 4 * d / (ms * 1e-3) / 1e9
-        launches = sum(p["launches"] for k, p in prof.items() if k != "nccl")
+        launches = sum(p["launches"] for k, p in launch_counts.items() if k != "nccl")
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
@@ -334,6 +363,8 @@ def bench_dist(args):
                           "busbw_gbs": round(2 * d / (nms * 1e-3) / 1e9 * 2 * (world - 1) / world, 3)},
             "kernels": {k: {"launches": v["launches"], "ms_per_step": round(v["ms"] / args.steps, 4),
                             "GBps": round(v["bytes"] / max(v["ms"], 1e-9) / 1e6, 1)} for k, v in prof.items()},
+            "kernels_region": {"steps": args.steps, "ms_per_step": round(prof_ms, 4),
+                               "note": "second timed region, CUDA events around every launch"},
             "roofline": roofline_of(prof, peak, pk), "gpu_launches": launches, "clocks": clk.summary(),
         }
     # e2e: pinned host -> device, all-reduce, device -> host

@@ -109,6 +109,8 @@ struct AllocState {
   uint32_t has_pred;
   uint32_t status;         // 0 searching, 1 crossing found, 2 all flips fit, 3 no flips
   uint32_t passes;
+  uint32_t collect;        // the crossing bin holds <= kAllocBins flips: gather and sort them
+  uint32_t ncoll;          // flips gathered by the collect stage
   FlipRec slot[4];
   // candidate samples L-1, L, L+1 (present[c]) with device-libm u / thresholds and the
   // float-threshold payload counts (n8, n4 + n8) the reference's bisection would see

@@ -96,6 +96,32 @@ __device__ __forceinline__ uint64_t dkey(double f) {
   return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 
+// Block-wide reduction of one u64 (all threads call; the result is valid in thread 0),
+// so each CTA issues one global atomic per quantity instead of one per warp: the
+// state words are single addresses and per-warp atomics serialise at L2.
+enum RedOp { kRedMin, kRedMax, kRedAdd };
+template <RedOp OP>
+__device__ __forceinline__ unsigned long long red_op(unsigned long long a, unsigned long long b) {
+  return OP == kRedMin ? (a < b ? a : b) : (OP == kRedMax ? (a > b ? a : b) : a + b);
+}
+template <RedOp OP>
+__device__ unsigned long long block_reduce(unsigned long long v) {
+  __shared__ unsigned long long part[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = red_op<OP>(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if (lane == 0) part[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    const unsigned long long id = OP == kRedMin ? ~0ull : 0ull;
+    v = lane < nw ? part[lane] : id;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = red_op<OP>(v, __shfl_xor_sync(0xffffffffu, v, o));
+  }
+  __syncthreads();
+  return v;
+}
+
 __device__ void alloc_init(AllocState* s, uint64_t* bins, uint64_t wmax) {
   const int t = threadIdx.x;
   for (int b = t; b < kAllocBins; b += blockDim.x) {
@@ -127,16 +153,13 @@ __device__ void alloc_prep(const float* __restrict__ F, uint32_t T, double alpha
     }
     level[j] = l;
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
-    kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
-    npos += __shfl_xor_sync(0xffffffffu, npos, o);
-  }
-  if ((threadIdx.x & 31) == 0 && npos) {
+  kmin = block_reduce<kRedMin>(kmin);
+  kmax = block_reduce<kRedMax>(kmax);
+  const unsigned long long np = block_reduce<kRedAdd>(npos);
+  if (threadIdx.x == 0 && np) {
     atomicMin(reinterpret_cast<unsigned long long*>(&s->kmin), kmin);
     atomicMax(reinterpret_cast<unsigned long long*>(&s->kmax), kmax);
-    atomicAdd(&s->npos, npos);
+    atomicAdd(&s->npos, static_cast<uint32_t>(np));
   }
 }
 
@@ -149,26 +172,33 @@ __device__ void alloc_start(AllocState* s) {
   }
 }
 
+// Bins of the current pass: kAllocBins equal slices of [klo, khi] in key space
+// (order-preserving u64 keys of the flip doubles).  Only weight and count per bin
+// (native 32-bit shared atomics: 64-bit shared min/max would be CAS loops under
+// contention); the next pass narrows to the crossing bin's slice.
+__device__ __forceinline__ int alloc_shift(const AllocState* s) {
+  const uint64_t span = s->khi - s->klo;
+  const int bits = span ? 64 - __clzll(static_cast<long long>(span)) : 0;
+  return bits > 10 ? bits - 10 : 0;
+}
+
+constexpr uint32_t kCollectMax = 256;  // crossing-bin flips finished by rank counting
+
 struct HistSmem {
   uint32_t bw[kAllocBins], bc[kAllocBins];
-  unsigned long long bmn[kAllocBins], bmx[kAllocBins];
+  unsigned long long bmn[kAllocBins];  // alloc_finish: sort keys
 };
 __device__ void alloc_hist(const double* __restrict__ level, uint32_t T, const AllocState* s, uint64_t* bins,
                            HistSmem& hs) {
   uint32_t* bw = hs.bw;
   uint32_t* bc = hs.bc;
-  unsigned long long* bmn = hs.bmn;
-  unsigned long long* bmx = hs.bmx;
   for (int b = threadIdx.x; b < kAllocBins; b += blockDim.x) {
     bw[b] = 0;
     bc[b] = 0;
-    bmn[b] = ~0ull;
-    bmx[b] = 0;
   }
   __syncthreads();
   const uint64_t klo = s->klo, span = s->khi - s->klo;
-  const int bits = span ? 64 - __clzll(static_cast<long long>(span)) : 0;
-  const int shift = bits > 10 ? bits - 10 : 0;
+  const int shift = alloc_shift(s);
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < T; j += gridDim.x * blockDim.x) {
     const double l = level[j];
     if (l != l) continue;
@@ -179,8 +209,6 @@ __device__ void alloc_hist(const double* __restrict__ level, uint32_t T, const A
         const uint32_t b = static_cast<uint32_t>((k - klo) >> shift);
         atomicAdd(&bw[b], t ? 4u : 2u);
         atomicAdd(&bc[b], 1u);
-        atomicMin(&bmn[b], static_cast<unsigned long long>(k));
-        atomicMax(&bmx[b], static_cast<unsigned long long>(k));
       }
     }
   }
@@ -190,25 +218,17 @@ __device__ void alloc_hist(const double* __restrict__ level, uint32_t T, const A
     unsigned long long* g = reinterpret_cast<unsigned long long*>(bins + 4 * b);
     atomicAdd(g + 0, static_cast<unsigned long long>(bw[b]));
     atomicAdd(g + 1, static_cast<unsigned long long>(bc[b]));
-    atomicMin(g + 2, bmn[b]);
-    atomicMax(g + 3, bmx[b]);
   }
 }
 
 __device__ void alloc_scan(AllocState* s, uint64_t* bins) {  // one CTA of kAllocBins threads
   __shared__ uint64_t wsum[32];
   __shared__ uint32_t cross_bin;
-  __shared__ unsigned long long pred_max;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const uint64_t w = bins[4 * t], c = bins[4 * t + 1], mn = bins[4 * t + 2], mx = bins[4 * t + 3];
+  const uint64_t w = bins[4 * t], c = bins[4 * t + 1];
   bins[4 * t] = 0;
   bins[4 * t + 1] = 0;
-  bins[4 * t + 2] = ~0ull;
-  bins[4 * t + 3] = 0;
-  if (t == 0) {
-    cross_bin = 0xffffffffu;
-    pred_max = 0;
-  }
+  if (t == 0) cross_bin = 0xffffffffu;
   // block inclusive scan of the bin weights
   uint64_t incl = w;
 #pragma unroll
@@ -233,24 +253,103 @@ __device__ void alloc_scan(AllocState* s, uint64_t* bins) {  // one CTA of kAllo
   if (w > 0 && below + incl > wmax && below + incl - w <= wmax) cross_bin = t;
   __syncthreads();
   const uint32_t cb = cross_bin;
-  if (cb != 0xffffffffu && static_cast<uint32_t>(t) < cb && c > 0) atomicMax(&pred_max, static_cast<unsigned long long>(mx));
-  __syncthreads();
   if (static_cast<uint32_t>(t) == cb) {
+    const int shift = alloc_shift(s);
+    const uint64_t lo = s->klo + (static_cast<uint64_t>(cb) << shift);
+    const uint64_t w_nom = (1ull << shift) - 1;
+    const uint64_t hi_nom = lo + w_nom < lo ? ~0ull : lo + w_nom;  // no wrap near the top of key space
     s->below_w = below + incl - w;
-    if (pred_max != 0) {
-      s->pred_key = s->has_pred ? max(s->pred_key, static_cast<uint64_t>(pred_max)) : pred_max;
-      s->has_pred = 1;
-    }
-    if (mn == mx) {
+    if (shift == 0) {  // a one-key slice: that key is the crossing flip
       s->status = 1;
-      s->cross_key = mn;
+      s->cross_key = lo;
     } else {
-      s->klo = mn;
-      s->khi = mx;
+      s->klo = lo;
+      s->khi = hi_nom < s->khi ? hi_nom : s->khi;
+      s->collect = c <= kCollectMax ? 1u : 0u;  // few enough flips left: rank them instead of another pass
+      s->ncoll = 0;
     }
     s->passes += 1;
   }
   if (t == 0 && cb == 0xffffffffu) s->status = s->passes == 0 ? 2 : 4;  // 4: internal error
+}
+
+// Collect stage: every flip with key in [klo, khi] (at most kCollectMax of them) into
+// bins[0..) (keys) and bins[kAllocBins..) (weights 2 / 4).
+__device__ void alloc_collect(const double* __restrict__ level, uint32_t T, AllocState* s, uint64_t* bins) {
+  const uint64_t klo = s->klo, span = s->khi - s->klo;
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < T; j += gridDim.x * blockDim.x) {
+    const double l = level[j];
+    if (l != l) continue;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const uint64_t k = dkey(__dsub_rn(t ? 8.0 : 4.0, l));
+      if (k - klo <= span) {
+        const uint32_t at = atomicAdd(&s->ncoll, 1u);
+        if (at < kCollectMax) {
+          bins[at] = k;
+          bins[kAllocBins + at] = t ? 4u : 2u;
+        }
+      }
+    }
+  }
+}
+
+// Finish on one CTA: each collected flip's cumulative weight below and through its key
+// (rank counting over at most kCollectMax flips) gives the crossing key exactly as
+// further histogram passes would: below + w(< key) <= wmax < below + w(<= key).
+__device__ void alloc_finish(AllocState* s, uint64_t* bins, HistSmem& hs) {
+  unsigned long long* key = hs.bmn;
+  uint32_t* w = hs.bw;
+  __shared__ unsigned int winner;
+  const int t = threadIdx.x;
+  const uint32_t n = s->ncoll;
+  if (n > kCollectMax) {  // cannot happen (the scan counted them); fail loudly
+    if (t == 0) s->status = 4;
+    return;
+  }
+  if (t == 0) winner = 0xffffffffu;
+  if (static_cast<uint32_t>(t) < n) {
+    key[t] = bins[t];
+    w[t] = static_cast<uint32_t>(bins[kAllocBins + t]);
+  }
+  __syncthreads();
+  const uint64_t below = s->below_w, wmax = s->wmax;
+  uint64_t lt = 0, le = 0;
+  if (static_cast<uint32_t>(t) < n) {
+    const unsigned long long k = key[t];
+    for (uint32_t i = 0; i < n; ++i) {
+      const unsigned long long ki = key[i];
+      lt += ki < k ? w[i] : 0u;
+      le += ki <= k ? w[i] : 0u;
+    }
+    if (below + lt <= wmax && below + le > wmax) atomicMin(&winner, static_cast<unsigned int>(t));
+  }
+  __syncthreads();
+  if (static_cast<uint32_t>(t) == winner) {
+    s->cross_key = key[t];
+    s->below_w = below + lt;
+    s->status = 1;
+    s->passes += 1;
+  }
+  __syncthreads();
+  if (t == 0 && s->status == 0) s->status = 4;
+}
+
+// The crossing flip's predecessor: the largest flip key below it (0 = none; no key is 0).
+__device__ void alloc_pred(const double* __restrict__ level, uint32_t T, AllocState* s) {
+  const uint64_t ck = s->cross_key;
+  unsigned long long mx = 0;
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < T; j += gridDim.x * blockDim.x) {
+    const double l = level[j];
+    if (l != l) continue;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const uint64_t k = dkey(__dsub_rn(t ? 8.0 : 4.0, l));
+      if (k < ck && k > mx) mx = k;
+    }
+  }
+  mx = block_reduce<kRedMax>(mx);
+  if (threadIdx.x == 0 && mx) atomicMax(reinterpret_cast<unsigned long long*>(&s->pred_key), mx);
 }
 
 // Find an F_j behind each flip key the host needs (crossing, predecessor, largest).
@@ -291,12 +390,9 @@ __device__ void alloc_neighbors(const double* __restrict__ level, uint32_t T, Al
       if (want_above && k > above && k < mn) mn = k;
     }
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-  }
-  if ((threadIdx.x & 31) == 0) {
+  mx = block_reduce<kRedMax>(mx);
+  mn = block_reduce<kRedMin>(mn);
+  if (threadIdx.x == 0) {
     if (mx) atomicMax(reinterpret_cast<unsigned long long*>(&s->slot[0].key), mx);
     if (mn != ~0ull) atomicMin(reinterpret_cast<unsigned long long*>(&s->slot[3].key), mn);
   }
@@ -386,13 +482,11 @@ __device__ void alloc_count(const float* __restrict__ F, uint32_t T, AllocState*
     }
   }
 #pragma unroll
-  for (int c = 0; c < 3; ++c)
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      n8[c] += __shfl_xor_sync(0xffffffffu, n8[c], o);
-      n48[c] += __shfl_xor_sync(0xffffffffu, n48[c], o);
-    }
-  if ((threadIdx.x & 31) == 0)
+  for (int c = 0; c < 3; ++c) {
+    n8[c] = block_reduce<kRedAdd>(n8[c]);
+    n48[c] = block_reduce<kRedAdd>(n48[c]);
+  }
+  if (threadIdx.x == 0)
     for (int c = 0; c < 3; ++c) {
       atomicAdd(&s->cand_n8[c], n8[c]);
       atomicAdd(&s->cand_n48[c], n48[c]);
@@ -435,12 +529,26 @@ __global__ void __launch_bounds__(kAllocBins) k_alloc_coop(const float* __restri
   grid.sync();
   for (int p = 0; p < kAllocMaxPasses; ++p) {
     if (st->status != 0) break;
+    if (st->collect) {
+      alloc_collect(w.level, T, st, w.bins);
+      grid.sync();
+      if (blockIdx.x == 0) alloc_finish(st, w.bins, hs);
+      grid.sync();
+      break;
+    }
     alloc_hist(w.level, T, st, w.bins, hs);
     grid.sync();
     if (blockIdx.x == 0) alloc_scan(st, w.bins);
     grid.sync();
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) alloc_slots_init(st);
+  if (st->status == 1) {
+    alloc_pred(w.level, T, st);
+    grid.sync();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->has_pred = st->status == 1 && st->pred_key != 0;
+    alloc_slots_init(st);
+  }
   grid.sync();
   alloc_neighbors(w.level, T, st);
   grid.sync();
