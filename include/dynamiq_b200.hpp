@@ -15,6 +15,7 @@
 //   codec.hpp:94  serialize_chunk(chunk, cfg) / parse_chunk(bytes, cfg)
 //   stats.hpp:19  compute_stats / reduce_stats
 //   allocation.hpp:63 allocate_fast(sq_norms, spec)
+//   allocation.hpp:57 allocate_general(sq_norms, spec), :80 allocate_fast_stateful(sq_norms, spec, state)
 //   engine.hpp:63 run_round(worker_values, config)
 //
 // CompressedChunk keeps the reference's serialized bytes (its wire format), so
@@ -262,26 +263,73 @@ struct BitAllocation {  // allocation.hpp:40-45
   double u = 0.0;
 };
 
-inline BitAllocation allocate_fast(std::span<const float> sq_norms, const BudgetSpec& spec) {
-  if (spec.widths != std::vector<int>{2, 4, 8}) throw std::invalid_argument("allocate_fast requires W = {2,4,8}");
+struct FastAllocatorState {  // allocation.hpp:75-79
+  double lo = -1e6;
+  double hi = 1e6;
+  double u = 0.0;
+};
+
+namespace detail {
+// upload the norms, run one device allocator on a scratch context, download widths / permutation
+template <class Call>
+inline BitAllocation run_allocator(std::span<const float> sq_norms, const BudgetSpec& spec, Call&& call) {
   dq_config c;
   dq_config_default(&c);
   c.budget_bits = spec.total_bits_per_coordinate;
+  c.group_size = spec.group_size;
+  c.super_group_size = spec.super_group_size;
+  c.hierarchical_scales = spec.hierarchical_scales;
   dq_ctx* ctx = nullptr;
-  detail::check(dq_ctx_create(&c, 0, &ctx));
+  check(dq_ctx_create(&c, 0, &ctx));
   std::unique_ptr<dq_ctx, int (*)(dq_ctx*)> guard(ctx, dq_ctx_destroy);
   const size_t T = sq_norms.size();
-  detail::Dev<float> F(T);
-  detail::Dev<uint8_t> w(T);
-  detail::Dev<uint32_t> p(T);
-  detail::cuda(cudaMemcpy(F.p, sq_norms.data(), T * 4, cudaMemcpyHostToDevice));
+  Dev<float> F(T);
+  Dev<uint8_t> w(T);
+  Dev<uint32_t> p(T);
+  cuda(cudaMemcpy(F.p, sq_norms.data(), T * 4, cudaMemcpyHostToDevice));
   BitAllocation a;
   uint32_t counts[3];
-  detail::check(dq_allocate_fast(ctx, F.p, T, spec.total_bits_per_coordinate, w.p, p.p, &a.u, &a.payload_bits, counts, nullptr));
+  check(call(ctx, F.p, T, w.p, p.p, &a.u, &a.payload_bits, counts));
   a.widths.resize(T);
   a.permutation.resize(T);
-  detail::cuda(cudaMemcpy(a.widths.data(), w.p, T, cudaMemcpyDeviceToHost));
-  detail::cuda(cudaMemcpy(a.permutation.data(), p.p, T * 4, cudaMemcpyDeviceToHost));
+  cuda(cudaMemcpy(a.widths.data(), w.p, T, cudaMemcpyDeviceToHost));
+  cuda(cudaMemcpy(a.permutation.data(), p.p, T * 4, cudaMemcpyDeviceToHost));
+  return a;
+}
+}  // namespace detail
+
+inline BitAllocation allocate_fast(std::span<const float> sq_norms, const BudgetSpec& spec) {
+  if (spec.widths != std::vector<int>{2, 4, 8}) throw std::invalid_argument("allocate_fast requires W = {2,4,8}");
+  return detail::run_allocator(sq_norms, spec, [&](dq_ctx* ctx, const float* F, size_t T, uint8_t* w, uint32_t* p,
+                                                   double* u, uint64_t* pay, uint32_t* counts) {
+    return dq_allocate_fast(ctx, F, T, spec.total_bits_per_coordinate, w, p, u, pay, counts, nullptr);
+  });
+}
+
+// allocation.hpp:57 — the device covers W = {2,4,8}, the set run_round uses (engine.cpp:306-307)
+inline BitAllocation allocate_general(std::span<const float> sq_norms, const BudgetSpec& spec) {
+  if (spec.widths != std::vector<int>{2, 4, 8})
+    throw std::invalid_argument("device allocate_general supports W = {2,4,8}");
+  return detail::run_allocator(sq_norms, spec, [&](dq_ctx* ctx, const float* F, size_t T, uint8_t* w, uint32_t* p,
+                                                   double* u, uint64_t* pay, uint32_t* counts) {
+    return dq_allocate_general(ctx, F, T, spec.total_bits_per_coordinate, w, p, u, pay, counts, nullptr);
+  });
+}
+
+// allocation.hpp:80-81
+inline BitAllocation allocate_fast_stateful(std::span<const float> sq_norms, const BudgetSpec& spec,
+                                            FastAllocatorState& state) {
+  if (spec.widths != std::vector<int>{2, 4, 8}) throw std::invalid_argument("allocate_fast requires W = {2,4,8}");
+  double st[3] = {state.lo, state.hi, state.u};
+  BitAllocation a = detail::run_allocator(
+      sq_norms, spec, [&](dq_ctx* ctx, const float* F, size_t T, uint8_t* w, uint32_t* p, double* u, uint64_t* pay,
+                          uint32_t* counts) {
+        return dq_allocate_fast_stateful(ctx, F, T, spec.total_bits_per_coordinate, st, w, p, u, pay, counts,
+                                         nullptr);
+      });
+  state.lo = st[0];
+  state.hi = st[1];
+  state.u = st[2];
   return a;
 }
 

@@ -2,6 +2,7 @@
 // test_engine.cpp) run against the B200 drop-in header include/dynamiq_b200.hpp.
 // Inputs and expected values come from the CPU oracle (oracle/dq_oracle.h, the
 // checker only).  Built and run by tests/test_gpu_cpp.py on a GPU box.
+#include <cmath>
 #include <cstdio>
 #include <functional>
 #include <string>
@@ -168,6 +169,40 @@ TEST_CASE("single worker is an exact no-op; b=2 is infeasible") {
   cfg.n_workers = 2;
   cfg.budget_bits = 2.0;
   CHECK_THROWS_AS(run_round({w, w}, cfg), InfeasibleBudget);
+}
+
+TEST_CASE("allocate_general and allocate_fast_stateful match the oracle") {
+  auto g = normal_vector(21, 6000, 1.0);
+  std::vector<float> F(g.size());
+  for (size_t j = 0; j < g.size(); ++j) F[j] = static_cast<float>(std::exp(4.0 * g[j]));
+  const int W[3] = {2, 4, 8};
+  for (double b : {3.0, 4.0, 6.0}) {
+    BudgetSpec spec;
+    spec.total_bits_per_coordinate = b;
+    BitAllocation a = allocate_general(F, spec);
+    std::vector<uint8_t> w(F.size());
+    std::vector<uint32_t> p(F.size());
+    double u = 0;
+    uint64_t pay = 0;
+    CHECK(dqo_allocate_general(F.data(), F.size(), b, 16, 256, 1, W, 3, w.data(), p.data(), &u, &pay) == 0);
+    CHECK(a.widths == w);
+    CHECK(a.permutation == p);
+    CHECK(a.u == u);
+    CHECK(a.payload_bits == pay);
+    FastAllocatorState st;
+    double ost[3] = {-1e6, 1e6, 0.0};
+    for (int round = 0; round < 6; ++round) {
+      BitAllocation s = allocate_fast_stateful(F, spec, st);
+      CHECK(dqo_allocate_fast_stateful(F.data(), F.size(), b, 16, 256, 1, ost, w.data(), p.data(), &u, &pay) == 0);
+      CHECK(s.widths == w);
+      CHECK(s.u == u);
+      CHECK(s.payload_bits == pay);
+      CHECK(st.lo == ost[0] && st.hi == ost[1] && st.u == ost[2]);
+    }
+  }
+  BudgetSpec bad;
+  bad.widths = {2, 4, 8, 16};
+  CHECK_THROWS_AS(allocate_general(F, bad), std::invalid_argument);
 }
 
 int main() {
