@@ -103,40 +103,45 @@ int dq_ctx_destroy(dq_ctx* ctx);
 int dq_ctx_set_config(dq_ctx* ctx, const dq_config* cfg);
 
 /* ---- codec primitives on device buffers (one chunk) ----------------------
- * Widths are given as run lengths n8, n4, n2 of the width-sorted body
- * (the reference's wire order, proj/src/codec.cpp:298-315). */
-size_t dq_chunk_bytes(uint32_t n8, uint32_t n4, uint32_t n2);
+ * Widths are given as run lengths n8, n4, n2, n16 of the width-sorted body
+ * (the reference's wire order 8, 4, 2, 16, proj/src/codec.cpp:298-315; width 16
+ * is the bf16 passthrough record, codec.cpp:82-86).  Device chunk bytes: */
+size_t dq_chunk_bytes(uint32_t n8, uint32_t n4, uint32_t n2, uint32_t n16);
+/* [codec.cpp:268-291 compressed_size_bits / 8] reference wire bytes incl. the 24-byte
+ * header (== dq_chunk_bytes + 24 when n16 == 0; passthrough records carry no scales) */
+size_t dq_wire_bytes(uint32_t n8, uint32_t n4, uint32_t n2, uint32_t n16);
 /* [codec.hpp:64-69 compress_chunk] values: n_sg*256 fp32 */
-int dq_compress_chunk(const float* d_values, uint32_t n8, uint32_t n4, uint32_t n2,
+int dq_compress_chunk(const float* d_values, uint32_t n8, uint32_t n4, uint32_t n2, uint32_t n16,
                       const dq_qctx* q, uint32_t first_sg_index, int non_uniform, void* d_out,
                       void* stream);
 /* [codec.hpp:86-91 decompress_accumulate_recompress] */
 int dq_dar_chunk(const void* d_in, const float* d_local, uint32_t n8, uint32_t n4, uint32_t n2,
-                 const dq_qctx* q, uint32_t first_sg_index, int non_uniform, void* d_out,
+                 uint32_t n16, const dq_qctx* q, uint32_t first_sg_index, int non_uniform, void* d_out,
                  void* stream);
 /* [codec.hpp:75-78 decompress_accumulate] acc += decompress(in) */
-int dq_da_chunk(const void* d_in, float* d_acc, uint32_t n8, uint32_t n4, uint32_t n2,
+int dq_da_chunk(const void* d_in, float* d_acc, uint32_t n8, uint32_t n4, uint32_t n2, uint32_t n16,
                 int non_uniform, void* stream);
 /* [codec.hpp:71-73 decompress_chunk] */
 int dq_decompress_chunk(const void* d_in, float* d_out, uint32_t n8, uint32_t n4, uint32_t n2,
-                        int non_uniform, void* stream);
+                        uint32_t n16, int non_uniform, void* stream);
 /* [codec.cpp:319-399 serialize_chunk / parse_chunk] host buffers.
- * to: writes dq_chunk_bytes + 24 bytes.  from: strict parse of reference bytes
+ * to: writes dq_wire_bytes bytes.  from: strict parse of reference bytes
  * (DQ_EMALFORMED on any malformed buffer), returns the run lengths. */
 int dq_to_reference_wire(const void* h_soa, uint32_t chunk_index, uint32_t n8, uint32_t n4,
-                         uint32_t n2, void* h_ref);
+                         uint32_t n2, uint32_t n16, void* h_ref);
 int dq_from_reference_wire(const void* h_ref, size_t len, void* h_soa, size_t soa_cap,
-                           uint32_t* chunk_index, uint32_t* n8, uint32_t* n4, uint32_t* n2);
+                           uint32_t* chunk_index, uint32_t* n8, uint32_t* n4, uint32_t* n2,
+                           uint32_t* n16);
 /* [codec.cpp:319-343 serialize_chunk] device buffers, stream-ordered: d_wire
- * receives dq_chunk_bytes + 24 bytes (header + records), one warp per record. */
+ * receives dq_wire_bytes bytes (header + records), one warp per record. */
 int dq_serialize_chunk(const void* d_soa, uint32_t chunk_index, uint32_t n8, uint32_t n4, uint32_t n2,
-                       void* d_wire, void* stream);
+                       uint32_t n16, void* d_wire, void* stream);
 /* [codec.cpp:345-399 parse_chunk] device buffers: strict parse with the
- * reference's checks and messages (DQ_EMALFORMED; width-16 bodies DQ_EINVAL).
- * Reads the header and the validation verdict back, so it synchronizes `stream`.
- * d_soa may be null (validate only); soa_cap < dq_chunk_bytes -> DQ_EINVAL. */
+ * reference's checks and messages (DQ_EMALFORMED).  Reads the header and the
+ * validation verdict back, so it synchronizes `stream`.  d_soa may be null
+ * (validate only); soa_cap < dq_chunk_bytes -> DQ_EINVAL. */
 int dq_parse_chunk(const void* d_wire, size_t len, void* d_soa, size_t soa_cap, uint32_t* chunk_index,
-                   uint32_t* n8, uint32_t* n4, uint32_t* n2, void* stream);
+                   uint32_t* n8, uint32_t* n4, uint32_t* n2, uint32_t* n16, void* stream);
 
 /* ---- statistics and allocation ------------------------------------------ */
 /* [stats.hpp:19 compute_stats] per super-group fp64-sequential mean / sum of squares */

@@ -61,19 +61,27 @@ struct Dev {  // owning device buffer
   Dev& operator=(const Dev&) = delete;
 };
 struct Runs {
-  uint32_t n8 = 0, n4 = 0, n2 = 0;
+  uint32_t n8 = 0, n4 = 0, n2 = 0, n16 = 0;
+  size_t count() const { return static_cast<size_t>(n8) + n4 + n2 + n16; }
 };
 inline Runs runs_of(std::span<const uint8_t> widths) {  // codec.cpp:298-315 order check
   Runs r;
   int prev = -1;
   for (uint8_t w : widths) {
-    const int cls = w == 8 ? 0 : w == 4 ? 1 : w == 2 ? 2 : -1;
-    if (cls < 0) throw std::invalid_argument("unsupported codec width " + std::to_string(w) + " on device");
+    const int cls = w == 8 ? 0 : w == 4 ? 1 : w == 2 ? 2 : w == 16 ? 3 : -1;
+    if (cls < 0) throw std::invalid_argument("unsupported codec width " + std::to_string(w));
     if (cls < prev) throw std::invalid_argument("chunk body must be ordered by width class 8,4,2,16");
     prev = cls;
-    (cls == 0 ? r.n8 : cls == 1 ? r.n4 : r.n2)++;
+    (cls == 0 ? r.n8 : cls == 1 ? r.n4 : cls == 2 ? r.n2 : r.n16)++;
   }
   return r;
+}
+inline std::vector<uint8_t> widths_of(const Runs& r) {
+  std::vector<uint8_t> w(r.n8, 8);
+  w.insert(w.end(), r.n4, 4);
+  w.insert(w.end(), r.n2, 2);
+  w.insert(w.end(), r.n16, 16);
+  return w;
 }
 }  // namespace detail
 
@@ -130,25 +138,24 @@ inline std::uint64_t compressed_size_bits(std::span<const std::uint8_t> widths, 
 namespace detail {
 // reference bytes -> device SoA chunk
 inline std::unique_ptr<Dev<uint8_t>> upload(const CompressedChunk& c, Runs* r) {
-  std::vector<uint8_t> soa(c.wire.size() + 1);
+  std::vector<uint8_t> soa(c.wire.size() * 2 + 64);  // >= device size (passthrough: +18 B per 512 B record)
   uint32_t ci = 0;
-  check(dq_from_reference_wire(c.wire.data(), c.wire.size(), soa.data(), soa.size(), &ci, &r->n8, &r->n4, &r->n2));
-  const size_t bytes = dq_chunk_bytes(r->n8, r->n4, r->n2);
+  check(dq_from_reference_wire(c.wire.data(), c.wire.size(), soa.data(), soa.size(), &ci, &r->n8, &r->n4, &r->n2,
+                               &r->n16));
+  const size_t bytes = dq_chunk_bytes(r->n8, r->n4, r->n2, r->n16);
   auto d = std::make_unique<Dev<uint8_t>>(bytes);
   cuda(cudaMemcpy(d->p, soa.data(), bytes, cudaMemcpyHostToDevice));
   return d;
 }
 inline CompressedChunk download(const uint8_t* dsoa, uint32_t chunk_index, Runs r) {
-  const size_t bytes = dq_chunk_bytes(r.n8, r.n4, r.n2);
+  const size_t bytes = dq_chunk_bytes(r.n8, r.n4, r.n2, r.n16);
   std::vector<uint8_t> soa(bytes + 1);
   cuda(cudaMemcpy(soa.data(), dsoa, bytes, cudaMemcpyDeviceToHost));
   CompressedChunk c;
   c.chunk_index = chunk_index;
-  c.widths.assign(r.n8, 8);
-  c.widths.insert(c.widths.end(), r.n4, 4);
-  c.widths.insert(c.widths.end(), r.n2, 2);
-  c.wire.resize(bytes + 24);
-  check(dq_to_reference_wire(soa.data(), chunk_index, r.n8, r.n4, r.n2, c.wire.data()));
+  c.widths = widths_of(r);
+  c.wire.resize(dq_wire_bytes(r.n8, r.n4, r.n2, r.n16));
+  check(dq_to_reference_wire(soa.data(), chunk_index, r.n8, r.n4, r.n2, r.n16, c.wire.data()));
   return c;
 }
 inline dq_qctx qctx(const QuantContext& q) {
@@ -164,10 +171,11 @@ inline CompressedChunk compress_chunk(std::span<const float> values, std::span<c
     throw std::invalid_argument("chunk length does not match widths");
   const detail::Runs r = detail::runs_of(widths);
   detail::Dev<float> dv(values.size());
-  detail::Dev<uint8_t> out(dq_chunk_bytes(r.n8, r.n4, r.n2));
+  detail::Dev<uint8_t> out(dq_chunk_bytes(r.n8, r.n4, r.n2, r.n16));
   detail::cuda(cudaMemcpy(dv.p, values.data(), values.size_bytes(), cudaMemcpyHostToDevice));
   const dq_qctx c = detail::qctx(q);
-  detail::check(dq_compress_chunk(dv.p, r.n8, r.n4, r.n2, &c, first_sg_index, books.non_uniform, out.p, nullptr));
+  detail::check(dq_compress_chunk(dv.p, r.n8, r.n4, r.n2, r.n16, &c, first_sg_index, books.non_uniform, out.p,
+                                  nullptr));
   return detail::download(out.p, q.chunk_index, r);
 }
 
@@ -177,13 +185,13 @@ inline CompressedChunk decompress_accumulate_recompress(const CompressedChunk& c
   cfg.validate();
   detail::Runs r;
   auto in = detail::upload(chunk, &r);
-  if (local.size() != static_cast<size_t>(r.n8 + r.n4 + r.n2) * 256)
-    throw std::invalid_argument("local buffer length does not match chunk");
+  if (local.size() != r.count() * 256) throw std::invalid_argument("local buffer length does not match chunk");
   detail::Dev<float> dl(local.size());
-  detail::Dev<uint8_t> out(dq_chunk_bytes(r.n8, r.n4, r.n2));
+  detail::Dev<uint8_t> out(dq_chunk_bytes(r.n8, r.n4, r.n2, r.n16));
   detail::cuda(cudaMemcpy(dl.p, local.data(), local.size_bytes(), cudaMemcpyHostToDevice));
   const dq_qctx c = detail::qctx(q);
-  detail::check(dq_dar_chunk(in->p, dl.p, r.n8, r.n4, r.n2, &c, first_sg_index, books.non_uniform, out.p, nullptr));
+  detail::check(dq_dar_chunk(in->p, dl.p, r.n8, r.n4, r.n2, r.n16, &c, first_sg_index, books.non_uniform, out.p,
+                             nullptr));
   return detail::download(out.p, q.chunk_index, r);
 }
 
@@ -192,10 +200,9 @@ inline void decompress_chunk(const CompressedChunk& chunk, const CodebookSet& bo
   cfg.validate();
   detail::Runs r;
   auto in = detail::upload(chunk, &r);
-  if (out.size() != static_cast<size_t>(r.n8 + r.n4 + r.n2) * 256)
-    throw std::invalid_argument("output length does not match chunk");
+  if (out.size() != r.count() * 256) throw std::invalid_argument("output length does not match chunk");
   detail::Dev<float> d(out.size());
-  detail::check(dq_decompress_chunk(in->p, d.p, r.n8, r.n4, r.n2, books.non_uniform, nullptr));
+  detail::check(dq_decompress_chunk(in->p, d.p, r.n8, r.n4, r.n2, r.n16, books.non_uniform, nullptr));
   detail::cuda(cudaMemcpy(out.data(), d.p, out.size_bytes(), cudaMemcpyDeviceToHost));
 }
 
@@ -204,11 +211,10 @@ inline void decompress_accumulate(const CompressedChunk& chunk, std::span<float>
   cfg.validate();
   detail::Runs r;
   auto in = detail::upload(chunk, &r);
-  if (acc.size() != static_cast<size_t>(r.n8 + r.n4 + r.n2) * 256)
-    throw std::invalid_argument("accumulator length does not match chunk");
+  if (acc.size() != r.count() * 256) throw std::invalid_argument("accumulator length does not match chunk");
   detail::Dev<float> d(acc.size());
   detail::cuda(cudaMemcpy(d.p, acc.data(), acc.size_bytes(), cudaMemcpyHostToDevice));
-  detail::check(dq_da_chunk(in->p, d.p, r.n8, r.n4, r.n2, books.non_uniform, nullptr));
+  detail::check(dq_da_chunk(in->p, d.p, r.n8, r.n4, r.n2, r.n16, books.non_uniform, nullptr));
   detail::cuda(cudaMemcpy(acc.data(), d.p, acc.size_bytes(), cudaMemcpyDeviceToHost));
 }
 
@@ -221,12 +227,11 @@ inline CompressedChunk parse_chunk(std::span<const std::uint8_t> bytes, const Co
   cfg.validate();
   CompressedChunk c;
   c.wire.assign(bytes.begin(), bytes.end());
-  std::vector<uint8_t> soa(bytes.size() + 1);
-  uint32_t n8, n4, n2;
-  detail::check(dq_from_reference_wire(bytes.data(), bytes.size(), soa.data(), soa.size(), &c.chunk_index, &n8, &n4, &n2));
-  c.widths.assign(n8, 8);
-  c.widths.insert(c.widths.end(), n4, 4);
-  c.widths.insert(c.widths.end(), n2, 2);
+  std::vector<uint8_t> soa(bytes.size() * 2 + 64);
+  detail::Runs r;
+  detail::check(dq_from_reference_wire(bytes.data(), bytes.size(), soa.data(), soa.size(), &c.chunk_index, &r.n8,
+                                       &r.n4, &r.n2, &r.n16));
+  c.widths = detail::widths_of(r);
   return c;
 }
 

@@ -11,6 +11,6 @@ from .api import (BUTTERFLY, KIND_FAST, KIND_FIXED, KIND_GENERAL, RING, BitAlloc
                   Communicator, Context, DeviceChunk, FastAllocatorState, PipelineConfig, QuantContext,
                   RoundResult, SharedSeed, ablation_ladder, allocate_fast, allocate_fast_stateful, allocate_general, chunk_bytes, compress_chunk, compressed_size_bits, compute_stats,
                   decompress_accumulate, decompress_accumulate_recompress, decompress_chunk, parse_chunk,
-                  reduce_stats, run_round, run_round_host, schedule, serialize_chunk, soa_from_reference)
+                  reduce_stats, run_round, run_round_host, schedule, serialize_chunk, soa_from_reference, wire_bytes)
 
 __version__ = "0.1.0"

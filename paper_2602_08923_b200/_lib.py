@@ -83,16 +83,19 @@ SIGNATURES = {
     "dq_ctx_create": (C.c_int, [_P(Config), C.c_int, _P(_V)]),
     "dq_ctx_destroy": (C.c_int, [_V]),
     "dq_ctx_set_config": (C.c_int, [_V, _P(Config)]),
-    "dq_chunk_bytes": (C.c_size_t, [C.c_uint32, C.c_uint32, C.c_uint32]),
-    "dq_compress_chunk": (C.c_int, [_V, C.c_uint32, C.c_uint32, C.c_uint32, _P(QCtx), C.c_uint32, C.c_int, _V, _V]),
-    "dq_dar_chunk": (C.c_int, [_V, _V, C.c_uint32, C.c_uint32, C.c_uint32, _P(QCtx), C.c_uint32, C.c_int, _V, _V]),
-    "dq_da_chunk": (C.c_int, [_V, _V, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int, _V]),
-    "dq_decompress_chunk": (C.c_int, [_V, _V, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int, _V]),
-    "dq_to_reference_wire": (C.c_int, [_V, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, _V]),
-    "dq_from_reference_wire": (C.c_int, [_V, C.c_size_t, _V, C.c_size_t, _u32p, _u32p, _u32p, _u32p]),
-    "dq_serialize_chunk": (C.c_int, [_V, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, _V, _V]),
+    "dq_chunk_bytes": (C.c_size_t, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32]),
+    "dq_wire_bytes": (C.c_size_t, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32]),
+    "dq_compress_chunk": (C.c_int, [_V, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, _P(QCtx), C.c_uint32, C.c_int,
+                                    _V, _V]),
+    "dq_dar_chunk": (C.c_int, [_V, _V, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, _P(QCtx), C.c_uint32, C.c_int,
+                               _V, _V]),
+    "dq_da_chunk": (C.c_int, [_V, _V, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int, _V]),
+    "dq_decompress_chunk": (C.c_int, [_V, _V, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int, _V]),
+    "dq_to_reference_wire": (C.c_int, [_V, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, _V]),
+    "dq_from_reference_wire": (C.c_int, [_V, C.c_size_t, _V, C.c_size_t, _u32p, _u32p, _u32p, _u32p, _u32p]),
+    "dq_serialize_chunk": (C.c_int, [_V, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, _V, _V]),
     "dq_parse_chunk": (C.c_int, [_V, C.c_size_t, _V, C.c_size_t, _P(C.c_uint32), _P(C.c_uint32),
-                                 _P(C.c_uint32), _P(C.c_uint32), _V]),
+                                 _P(C.c_uint32), _P(C.c_uint32), _P(C.c_uint32), _V]),
     "dq_compute_stats": (C.c_int, [_V, C.c_size_t, _V, _V, _V]),
     "dq_reduce_stats": (C.c_int, [_V, _V, C.c_uint32, C.c_size_t, _V, _V, _V]),
     "dq_allocate_fast": (C.c_int, [_V, _V, C.c_size_t, C.c_double, _V, _V, _P(C.c_double), _P(C.c_uint64),

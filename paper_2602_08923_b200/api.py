@@ -106,21 +106,27 @@ class PipelineConfig:
 class DeviceChunk:
     """A compressed chunk resident in HBM (dq tiled SoA layout, include/dynamiq_b200.h).
 
-    ``widths`` is implied by the run lengths (8, 4, 2 order) like the
-    reference's wire header (proj/src/codec.cpp:283-317)."""
+    ``widths`` is implied by the run lengths (8, 4, 2, 16 order) like the
+    reference's wire header (proj/src/codec.cpp:283-317); width 16 is the bf16
+    passthrough record (codec.cpp:82-86)."""
     chunk_index: int
     n8: int
     n4: int
     n2: int
-    data: torch.Tensor  # uint8, dq_chunk_bytes(n8, n4, n2)
+    data: torch.Tensor  # uint8, dq_chunk_bytes(n8, n4, n2, n16)
+    n16: int = 0
 
     @property
     def n_sg(self) -> int:
-        return self.n8 + self.n4 + self.n2
+        return self.n8 + self.n4 + self.n2 + self.n16
+
+    @property
+    def runs(self) -> tuple:
+        return self.n8, self.n4, self.n2, self.n16
 
     @property
     def widths(self) -> np.ndarray:
-        return np.array([8] * self.n8 + [4] * self.n4 + [2] * self.n2, np.uint8)
+        return np.array([8] * self.n8 + [4] * self.n4 + [2] * self.n2 + [16] * self.n16, np.uint8)
 
 
 def _stream() -> C.c_void_p:
@@ -136,19 +142,16 @@ def _runs(widths) -> tuple:
     (proj/src/codec.cpp:298-315)."""
     w = np.asarray(widths).astype(np.int64, copy=False).ravel()
     lut = np.full(256, -1, np.int64)
-    lut[[8, 4, 2]] = [0, 1, 2]
+    lut[[8, 4, 2, 16]] = [0, 1, 2, 3]
     ok = (w >= 0) & (w < 256)
     cls = np.where(ok, lut[np.clip(w, 0, 255)], -1)
     bad = np.flatnonzero(cls < 0)
     if bad.size:
-        x = int(w[bad[0]])
-        if x == 16:
-            raise InvalidArgument(2, "width-16 passthrough is not supported by the device codec")
-        raise InvalidArgument(2, f"unsupported codec width {x}")
+        raise InvalidArgument(2, f"unsupported codec width {int(w[bad[0]])}")
     if np.any(np.diff(cls) < 0):
         raise InvalidArgument(2, "chunk body must be ordered by width class 8,4,2,16")
-    cnt = np.bincount(cls, minlength=3)
-    return int(cnt[0]), int(cnt[1]), int(cnt[2])
+    cnt = np.bincount(cls, minlength=4)
+    return int(cnt[0]), int(cnt[1]), int(cnt[2]), int(cnt[3])
 
 
 def _f32(t: torch.Tensor, n: int, what: str) -> torch.Tensor:
@@ -162,8 +165,14 @@ def _f32(t: torch.Tensor, n: int, what: str) -> torch.Tensor:
     return t
 
 
-def chunk_bytes(n8: int, n4: int, n2: int) -> int:
-    return lib().dq_chunk_bytes(n8, n4, n2)
+def chunk_bytes(n8: int, n4: int, n2: int, n16: int = 0) -> int:
+    """Device chunk bytes (dq tiled SoA)."""
+    return lib().dq_chunk_bytes(n8, n4, n2, n16)
+
+
+def wire_bytes(n8: int, n4: int, n2: int, n16: int = 0) -> int:
+    """Reference serialize_chunk bytes incl. the 24-byte header (codec.cpp:268-291)."""
+    return lib().dq_wire_bytes(n8, n4, n2, n16)
 
 
 def compressed_size_bits(widths, S: int = 256, s: int = 16, hierarchical_scales: bool = True) -> int:
@@ -176,13 +185,13 @@ def compressed_size_bits(widths, S: int = 256, s: int = 16, hierarchical_scales:
 def compress_chunk(values: torch.Tensor, widths, cfg: CodecConfig, qctx: QuantContext,
                    first_sg_index: int = 0) -> DeviceChunk:
     cfg.validate()
-    n8, n4, n2 = _runs(widths)
-    v = _f32(values, (n8 + n4 + n2) * 256, "chunk")
-    out = torch.empty(max(chunk_bytes(n8, n4, n2), 1), dtype=torch.uint8, device=v.device)
+    n8, n4, n2, n16 = _runs(widths)
+    v = _f32(values, (n8 + n4 + n2 + n16) * 256, "chunk")
+    out = torch.empty(max(chunk_bytes(n8, n4, n2, n16), 1), dtype=torch.uint8, device=v.device)
     q = qctx._c()
-    check(lib().dq_compress_chunk(_ptr(v), n8, n4, n2, C.byref(q), first_sg_index, int(cfg.non_uniform),
+    check(lib().dq_compress_chunk(_ptr(v), n8, n4, n2, n16, C.byref(q), first_sg_index, int(cfg.non_uniform),
                                   _ptr(out), _stream()))
-    return DeviceChunk(qctx.chunk_index, n8, n4, n2, out)
+    return DeviceChunk(qctx.chunk_index, n8, n4, n2, out, n16)
 
 
 def decompress_accumulate_recompress(chunk: DeviceChunk, local: torch.Tensor, cfg: CodecConfig,
@@ -191,9 +200,9 @@ def decompress_accumulate_recompress(chunk: DeviceChunk, local: torch.Tensor, cf
     loc = _f32(local, chunk.n_sg * 256, "local buffer")
     out = torch.empty_like(chunk.data)
     q = qctx._c()
-    check(lib().dq_dar_chunk(_ptr(chunk.data), _ptr(loc), chunk.n8, chunk.n4, chunk.n2, C.byref(q),
+    check(lib().dq_dar_chunk(_ptr(chunk.data), _ptr(loc), *chunk.runs, C.byref(q),
                              first_sg_index, int(cfg.non_uniform), _ptr(out), _stream()))
-    return DeviceChunk(qctx.chunk_index, chunk.n8, chunk.n4, chunk.n2, out)
+    return DeviceChunk(qctx.chunk_index, chunk.n8, chunk.n4, chunk.n2, out, chunk.n16)
 
 
 def decompress_accumulate(chunk: DeviceChunk, acc: torch.Tensor, cfg: CodecConfig) -> None:
@@ -203,7 +212,7 @@ def decompress_accumulate(chunk: DeviceChunk, acc: torch.Tensor, cfg: CodecConfi
         raise InvalidArgument(2, "accumulator must be a contiguous, aligned CUDA float32 tensor")
     if acc.numel() != chunk.n_sg * 256:
         raise InvalidArgument(2, "accumulator length does not match chunk")
-    check(lib().dq_da_chunk(_ptr(chunk.data), _ptr(acc), chunk.n8, chunk.n4, chunk.n2, int(cfg.non_uniform),
+    check(lib().dq_da_chunk(_ptr(chunk.data), _ptr(acc), *chunk.runs, int(cfg.non_uniform),
                             _stream()))
 
 
@@ -213,7 +222,7 @@ def decompress_chunk(chunk: DeviceChunk, cfg: CodecConfig, out: Optional[torch.T
         out = torch.empty(chunk.n_sg * 256, dtype=torch.float32, device=chunk.data.device)
     elif out.numel() != chunk.n_sg * 256:
         raise InvalidArgument(2, "output length does not match chunk")
-    check(lib().dq_decompress_chunk(_ptr(chunk.data), _ptr(out), chunk.n8, chunk.n4, chunk.n2,
+    check(lib().dq_decompress_chunk(_ptr(chunk.data), _ptr(out), *chunk.runs,
                                     int(cfg.non_uniform), _stream()))
     return out
 
@@ -222,27 +231,30 @@ def serialize_chunk(chunk: DeviceChunk, device: bool = False):
     """Reference wire bytes (proj/src/codec.cpp:319-343): host ``bytes``, or with
     ``device=True`` a CUDA uint8 tensor serialized on the GPU (dq_serialize_chunk)."""
     if device:
-        out = torch.empty(chunk_bytes(chunk.n8, chunk.n4, chunk.n2) + 24, dtype=torch.uint8,
+        out = torch.empty(wire_bytes(*chunk.runs), dtype=torch.uint8,
                           device=chunk.data.device)
-        check(lib().dq_serialize_chunk(_ptr(chunk.data), chunk.chunk_index, chunk.n8, chunk.n4, chunk.n2,
+        check(lib().dq_serialize_chunk(_ptr(chunk.data), chunk.chunk_index, *chunk.runs,
                                        _ptr(out), _stream()))
         return out
     soa = chunk.data.cpu().numpy()
-    out = np.zeros(chunk_bytes(chunk.n8, chunk.n4, chunk.n2) + 24, np.uint8)
-    check(lib().dq_to_reference_wire(soa.ctypes.data_as(C.c_void_p), chunk.chunk_index, chunk.n8, chunk.n4,
-                                     chunk.n2, out.ctypes.data_as(C.c_void_p)))
+    out = np.zeros(wire_bytes(*chunk.runs), np.uint8)
+    check(lib().dq_to_reference_wire(soa.ctypes.data_as(C.c_void_p), chunk.chunk_index, *chunk.runs,
+                                     out.ctypes.data_as(C.c_void_p)))
     return out.tobytes()
 
 
 def soa_from_reference(buf: bytes):
-    """Strict parse of reference wire bytes into the device layout (host numpy array)."""
+    """Strict parse of reference wire bytes into the device layout (host numpy array)
+    -> (chunk_index, n8, n4, n2, n16, soa)."""
     b = np.frombuffer(buf, np.uint8).copy()
-    cap = max(len(buf), 1)
+    count = int(np.frombuffer(b[4:8].tobytes(), np.uint32)[0]) if b.size >= 8 else 0
+    cap = max(len(buf) + 32 * min(count, len(buf)), 1)  # passthrough records carry no scales on the wire
     soa = np.zeros(cap, np.uint8)
-    ci, n8, n4, n2 = C.c_uint32(), C.c_uint32(), C.c_uint32(), C.c_uint32()
+    ci, n8, n4, n2, n16 = (C.c_uint32() for _ in range(5))
     check(lib().dq_from_reference_wire(b.ctypes.data_as(C.c_void_p), b.size, soa.ctypes.data_as(C.c_void_p),
-                                       soa.size, C.byref(ci), C.byref(n8), C.byref(n4), C.byref(n2)))
-    return ci.value, n8.value, n4.value, n2.value, soa[: chunk_bytes(n8.value, n4.value, n2.value)]
+                                       soa.size, C.byref(ci), C.byref(n8), C.byref(n4), C.byref(n2), C.byref(n16)))
+    runs = (n8.value, n4.value, n2.value, n16.value)
+    return (ci.value,) + runs + (soa[: chunk_bytes(*runs)],)
 
 
 def parse_chunk(buf, device="cuda") -> DeviceChunk:
@@ -253,15 +265,17 @@ def parse_chunk(buf, device="cuda") -> DeviceChunk:
     if isinstance(buf, torch.Tensor):
         if not (buf.is_cuda and buf.dtype == torch.uint8 and buf.is_contiguous()):
             raise InvalidArgument(2, "device wire buffer must be a contiguous CUDA uint8 tensor")
-        ci, n8, n4, n2 = C.c_uint32(), C.c_uint32(), C.c_uint32(), C.c_uint32()
-        # a valid body is exactly the device layout's size: len - 24
-        data = torch.empty(max(buf.numel() - 24, 1), dtype=torch.uint8, device=buf.device)
-        check(lib().dq_parse_chunk(_ptr(buf), buf.numel(), _ptr(data), data.numel(), C.byref(ci), C.byref(n8),
-                                   C.byref(n4), C.byref(n2), _stream()))
-        return DeviceChunk(ci.value, n8.value, n4.value, n2.value, data)
-    ci, n8, n4, n2, soa = soa_from_reference(buf)
+        ci, n8, n4, n2, n16 = (C.c_uint32() for _ in range(5))
+        outs = (C.byref(ci), C.byref(n8), C.byref(n4), C.byref(n2), C.byref(n16))
+        # validate and read the run lengths, then parse into a buffer of the device size
+        check(lib().dq_parse_chunk(_ptr(buf), buf.numel(), None, 0, *outs, _stream()))
+        runs = (n8.value, n4.value, n2.value, n16.value)
+        data = torch.empty(max(chunk_bytes(*runs), 1), dtype=torch.uint8, device=buf.device)
+        check(lib().dq_parse_chunk(_ptr(buf), buf.numel(), _ptr(data), data.numel(), *outs, _stream()))
+        return DeviceChunk(ci.value, n8.value, n4.value, n2.value, data, n16.value)
+    ci, n8, n4, n2, n16, soa = soa_from_reference(buf)
     data = torch.from_numpy(soa.copy() if soa.size else np.zeros(1, np.uint8)).to(device)
-    return DeviceChunk(ci, n8, n4, n2, data)
+    return DeviceChunk(ci, n8, n4, n2, data, n16)
 
 
 def compute_stats(x: torch.Tensor):

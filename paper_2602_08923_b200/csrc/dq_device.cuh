@@ -66,6 +66,19 @@ __host__ __device__ __forceinline__ float bf16_to_float(uint16_t b) {
   return c.f;
 #endif
 }
+// Round to nearest even onto bf16; inf/nan pass through truncated, a nan stays a nan
+// (bf16.hpp:17-28, the width-16 passthrough record).
+__device__ __forceinline__ uint16_t bf16_rne(float v) {
+  uint32_t u = __float_as_uint(v);
+  if (((u >> 23) & 0xffu) == 0xffu) {
+    uint16_t hi = static_cast<uint16_t>(u >> 16);
+    if ((u & 0x7fffffu) != 0 && (hi & 0x7f) == 0) hi |= 1;
+    return hi;
+  }
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return static_cast<uint16_t>(u >> 16);
+}
+
 // Round toward +inf onto bf16 with clamp below +inf (bf16.hpp:30-40).
 __device__ __forceinline__ uint16_t bf16_round_up(float v) {
   const uint32_t u = __float_as_uint(v);
@@ -86,21 +99,37 @@ __device__ __forceinline__ uint16_t bf16_round_up(float v) {
 //   hierarchical (default, s = 16): gs = 256/s u8 codes, ss = 2 (bf16 sg_scale);
 //   flat bf16 (ablation): gs = 2 * 256/s bytes (one bf16 per group), ss = 0.
 // gshift = log2(s / 8): lanes per group when a warp holds a super-group 8 entries per lane.
+// Width-16 passthrough super-groups (codec.cpp:82-86: 256 bf16, no scales) form a fourth
+// run after the width-2 run, as on the wire (8, 4, 2, 16); their tile metadata slots
+// are reserved but unused (zero), so the device chunk is 18 B per such super-group
+// larger than its wire body.
 struct Layout {
   uint32_t nsg, n8, n4;
   uint32_t gs = 16, ss = 2, gshift = 1;
+  uint32_t n16 = 0;
   __host__ __device__ bool hierarchical() const { return ss != 0; }
   __host__ __device__ bool default_format() const { return gs == 16 && ss == 2 && gshift == 1; }
-  __host__ __device__ uint32_t n2() const { return nsg - n8 - n4; }
-  __host__ __device__ uint32_t width(uint32_t i) const { return i < n8 ? 8 : (i < n8 + n4 ? 4 : 2); }
+  __host__ __device__ uint32_t n2() const { return nsg - n8 - n4 - n16; }
+  __host__ __device__ uint32_t width(uint32_t i) const {
+    return i < n8 ? 8 : (i < n8 + n4 ? 4 : (i < nsg - n16 ? 2 : 16));
+  }
   // payload bytes of super-groups [0, k)
   __host__ __device__ uint64_t pay_prefix(uint32_t k) const {
     const uint32_t a = k < n8 ? k : n8;
     const uint32_t r = k - a;
     const uint32_t b = r < n4 ? r : n4;
-    const uint32_t c = r - b;
-    return 256ull * a + 128ull * b + 64ull * c;
+    const uint32_t r2 = r - b;
+    if (n16 == 0) return 256ull * a + 128ull * b + 64ull * r2;  // no passthrough run (every round)
+    const uint32_t m2 = n2(), c = r2 < m2 ? r2 : m2;
+    return 256ull * a + 128ull * b + 64ull * c + 512ull * (r2 - c);
   }
+  // scale-metadata bytes of the wire records of super-groups [0, k) (width 16 has none)
+  __host__ __device__ uint64_t meta_prefix(uint32_t k) const {
+    const uint32_t scaled = nsg - n16;
+    return static_cast<uint64_t>(gs + ss) * (k < scaled ? k : scaled);
+  }
+  // wire body bytes (serialize_chunk after the 24-byte header)
+  __host__ __device__ uint64_t wire_body() const { return pay_prefix(nsg) + meta_prefix(nsg); }
   __host__ __device__ uint64_t tile_offset(uint32_t t) const {
     const uint32_t k = t * kTileSG < nsg ? t * kTileSG : nsg;
     return pay_prefix(k) + static_cast<uint64_t>(gs + ss) * k;
@@ -111,7 +140,18 @@ struct Layout {
     uint64_t payload, codes, scale;
     uint32_t width;
   };
+  // a super-group of the quantized runs (i < nsg - n16): width without the passthrough test
+  __host__ __device__ SG locate_q(uint32_t i) const {
+    SG s = locate_at(i);
+    s.width = i < n8 ? 8 : (i < n8 + n4 ? 4 : 2);
+    return s;
+  }
   __host__ __device__ SG locate(uint32_t i) const {
+    SG s = locate_at(i);
+    s.width = width(i);
+    return s;
+  }
+  __host__ __device__ SG locate_at(uint32_t i) const {
     const uint32_t t = i / kTileSG, first = t * kTileSG;
     const uint32_t last = first + kTileSG < nsg ? first + kTileSG : nsg;
     const uint32_t cnt = last - first;
@@ -121,7 +161,6 @@ struct Layout {
     s.payload = base + (pay_prefix(i) - pay_prefix(first));
     s.codes = base + tp + static_cast<uint64_t>(gs) * (i - first);
     s.scale = base + tp + static_cast<uint64_t>(gs) * cnt + static_cast<uint64_t>(ss) * (i - first);
-    s.width = width(i);
     return s;
   }
 };

@@ -706,10 +706,15 @@ void to_reference(const uint8_t* soa, uint32_t chunk, const Layout& L, uint8_t* 
   put32(8, L.n8);
   put32(12, L.n4);
   put32(16, L.n2());
-  put32(20, 0);
+  put32(20, L.n16);
   size_t at = 24;
   for (uint32_t i = 0; i < L.nsg; ++i) {
     const Layout::SG g = L.locate(i);
+    if (g.width == 16) {  // passthrough record: payload only (codec.cpp:334-337)
+      std::memcpy(out + at, soa + g.payload, 512);
+      at += 512;
+      continue;
+    }
     std::memcpy(out + at, soa + g.scale, L.ss);
     std::memcpy(out + at + L.ss, soa + g.codes, L.gs);
     std::memcpy(out + at + L.ss + L.gs, soa + g.payload, 32 * g.width);
@@ -1613,12 +1618,24 @@ int dq_ctx_set_config(dq_ctx* ctx, const dq_config* cfg) {
   });
 }
 
-size_t dq_chunk_bytes(uint32_t n8, uint32_t n4, uint32_t n2) {
-  Layout L{n8 + n4 + n2, n8, n4};
+static Layout runs_layout(uint32_t n8, uint32_t n4, uint32_t n2, uint32_t n16) {
+  if (static_cast<uint64_t>(n8) + n4 + n2 + n16 > 0xffffffffull) invalid("too many super-groups");
+  Layout L{n8 + n4 + n2 + n16, n8, n4};
+  L.n16 = n16;
+  return L;
+}
+
+size_t dq_chunk_bytes(uint32_t n8, uint32_t n4, uint32_t n2, uint32_t n16) {
+  const Layout L = runs_layout(n8, n4, n2, n16);
   return static_cast<size_t>(L.bytes());
 }
 
-static CodecArgs prim_args(const dq_qctx* q, uint32_t n8, uint32_t n4, uint32_t n2, uint32_t first,
+size_t dq_wire_bytes(uint32_t n8, uint32_t n4, uint32_t n2, uint32_t n16) {
+  const Layout L = runs_layout(n8, n4, n2, n16);
+  return static_cast<size_t>(24 + L.wire_body());
+}
+
+static CodecArgs prim_args(const dq_qctx* q, uint32_t n8, uint32_t n4, uint32_t n2, uint32_t n16, uint32_t first,
                            int non_uniform) {
   if (!q) invalid("null qctx");
   if (q->correlated && (q->n_slots == 0 || q->hop_slot >= q->n_slots))
@@ -1631,18 +1648,18 @@ static CodecArgs prim_args(const dq_qctx* q, uint32_t n8, uint32_t n4, uint32_t 
   c.correlated = q->correlated;
   c.non_uniform = non_uniform;
   CodecArgs a = base_args(c, q->chunk_index);
-  a.L = Layout{n8 + n4 + n2, n8, n4};
+  a.L = runs_layout(n8, n4, n2, n16);
   a.first_sg = first;
   a.slot = q->hop_slot;
   a.n_slots = q->n_slots ? q->n_slots : 1;
   return a;
 }
 
-int dq_compress_chunk(const float* d_values, uint32_t n8, uint32_t n4, uint32_t n2, const dq_qctx* q,
+int dq_compress_chunk(const float* d_values, uint32_t n8, uint32_t n4, uint32_t n2, uint32_t n16, const dq_qctx* q,
                       uint32_t first, int non_uniform, void* d_out, void* stream) {
   return guarded([&] {
     ensure_books();
-    CodecArgs a = prim_args(q, n8, n4, n2, first, non_uniform);
+    CodecArgs a = prim_args(q, n8, n4, n2, n16, first, non_uniform);
     a.acc_in = d_values;
     a.out = static_cast<uint8_t*>(d_out);
     launch_quant(a, 1, false, S(stream));
@@ -1650,11 +1667,11 @@ int dq_compress_chunk(const float* d_values, uint32_t n8, uint32_t n4, uint32_t 
   });
 }
 
-int dq_dar_chunk(const void* d_in, const float* d_local, uint32_t n8, uint32_t n4, uint32_t n2,
+int dq_dar_chunk(const void* d_in, const float* d_local, uint32_t n8, uint32_t n4, uint32_t n2, uint32_t n16,
                  const dq_qctx* q, uint32_t first, int non_uniform, void* d_out, void* stream) {
   return guarded([&] {
     ensure_books();
-    CodecArgs a = prim_args(q, n8, n4, n2, first, non_uniform);
+    CodecArgs a = prim_args(q, n8, n4, n2, n16, first, non_uniform);
     a.acc_in = d_local;
     a.in = static_cast<const uint8_t*>(d_in);
     a.out = static_cast<uint8_t*>(d_out);
@@ -1663,12 +1680,12 @@ int dq_dar_chunk(const void* d_in, const float* d_local, uint32_t n8, uint32_t n
   });
 }
 
-int dq_da_chunk(const void* d_in, float* d_acc, uint32_t n8, uint32_t n4, uint32_t n2, int non_uniform,
+int dq_da_chunk(const void* d_in, float* d_acc, uint32_t n8, uint32_t n4, uint32_t n2, uint32_t n16, int non_uniform,
                 void* stream) {
   return guarded([&] {
     ensure_books();
     dq_qctx q{0, 0, 0, 0, 1, 0};
-    CodecArgs a = prim_args(&q, n8, n4, n2, 0, non_uniform);
+    CodecArgs a = prim_args(&q, n8, n4, n2, n16, 0, non_uniform);
     a.in = static_cast<const uint8_t*>(d_in);
     a.acc_in = d_acc;
     a.acc_out = d_acc;
@@ -1677,12 +1694,12 @@ int dq_da_chunk(const void* d_in, float* d_acc, uint32_t n8, uint32_t n4, uint32
   });
 }
 
-int dq_decompress_chunk(const void* d_in, float* d_out, uint32_t n8, uint32_t n4, uint32_t n2,
+int dq_decompress_chunk(const void* d_in, float* d_out, uint32_t n8, uint32_t n4, uint32_t n2, uint32_t n16,
                         int non_uniform, void* stream) {
   return guarded([&] {
     ensure_books();
     dq_qctx q{0, 0, 0, 0, 1, 0};
-    CodecArgs a = prim_args(&q, n8, n4, n2, 0, non_uniform);
+    CodecArgs a = prim_args(&q, n8, n4, n2, n16, 0, non_uniform);
     a.in = static_cast<const uint8_t*>(d_in);
     a.acc_out = d_out;
     launch_decode(a, 0, S(stream));
@@ -1691,29 +1708,29 @@ int dq_decompress_chunk(const void* d_in, float* d_out, uint32_t n8, uint32_t n4
 }
 
 int dq_to_reference_wire(const void* h_soa, uint32_t chunk_index, uint32_t n8, uint32_t n4, uint32_t n2,
-                         void* h_ref) {
+                         uint32_t n16, void* h_ref) {
   return guarded([&] {
-    Layout L{n8 + n4 + n2, n8, n4};
+    const Layout L = runs_layout(n8, n4, n2, n16);
     to_reference(static_cast<const uint8_t*>(h_soa), chunk_index, L, static_cast<uint8_t*>(h_ref));
   });
 }
 
 int dq_serialize_chunk(const void* d_soa, uint32_t chunk_index, uint32_t n8, uint32_t n4, uint32_t n2,
-                       void* d_wire, void* stream) {
+                       uint32_t n16, void* d_wire, void* stream) {
   return guarded([&] {
-    if (!d_wire || (!d_soa && n8 + n4 + n2)) invalid("null argument");
+    if (!d_wire || (!d_soa && n8 + n4 + n2 + n16)) invalid("null argument");
     if (reinterpret_cast<uintptr_t>(d_wire) % 4 || reinterpret_cast<uintptr_t>(d_soa) % 2)
       invalid("wire buffer must be 4-byte aligned, chunk 2-byte aligned");
-    const Layout L{n8 + n4 + n2, n8, n4};
+    const Layout L = runs_layout(n8, n4, n2, n16);
     launch_to_wire(static_cast<const uint8_t*>(d_soa), L, chunk_index, static_cast<uint8_t*>(d_wire), S(stream));
     DQ_CUDA(cudaGetLastError());
   });
 }
 
 int dq_parse_chunk(const void* d_wire, size_t len, void* d_soa, size_t soa_cap, uint32_t* chunk_index,
-                   uint32_t* n8, uint32_t* n4, uint32_t* n2, void* stream) {
+                   uint32_t* n8, uint32_t* n4, uint32_t* n2, uint32_t* n16, void* stream) {
   return guarded([&] {
-    if (!chunk_index || !n8 || !n4 || !n2 || (!d_wire && len)) invalid("null argument");
+    if (!chunk_index || !n8 || !n4 || !n2 || !n16 || (!d_wire && len)) invalid("null argument");
     if (reinterpret_cast<uintptr_t>(d_wire) % 2 || reinterpret_cast<uintptr_t>(d_soa) % 2)
       invalid("buffers must be 2-byte aligned");
     auto mal = [](const char* m) { throw Error(DQ_EMALFORMED, std::string("malformed compressed buffer: ") + m); };
@@ -1725,16 +1742,16 @@ int dq_parse_chunk(const void* d_wire, size_t len, void* d_soa, size_t soa_cap, 
     DQ_CUDA(cudaStreamSynchronize(st));
     const uint32_t count = h[1], r8 = h[2], r4 = h[3], r2 = h[4], r16 = h[5];
     if (static_cast<uint64_t>(r8) + r4 + r2 + r16 != count) mal("width run-lengths do not sum to the super-group count");
-    if (r16) invalid("width-16 passthrough is not supported by the device codec");
-    const Layout L{count, r8, r4};
-    // super-groups whose record fits in len (codec.cpp:380-383 checks each before reading it)
+    Layout L{count, r8, r4};
+    L.n16 = r16;
+    // super-groups whose record fits in len (codec.cpp:371-383 checks each before reading it)
     const uint64_t body = len - 24;
     uint32_t fit = count;
-    if (L.pay_prefix(count) + static_cast<uint64_t>(L.gs + L.ss) * count > body) {
+    if (L.wire_body() > body) {
       uint32_t lo = 0, hi = count;  // largest k with record_end(k) <= body
       while (lo < hi) {
         const uint32_t mid = lo + (hi - lo + 1) / 2;
-        if (L.pay_prefix(mid) + static_cast<uint64_t>(L.gs + L.ss) * mid <= body) lo = mid;
+        if (L.pay_prefix(mid) + L.meta_prefix(mid) <= body) lo = mid;
         else hi = mid - 1;
       }
       fit = lo;
@@ -1750,18 +1767,19 @@ int dq_parse_chunk(const void* d_wire, size_t len, void* d_soa, size_t soa_cap, 
     DQ_CUDA(cudaFreeAsync(bad, st));
     DQ_CUDA(cudaStreamSynchronize(st));
     if (hb != ~0ull) mal(hb & 1 ? "zero super-group scale with nonzero payload" : "zero super-group scale with nonzero group scale");
-    if (fit < count) mal("truncated super-group body");
-    if (24 + L.bytes() != len) mal("trailing bytes after chunk body");
+    if (fit < count) mal(L.width(fit) == 16 ? "truncated width-16 body" : "truncated super-group body");
+    if (24 + L.wire_body() != len) mal("trailing bytes after chunk body");
     if (d_soa && !write) invalid("output capacity");
     *chunk_index = h[0];
     *n8 = r8;
     *n4 = r4;
     *n2 = r2;
+    *n16 = r16;
   });
 }
 
 int dq_from_reference_wire(const void* h_ref, size_t len, void* h_soa, size_t soa_cap,
-                           uint32_t* chunk_index, uint32_t* n8, uint32_t* n4, uint32_t* n2) {
+                           uint32_t* chunk_index, uint32_t* n8, uint32_t* n4, uint32_t* n2, uint32_t* n16) {
   // strict parser with the reference's checks (codec.cpp:345-399), S=256, s=16, hierarchical
   return guarded([&] {
     const uint8_t* b = static_cast<const uint8_t*>(h_ref);
@@ -1774,11 +1792,16 @@ int dq_from_reference_wire(const void* h_ref, size_t len, void* h_soa, size_t so
     const uint32_t count = get32(4);
     const uint32_t r8 = get32(8), r4 = get32(12), r2 = get32(16), r16 = get32(20);
     if (static_cast<uint64_t>(r8) + r4 + r2 + r16 != count) mal("width run-lengths do not sum to the super-group count");
-    if (r16) invalid("width-16 passthrough is not supported by the device codec");
     Layout L{count, r8, r4};
+    L.n16 = r16;
     size_t at = 24;
     for (uint32_t i = 0; i < count; ++i) {
       const uint32_t w = L.width(i);
+      if (w == 16) {
+        if (len - at < 512) mal("truncated width-16 body");
+        at += 512;
+        continue;
+      }
       const size_t rec = 18 + 32 * w;
       if (len - at < rec) mal("truncated super-group body");
       if ((b[at] | b[at + 1] << 8) == 0) {
@@ -1795,6 +1818,13 @@ int dq_from_reference_wire(const void* h_ref, size_t len, void* h_soa, size_t so
     at = 24;
     for (uint32_t i = 0; i < count; ++i) {
       const Layout::SG g = L.locate(i);
+      if (g.width == 16) {  // reserved scale slots read as zero
+        std::memset(o + g.scale, 0, 2);
+        std::memset(o + g.codes, 0, 16);
+        std::memcpy(o + g.payload, b + at, 512);
+        at += 512;
+        continue;
+      }
       std::memcpy(o + g.scale, b + at, 2);
       std::memcpy(o + g.codes, b + at + 2, 16);
       std::memcpy(o + g.payload, b + at + 18, 32 * g.width);
@@ -1804,6 +1834,7 @@ int dq_from_reference_wire(const void* h_ref, size_t len, void* h_soa, size_t so
     *n8 = r8;
     *n4 = r4;
     *n2 = r2;
+    *n16 = r16;
   });
 }
 

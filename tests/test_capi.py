@@ -60,27 +60,36 @@ def test_version_and_defaults(L):
     assert (c.fixed_width, c.allocator, c.topology, c.codec, c.seed, c.round, c.threads) == (4, 1, 0, 0, 1, 0, 1)
 
 
-@pytest.mark.parametrize("runs", [(0, 0, 0), (1, 0, 0), (3, 5, 9), (64, 0, 1), (70, 70, 70)])
+def _widths(runs):
+    runs = tuple(runs) + (0,) * (4 - len(runs))
+    return [8] * runs[0] + [4] * runs[1] + [2] * runs[2] + [16] * runs[3]
+
+
+@pytest.mark.parametrize("runs", [(0, 0, 0, 0), (1, 0, 0, 0), (3, 5, 9, 0), (64, 0, 1, 0), (70, 70, 70, 0),
+                                  (0, 0, 0, 1), (2, 3, 4, 5), (64, 0, 0, 64)])
 def test_chunk_bytes_match_wire_size(L, port, runs):
-    w = [8] * runs[0] + [4] * runs[1] + [2] * runs[2]
-    assert L.dq_chunk_bytes(*runs) * 8 == port.compressed_size_bits(w) - 192
+    w = _widths(runs)
+    assert L.dq_wire_bytes(*runs) * 8 == port.compressed_size_bits(w)
+    assert L.dq_chunk_bytes(*runs) == L.dq_wire_bytes(*runs) - 24 + 18 * runs[3]
 
 
 def _ref_bytes(port, runs, seed=1):
-    w = np.array([8] * runs[0] + [4] * runs[1] + [2] * runs[2], np.uint8)
+    w = np.array(_widths(runs), np.uint8)
     v = det_values(seed, w.size * 256)
     return port.compress_chunk(v, w, port.codec(), port.qctx(seed, 0, 3, 1, 4, True), first_sg=2)
 
 
-@pytest.mark.parametrize("runs", [(1, 0, 0), (0, 1, 0), (0, 0, 1), (3, 5, 9), (65, 2, 64), (0, 130, 1)])
+@pytest.mark.parametrize("runs", [(1, 0, 0, 0), (0, 1, 0, 0), (0, 0, 1, 0), (3, 5, 9, 0), (65, 2, 64, 0),
+                                  (0, 130, 1, 0), (0, 0, 0, 1), (1, 2, 3, 4), (70, 0, 0, 70)])
 def test_wire_roundtrip(port, runs):
     import paper_2602_08923_b200 as dq
     ref = _ref_bytes(port, runs)
-    ci, n8, n4, n2, soa = dq.soa_from_reference(ref)
-    assert (ci, n8, n4, n2) == (3,) + runs
+    ci, n8, n4, n2, n16, soa = dq.soa_from_reference(ref)
+    assert (ci, n8, n4, n2, n16) == (3,) + runs
     out = np.zeros(len(ref), np.uint8)
     from paper_2602_08923_b200._lib import check, lib
-    check(lib().dq_to_reference_wire(soa.ctypes.data_as(C.c_void_p), ci, n8, n4, n2, out.ctypes.data_as(C.c_void_p)))
+    check(lib().dq_to_reference_wire(soa.ctypes.data_as(C.c_void_p), ci, n8, n4, n2, n16,
+                                     out.ctypes.data_as(C.c_void_p)))
     assert out.tobytes() == ref
 
 
@@ -101,24 +110,30 @@ def test_malformed_rejected(port):
     z[-1] = 0xFF
     with pytest.raises(dq.MalformedBuffer):
         dq.soa_from_reference(bytes(z))
+    # passthrough records: their own truncation message, no zero-scale rule (codec.cpp:371-376)
+    p16 = _ref_bytes(port, (1, 0, 0, 2), seed=5)
+    with pytest.raises(dq.MalformedBuffer, match="truncated width-16 body"):
+        dq.soa_from_reference(p16[:-1])
+    with pytest.raises(dq.MalformedBuffer, match="truncated super-group body"):
+        dq.soa_from_reference(p16[:24 + 100])
 
 
 def test_random_flips_reject_or_roundtrip(port):
     """proj/tests/test_codec.cpp:209-222: a flipped bit is rejected or re-serializes identically."""
     import paper_2602_08923_b200 as dq
     from paper_2602_08923_b200._lib import check, lib
-    ref = _ref_bytes(port, (1, 1, 1), seed=4)
+    ref = _ref_bytes(port, (1, 1, 1, 1), seed=4)
     rng = np.random.default_rng(0)
-    for _ in range(300):
+    for _ in range(400):
         t = bytearray(ref)
         pos = int(rng.integers(0, len(t)))
         t[pos] ^= 1 << int(rng.integers(0, 8))
         try:
-            ci, n8, n4, n2, soa = dq.soa_from_reference(bytes(t))
+            ci, n8, n4, n2, n16, soa = dq.soa_from_reference(bytes(t))
         except (dq.MalformedBuffer, dq.InvalidArgument):
             continue
-        out = np.zeros(dq.chunk_bytes(n8, n4, n2) + 24, np.uint8)
-        check(lib().dq_to_reference_wire(soa.ctypes.data_as(C.c_void_p), ci, n8, n4, n2,
+        out = np.zeros(dq.wire_bytes(n8, n4, n2, n16), np.uint8)
+        check(lib().dq_to_reference_wire(soa.ctypes.data_as(C.c_void_p), ci, n8, n4, n2, n16,
                                          out.ctypes.data_as(C.c_void_p)))
         assert out.tobytes() == bytes(t)
 

@@ -23,7 +23,8 @@ def dq():
     return dq
 
 
-RUNS = [(1, 0, 0), (0, 1, 0), (0, 0, 1), (3, 5, 9), (70, 1, 60), (0, 130, 0), (64, 64, 64)]
+RUNS = [(1, 0, 0), (0, 1, 0), (0, 0, 1), (3, 5, 9), (70, 1, 60), (0, 130, 0), (64, 64, 64),
+        (0, 0, 0, 1), (2, 3, 4, 5), (64, 0, 1, 70)]  # width-16 passthrough runs last (codec.cpp:82-86)
 SLOTS = [(1, 0), (2, 0), (2, 1), (3, 2), (4, 0), (4, 1), (4, 3), (5, 4), (6, 2), (7, 6), (8, 0), (8, 1),
          (8, 4), (8, 7), (16, 0), (16, 9)]
 
@@ -152,7 +153,9 @@ def test_errors(dq):
     with pytest.raises(dq.InvalidArgument):
         dq.compress_chunk(x, [4, 8], cfg, dq.QuantContext())  # unsorted body
     with pytest.raises(dq.InvalidArgument):
-        dq.compress_chunk(x, [16, 16], cfg, dq.QuantContext())
+        dq.compress_chunk(x, [3, 3], cfg, dq.QuantContext())  # check_width (codec.cpp:15-18)
+    with pytest.raises(dq.InvalidArgument):
+        dq.compress_chunk(x, [16, 2], cfg, dq.QuantContext())  # passthrough run must be last
     with pytest.raises(dq.InvalidArgument):
         dq.compress_chunk(x, [4], cfg, dq.QuantContext())  # length mismatch
     with pytest.raises(dq.InvalidArgument):

@@ -23,8 +23,13 @@ def _vals(seed, n):
     return det_values(seed, n) if n else np.zeros(0, np.float32)
 
 
+def _widths(runs):
+    runs = tuple(runs) + (0,) * (4 - len(runs))
+    return [8] * runs[0] + [4] * runs[1] + [2] * runs[2] + [16] * runs[3]
+
+
 def _ref_bytes(port, runs, seed=1):
-    w = np.array([8] * runs[0] + [4] * runs[1] + [2] * runs[2], np.uint8)
+    w = np.array(_widths(runs), np.uint8)
     v = _vals(seed, w.size * 256)
     return port.compress_chunk(v, w, port.codec(), port.qctx(seed, 0, 3, 1, 4, True), first_sg=2)
 
@@ -33,13 +38,14 @@ def _dev(b: bytes):
     return torch.tensor(np.frombuffer(b, np.uint8).copy(), dtype=torch.uint8, device="cuda")
 
 
-RUNS = [(0, 0, 0), (1, 0, 0), (0, 1, 0), (0, 0, 1), (3, 5, 9), (65, 2, 64), (0, 130, 1), (200, 300, 500)]
+RUNS = [(0, 0, 0), (1, 0, 0), (0, 1, 0), (0, 0, 1), (3, 5, 9), (65, 2, 64), (0, 130, 1), (200, 300, 500),
+        (0, 0, 0, 1), (1, 2, 3, 4), (64, 0, 0, 65)]
 
 
 @pytest.mark.parametrize("runs", RUNS)
 def test_device_serialize_matches_oracle(dq, port, runs):
     """GPU compress -> GPU serialize == the oracle's compress_chunk wire bytes."""
-    w = [8] * runs[0] + [4] * runs[1] + [2] * runs[2]
+    w = _widths(runs)
     v = _vals(1, len(w) * 256)
     ch = dq.compress_chunk(torch.from_numpy(v).cuda(), w, dq.CodecConfig(),
                            dq.QuantContext(dq.SharedSeed(1, 0), 3, 1, 4, True), first_sg_index=2)
@@ -51,9 +57,9 @@ def test_device_serialize_matches_oracle(dq, port, runs):
 @pytest.mark.parametrize("runs", RUNS)
 def test_device_parse_matches_host(dq, port, runs):
     ref = _ref_bytes(port, runs)
-    ci, n8, n4, n2, soa = dq.soa_from_reference(ref)
+    ci, n8, n4, n2, n16, soa = dq.soa_from_reference(ref)
     ch = dq.parse_chunk(_dev(ref))
-    assert (ch.chunk_index, ch.n8, ch.n4, ch.n2) == (ci, n8, n4, n2)
+    assert (ch.chunk_index, ch.n8, ch.n4, ch.n2, ch.n16) == (ci, n8, n4, n2, n16)
     assert np.array_equal(ch.data.cpu().numpy()[: soa.size], soa)
     assert bytes(dq.serialize_chunk(ch, device=True).cpu().numpy()) == ref
 
@@ -72,9 +78,9 @@ def _same(dq, buf: bytes):
     dev = _outcome(lambda: dq.parse_chunk(_dev(buf)))
     assert host[0] == dev[0], (host, dev)
     if host[0] == "ok":
-        ci, n8, n4, n2, soa = host[1]
+        ci, n8, n4, n2, n16, soa = host[1]
         ch = dev[1]
-        assert (ch.chunk_index, ch.n8, ch.n4, ch.n2) == (ci, n8, n4, n2)
+        assert (ch.chunk_index, ch.n8, ch.n4, ch.n2, ch.n16) == (ci, n8, n4, n2, n16)
         assert np.array_equal(ch.data.cpu().numpy()[: soa.size], soa)
     else:
         assert host[1] == dev[1]
@@ -90,9 +96,12 @@ def test_device_parse_malformed(dq, port):
     t[8] += 1  # run lengths no longer sum to the count
     assert _same(dq, bytes(t)) == "MalformedBuffer"
     t = bytearray(ref)
-    t[20] = 1  # width-16 body
+    t[20] = 1  # a width-16 run the body does not hold
     t[4] += 1
-    assert _same(dq, bytes(t)) == "InvalidArgument"
+    assert _same(dq, bytes(t)) == "MalformedBuffer"
+    p16 = _ref_bytes(port, (1, 0, 0, 2), seed=5)
+    for cut in (len(p16) - 1, 24 + 100, 24 + 274 + 511):
+        assert _same(dq, p16[:cut]) == "MalformedBuffer"
     zeros = port.compress_chunk(np.zeros(3 * 256, np.float32), np.array([8, 4, 2], np.uint8), port.codec(),
                                 port.qctx(9))
     for pos, kind in ((24 + 2, "group scale"), (-1, "payload"), (24 + 274 + 146 + 5, "group scale")):
@@ -113,7 +122,7 @@ def test_device_parse_malformed(dq, port):
 def test_device_parse_random_flips(dq, port):
     """test_codec.cpp:209-222: a flipped bit is rejected or re-serializes identically,
     with the same verdict and message as the host parser."""
-    ref = _ref_bytes(port, (2, 2, 2), seed=4)
+    ref = _ref_bytes(port, (2, 2, 2, 2), seed=4)
     zeros = port.compress_chunk(np.zeros(6 * 256, np.float32), np.array([8, 8, 4, 4, 2, 2], np.uint8),
                                 port.codec(), port.qctx(4))
     rng = np.random.default_rng(0)
@@ -139,7 +148,7 @@ def test_device_wire_roundtrip_large(dq):
     w = np.repeat(np.array([8, 4, 2], np.uint8), [n8, n4, n2])
     ch = dq.compress_chunk(x, w, dq.CodecConfig(), dq.QuantContext(dq.SharedSeed(1, 0), 1, 0, 4, True))
     wire = dq.serialize_chunk(ch, device=True)
-    assert wire.numel() == dq.chunk_bytes(n8, n4, n2) + 24
+    assert wire.numel() == dq.wire_bytes(n8, n4, n2)
     back = dq.parse_chunk(wire)
     assert torch.equal(back.data[: ch.data.numel()], ch.data)
     assert torch.equal(dq.serialize_chunk(back, device=True), wire)

@@ -36,5 +36,5 @@ def sg_block(rng: np.random.Generator, nsg: int, kind: str = "mixed") -> np.ndar
     raise ValueError(kind)
 
 
-def sorted_widths(n8: int, n4: int, n2: int) -> np.ndarray:
-    return np.array([8] * n8 + [4] * n4 + [2] * n2, np.uint8)
+def sorted_widths(n8: int, n4: int, n2: int, n16: int = 0) -> np.ndarray:
+    return np.array([8] * n8 + [4] * n4 + [2] * n2 + [16] * n16, np.uint8)
