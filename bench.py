@@ -143,10 +143,21 @@ def roofline_of(prof, peak, peak_kind, kernel="quant_dar"):
                 traffic = json.load(f).get(kernel, {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    return {"bound": "hbm", "kernel": kernel, "achieved": round(achieved, 1), "peak": peak, "peak_source": peak_kind,
-            "unit": "GB/s", "frac": round(achieved / peak, 4),
-            "algorithmic_bytes_per_launch": p["bytes"] / max(p["launches"], 1),
-            "avg_launch_ms": p["ms"] / max(p["launches"], 1), "launches": p["launches"], "traffic": traffic}
+    out = {"bound": "hbm", "kernel": kernel, "achieved": round(achieved, 1), "peak": peak, "peak_source": peak_kind,
+           "unit": "GB/s", "frac": round(achieved / peak, 4),
+           "algorithmic_bytes_per_launch": p["bytes"] / max(p["launches"], 1),
+           "avg_launch_ms": p["ms"] / max(p["launches"], 1), "launches": p["launches"], "traffic": traffic}
+    # the fused hop is integer-issue-bound: the issue-side numbers of the
+    # same kernel from the committed ncu capture
+    try:
+        with open(tpath) as f:
+            nc = json.load(f).get(kernel, {})
+        if "ipc" in nc:
+            out["issue"] = {"ipc": nc["ipc"], "max_ipc": 4.0, "alu_pipe_pct": nc.get("alu_pipe_pct"),
+                            "issue_active_pct": nc.get("issue_active_pct"), "source": "profiles/ncu_traffic.json"}
+    except Exception:
+        pass
+    return out
 
 
 def cpu_baseline(n, d_sample, budget, topology, sigma_log, steps=1):
