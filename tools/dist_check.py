@@ -35,12 +35,18 @@ def main():
     cases += [("butterfly", 1 << 24, 4.0, "peer"), ("butterfly", 3000, 6.0, "peer")]
     cases += [("ring", 1 << 24, 4.0, t) for t in only] + [("ring", 1 << 28, 4.0, t) for t in only]
     cases += [("ring", 3000, 6.0, "peer"), ("ring", 1 << 22, 2.6, "peer")]
+    cases = [c + ({},) for c in cases]
+    # ablation formats (generic kernels over NCCL) and the general allocator, on every rank
+    flat32 = {"group_size": 32, "hierarchical_scales": False}
+    cases += [("ring", 1 << 16, 5.0, "peer", flat32), ("butterfly", (1 << 18) + 77, 5.0, "peer", flat32),
+              ("ring", 1 << 16, 4.0, "peer", {"allocator": dq.KIND_GENERAL}),
+              ("ring", (1 << 20) + 5, 4.0, "peer", {"allocator": dq.KIND_GENERAL, "correlated": False})]
     comms = {}
-    for topo, d, b, transport in cases:
+    for topo, d, b, transport, extra in cases:
         if topo == "butterfly" and world & (world - 1):
             continue
         cfg = dq.PipelineConfig(n_workers=world, budget_bits=b, seed=dq.SharedSeed(3, 1),
-                                topology=dq.BUTTERFLY if topo == "butterfly" else dq.RING)
+                                topology=dq.BUTTERFLY if topo == "butterfly" else dq.RING, **extra)
         g = torch.Generator(device="cuda").manual_seed(7)
         T = (d + 255) // 256
         scale = torch.exp(4.0 * torch.randn(T, device="cuda", generator=g))
@@ -49,7 +55,7 @@ def main():
         if rank == 0 and os.environ.get("DIST_CHECK_VERBOSE"):
             print(f"case {topo} {transport} d={d} b={b}", file=sys.stderr, flush=True)
         # peer-transport contexts are reused across sizes and budgets (region regrowth, epochs)
-        key = (topo, transport, b)
+        key = (topo, transport, b, tuple(sorted(extra.items())))
         if key not in comms:
             comms[key] = dq.Communicator(cfg, rank, world, transport=transport)
         comm = comms[key]
@@ -70,12 +76,17 @@ def main():
             if d <= (1 << 16):
                 from oracle.oracle import Oracle
                 port = Oracle("port")
-                want = port.run_round([w.cpu().numpy() for w in ws], port.round_cfg(world, b, topo, seed=3, rnd=1))
+                okw = {"s": extra.get("group_size", 16), "hierarchical": extra.get("hierarchical_scales", True),
+                       "correlated": extra.get("correlated", True),
+                       "allocator": {0: "general", 1: "fast", 2: "fixed"}[extra.get("allocator", dq.KIND_FAST)]}
+                want = port.run_round([w.cpu().numpy() for w in ws],
+                                      port.round_cfg(world, b, topo, seed=3, rnd=1, **okw))
                 rec["match_oracle"] = bool(np.array_equal(out.cpu().numpy().view(np.uint32),
                                                           want["synced"].view(np.uint32)))
             ok &= all(v for k, v in rec.items() if k.startswith("match") or k in ("ranks_agree", "same_twice"))
             ok &= rec["transport"] == transport
-            results[f"{topo}_{transport}_d{d}_b{b}"] = rec
+            tag = "".join(f"_{k}{v}" for k, v in sorted(extra.items()))
+            results[f"{topo}_{transport}_d{d}_b{b}{tag}"] = rec
         dist.barrier()
     comms.clear()
     if rank == 0:
