@@ -26,3 +26,20 @@ def test_distributed_allreduce_matches_simulation():
     assert lines, r.stdout[-3000:] + r.stderr[-3000:]
     res = json.loads(lines[-1])
     assert res["ok"], json.dumps(res, indent=1)
+
+
+def test_back_to_back_async_rounds():
+    """24 all-reduces enqueued without host syncs (sizes alternate: region regrowth, epochs,
+    round parities) — every output bit-identical to the simulated round and across ranks."""
+    torch = pytest.importorskip("torch")
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    n = min(n, 8)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(ROOT, "tools", "dist_stress.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert lines, r.stdout[-3000:] + r.stderr[-3000:]
+    res = json.loads(lines[-1])
+    assert res["ok"], json.dumps(res, indent=1)
