@@ -178,6 +178,23 @@ struct PeerMem {
   size_t total() const { return flags() + 4 * cap_units * slots(); }
 };
 
+// Statistics exchange area of one rank (peer transport): per round parity the [n][T]
+// mean and sum-of-squares rows every rank stores its row into, then n row flags.
+struct StatsMem {
+  uint8_t* base = nullptr;
+  std::vector<uint8_t*> peer;
+  uint32_t n = 0, T = 0, epoch = 0;
+  size_t rows() const { return 4ull * n * T; }  // bytes of one [n][T] float array
+  float* mean(uint8_t* b, uint32_t par, uint32_t r) const {
+    return reinterpret_cast<float*>(b + 2ull * par * rows()) + static_cast<size_t>(r) * T;
+  }
+  float* sq(uint8_t* b, uint32_t par, uint32_t r) const {
+    return reinterpret_cast<float*>(b + (2ull * par + 1) * rows()) + static_cast<size_t>(r) * T;
+  }
+  uint32_t* flags(uint8_t* b, uint32_t par) const { return reinterpret_cast<uint32_t*>(b + 4 * rows()) + par * n; }
+  size_t total() const { return 4 * rows() + 2ull * n * sizeof(uint32_t); }
+};
+
 struct dq_ctx {
   dq_config cfg{};
   int device = 0;
@@ -230,15 +247,20 @@ struct dq_ctx {
   int pieces = 4;                       // pipeline pieces per chunk
   int transport = DQ_TRANSPORT_PEER;    // ring transport (butterfly always uses NCCL)
   PeerMem pm;
+  StatsMem sm;
+  DevBuf<unsigned int> sdone;           // fused stats all-gather: block completion counter
   DevBuf<uint8_t> ipc;                  // IPC handle exchange
-  void close_peers() {
-    for (size_t q = 0; q < pm.peer.size(); ++q)
-      if (pm.peer[q] && pm.peer[q] != pm.base) cudaIpcCloseMemHandle(pm.peer[q]);
-    pm.peer.clear();
+  static void close_map(std::vector<uint8_t*>& peer, const uint8_t* base) {
+    for (size_t q = 0; q < peer.size(); ++q)
+      if (peer[q] && peer[q] != base) cudaIpcCloseMemHandle(peer[q]);
+    peer.clear();
   }
+  void close_peers() { close_map(pm.peer, pm.base); }
   ~dq_ctx() {
     close_peers();
+    close_map(sm.peer, sm.base);
     if (pm.base) cudaFree(pm.base);
+    if (sm.base) cudaFree(sm.base);
     if (h_state) cudaFreeHost(h_state);
     if (h_counts) cudaFreeHost(h_counts);
     if (h_vn) cudaFreeHost(h_vn);
@@ -1096,9 +1118,54 @@ uint8_t* ring_pipelined(dq_ctx* ctx, const Prepared& pr, const std::vector<Codec
 // same round, after the stats all-gather has ordered all of every peer's previous
 // round (its last stores into this rank's region) before it.  If any rank cannot map
 // a peer, every rank falls back to the NCCL transport.
+// Export `base` by CUDA IPC and map every other rank's region (collective: one NCCL
+// all-gather of the 64-byte handles, then an all-reduce of the per-rank success so every
+// rank takes the same decision).  peer[me] = base.
+bool ipc_map(dq_ctx* ctx, uint8_t* base, std::vector<uint8_t*>& peer, cudaStream_t st) {
+  const uint32_t n = ctx->cfg.n_workers, me = static_cast<uint32_t>(ctx->rank);
+  ctx->ipc.reserve(static_cast<size_t>(n) * (sizeof(cudaIpcMemHandle_t) + 4));
+  cudaIpcMemHandle_t h;
+  DQ_CUDA(cudaIpcGetMemHandle(&h, base));
+  const size_t hs = sizeof(h);
+  DQ_CUDA(cudaMemcpyAsync(ctx->ipc.p + me * hs, &h, hs, cudaMemcpyHostToDevice, st));
+  DQ_NCCL(ncclAllGather(ctx->ipc.p + me * hs, ctx->ipc.p, hs, ncclUint8, ctx->comm, st));
+  std::vector<uint8_t> all(n * hs);
+  DQ_CUDA(cudaMemcpyAsync(all.data(), ctx->ipc.p, n * hs, cudaMemcpyDeviceToHost, st));
+  DQ_CUDA(cudaStreamSynchronize(st));
+  peer.assign(n, nullptr);
+  int ok = 1;
+  for (uint32_t q = 0; q < n; ++q) {
+    if (q == me) {
+      peer[q] = base;
+      continue;
+    }
+    cudaIpcMemHandle_t hq;
+    std::memcpy(&hq, all.data() + q * hs, hs);
+    void* ptr = nullptr;
+    if (cudaIpcOpenMemHandle(&ptr, hq, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      ok = 0;
+      break;
+    }
+    peer[q] = static_cast<uint8_t*>(ptr);
+  }
+  int* dok = reinterpret_cast<int*>(ctx->ipc.p + n * hs);
+  DQ_CUDA(cudaMemcpyAsync(dok, &ok, sizeof ok, cudaMemcpyHostToDevice, st));
+  DQ_NCCL(ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, ctx->comm, st));
+  DQ_CUDA(cudaMemcpyAsync(&ok, dok, sizeof ok, cudaMemcpyDeviceToHost, st));
+  DQ_CUDA(cudaStreamSynchronize(st));
+  if (!ok) dq_ctx::close_map(peer, base);
+  return ok != 0;
+}
+
+void peer_fallback(dq_ctx* ctx) {
+  ctx->transport = DQ_TRANSPORT_NCCL;
+  std::fprintf(stderr, "dynamiq_b200: peer mapping failed on some rank; using NCCL p2p\n");
+}
+
 bool peer_setup(dq_ctx* ctx, size_t mb, uint32_t max_nsg, uint32_t ninbox, cudaStream_t st) {
   PeerMem& pm = ctx->pm;
-  const uint32_t n = ctx->cfg.n_workers, me = static_cast<uint32_t>(ctx->rank);
+  const uint32_t n = ctx->cfg.n_workers;
   if (pm.base && pm.n == n && pm.ninbox == ninbox && mb <= pm.cap && max_nsg <= pm.cap_units) return true;
   DQ_CUDA(cudaStreamSynchronize(st));
   ctx->close_peers();
@@ -1110,46 +1177,40 @@ bool peer_setup(dq_ctx* ctx, size_t mb, uint32_t max_nsg, uint32_t ninbox, cudaS
   pm.cap_units = max_nsg + max_nsg / 4 + 64;
   DQ_CUDA(cudaMalloc(&pm.base, pm.total()));
   DQ_CUDA(cudaMemsetAsync(pm.base + pm.flags(), 0, pm.total() - pm.flags(), st));
-  ctx->ipc.reserve(static_cast<size_t>(n) * (sizeof(cudaIpcMemHandle_t) + 4));
-  cudaIpcMemHandle_t h;
-  DQ_CUDA(cudaIpcGetMemHandle(&h, pm.base));
-  const size_t hs = sizeof(h);
-  DQ_CUDA(cudaMemcpyAsync(ctx->ipc.p + me * hs, &h, hs, cudaMemcpyHostToDevice, st));
-  DQ_NCCL(ncclAllGather(ctx->ipc.p + me * hs, ctx->ipc.p, hs, ncclUint8, ctx->comm, st));
-  std::vector<uint8_t> all(n * hs);
-  DQ_CUDA(cudaMemcpyAsync(all.data(), ctx->ipc.p, n * hs, cudaMemcpyDeviceToHost, st));
-  DQ_CUDA(cudaStreamSynchronize(st));
-  if (old) DQ_CUDA(cudaFree(old));  // every rank closed its mapping before the all-gather
-  pm.peer.assign(n, nullptr);
-  int ok = 1;
-  for (uint32_t q = 0; q < n; ++q) {
-    if (q == me) {
-      pm.peer[q] = pm.base;
-      continue;
-    }
-    cudaIpcMemHandle_t hq;
-    std::memcpy(&hq, all.data() + q * hs, hs);
-    void* ptr = nullptr;
-    if (cudaIpcOpenMemHandle(&ptr, hq, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-      cudaGetLastError();
-      ok = 0;
-      break;
-    }
-    pm.peer[q] = static_cast<uint8_t*>(ptr);
-  }
-  int* dok = reinterpret_cast<int*>(ctx->ipc.p + n * hs);
-  DQ_CUDA(cudaMemcpyAsync(dok, &ok, sizeof ok, cudaMemcpyHostToDevice, st));
-  DQ_NCCL(ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, ctx->comm, st));
-  DQ_CUDA(cudaMemcpyAsync(&ok, dok, sizeof ok, cudaMemcpyDeviceToHost, st));
-  DQ_CUDA(cudaStreamSynchronize(st));
+  const bool ok = ipc_map(ctx, pm.base, pm.peer, st);
+  if (old) DQ_CUDA(cudaFree(old));  // every rank closed its mapping of it before the handle all-gather
   if (!ok) {
-    ctx->close_peers();
     DQ_CUDA(cudaFree(pm.base));
     pm.base = nullptr;
-    ctx->transport = DQ_TRANSPORT_NCCL;
-    std::fprintf(stderr, "dynamiq_b200: peer mapping failed on some rank; ring uses NCCL p2p\n");
+    peer_fallback(ctx);
   }
-  return ok != 0;
+  return ok;
+}
+
+// The statistics exchange area (collective, same decision on every rank: T and n are
+// round-global).  Rebuilt when T or n changes.
+bool stats_setup(dq_ctx* ctx, uint32_t T, cudaStream_t st) {
+  StatsMem& sm = ctx->sm;
+  const uint32_t n = ctx->cfg.n_workers;
+  if (sm.base && sm.n == n && sm.T == T) return true;
+  DQ_CUDA(cudaStreamSynchronize(st));
+  dq_ctx::close_map(sm.peer, sm.base);
+  uint8_t* old = sm.base;
+  sm.base = nullptr;
+  sm.n = n;
+  sm.T = T;
+  DQ_CUDA(cudaMalloc(&sm.base, sm.total()));
+  DQ_CUDA(cudaMemsetAsync(sm.base + 4 * sm.rows(), 0, sm.total() - 4 * sm.rows(), st));
+  ctx->sdone.reserve(1);
+  DQ_CUDA(cudaMemsetAsync(ctx->sdone.p, 0, sizeof(unsigned int), st));
+  const bool ok = ipc_map(ctx, sm.base, sm.peer, st);
+  if (old) DQ_CUDA(cudaFree(old));
+  if (!ok) {
+    DQ_CUDA(cudaFree(sm.base));
+    sm.base = nullptr;
+    peer_fallback(ctx);
+  }
+  return ok;
 }
 
 // Ring over peer memory: at hop h rank r runs the fused kernel on chunk r-1-h, reading
@@ -1344,18 +1405,41 @@ void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info
   reserve_round(ctx, T, n);
   ctx->xptrs.reserve(1);
   DQ_CUDA(cudaMemcpyAsync(ctx->xptrs.p, &x, sizeof(float*), cudaMemcpyHostToDevice, st));
-  // (a) local stats into this rank's row, (b) all-gather rows, fixed-order fp64 reduce (H4)
-  float* my_mean = ctx->mean_all.p + static_cast<size_t>(me) * T;
-  float* my_sq = ctx->sq_all.p + static_cast<size_t>(me) * T;
-  timed(ctx, K_STATS, 4.0 * d + 8.0 * T, st, [&] { launch_stats(ctx->xptrs.p, 1, d, T, my_mean, my_sq, st); });
-  timed(ctx, K_NCCL, 8.0 * T * n, st, [&] {
-    DQ_NCCL(ncclGroupStart());
-    DQ_NCCL(ncclAllGather(my_mean, ctx->mean_all.p, T, ncclFloat, ctx->comm, st));
-    DQ_NCCL(ncclAllGather(my_sq, ctx->sq_all.p, T, ncclFloat, ctx->comm, st));
-    DQ_NCCL(ncclGroupEnd());
-  });
-  timed(ctx, K_REDUCE, 8.0 * (n + 1) * T, st,
-        [&] { launch_reduce_stats(ctx->mean_all.p, ctx->sq_all.p, n, T, ctx->gmean.p, ctx->gsq.p, st); });
+  // (a) local stats into this rank's row, (b) all-gather rows, fixed-order fp64 reduce (H4).
+  // Peer transport: the all-gather is fused into the statistics kernel (each block stores
+  // its rows into every rank's exchange area over NVLink, the last block raises the row
+  // flags) and the reduction waits for all rows' flags; this also orders every peer's
+  // previous round before any store of this round into its regions.
+  if (ctx->transport == DQ_TRANSPORT_PEER && n <= static_cast<uint32_t>(kMaxPeers) && stats_setup(ctx, T, st)) {
+    StatsMem& sm = ctx->sm;
+    const uint32_t ep = ++sm.epoch, par = ep & 1u;
+    StatsPeerArgs sp{};
+    for (uint32_t q = 0; q < n; ++q) {
+      sp.mean[q] = sm.mean(sm.peer[q], par, me);
+      sp.sq[q] = sm.sq(sm.peer[q], par, me);
+      sp.flag[q] = sm.flags(sm.peer[q], par) + me;
+    }
+    sp.done = ctx->sdone.p;
+    sp.n = n;
+    sp.epoch = ep;
+    timed(ctx, K_STATS, 4.0 * d + 8.0 * T * n, st, [&] { launch_stats_peer(ctx->xptrs.p, d, T, sp, st); });
+    timed(ctx, K_REDUCE, 8.0 * (n + 1) * T, st, [&] {
+      launch_reduce_stats_peer(sm.mean(sm.base, par, 0), sm.sq(sm.base, par, 0), sm.flags(sm.base, par), ep, n, T,
+                               ctx->gmean.p, ctx->gsq.p, st);
+    });
+  } else {
+    float* my_mean = ctx->mean_all.p + static_cast<size_t>(me) * T;
+    float* my_sq = ctx->sq_all.p + static_cast<size_t>(me) * T;
+    timed(ctx, K_STATS, 4.0 * d + 8.0 * T, st, [&] { launch_stats(ctx->xptrs.p, 1, d, T, my_mean, my_sq, st); });
+    timed(ctx, K_NCCL, 8.0 * T * n, st, [&] {
+      DQ_NCCL(ncclGroupStart());
+      DQ_NCCL(ncclAllGather(my_mean, ctx->mean_all.p, T, ncclFloat, ctx->comm, st));
+      DQ_NCCL(ncclAllGather(my_sq, ctx->sq_all.p, T, ncclFloat, ctx->comm, st));
+      DQ_NCCL(ncclGroupEnd());
+    });
+    timed(ctx, K_REDUCE, 8.0 * (n + 1) * T, st,
+          [&] { launch_reduce_stats(ctx->mean_all.p, ctx->sq_all.p, n, T, ctx->gmean.p, ctx->gsq.p, st); });
+  }
   DQ_CUDA(cudaGetLastError());
   Prepared p = prepare(ctx, T, st);
   fill_info_alloc(info, p);

@@ -87,6 +87,20 @@ void launch_selftest(int which, uint64_t n, uint64_t seed, unsigned long long* b
 // (pointer array in device memory) -> mean[w * T + j], sq[w * T + j]
 void launch_stats(const float* const* xs, uint32_t n_workers, uint64_t d, uint32_t T, float* mean,
                   float* sq, cudaStream_t st);
+// Statistics all-gather fused into the statistics kernel (peer transport): row `me` of
+// every rank's area (mean[r], sq[r] = peer pointers), completion flags flag[r] (row me
+// on rank r) set to epoch by the last block; done = local block-completion counter.
+struct StatsPeerArgs {
+  float* mean[kMaxPeers];
+  float* sq[kMaxPeers];
+  uint32_t* flag[kMaxPeers];
+  unsigned int* done;
+  uint32_t n, epoch;
+};
+void launch_stats_peer(const float* const* xs, uint64_t d, uint32_t T, const StatsPeerArgs& sp, cudaStream_t st);
+// reduction of the fused all-gather's rows after waiting for all n row flags == epoch
+void launch_reduce_stats_peer(const float* mean, const float* sq, const uint32_t* flags, uint32_t epoch,
+                              uint32_t n, uint32_t T, float* gm, float* gs, cudaStream_t st);
 // rank-ordered fp64 reduction of [n][T] stats -> global [T]
 void launch_reduce_stats(const float* mean, const float* sq, uint32_t n, uint32_t T, float* gmean,
                          float* gsq, cudaStream_t st);

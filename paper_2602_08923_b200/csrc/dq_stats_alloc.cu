@@ -31,8 +31,13 @@ namespace dq {
 // ------------------------------------------------------------ statistics
 constexpr int kStatSG = 128;
 
+// PEER: the statistics all-gather fused into the kernel — every block stores its
+// super-groups' (mean, sq) into row `me` of every rank's statistics area over NVLink;
+// the last block to finish (system-scope fences before the completion count) raises
+// row me's flag on every rank.  The reduction waits for all rows' flags.
+template <bool PEER>
 __global__ void __launch_bounds__(kStatSG) k_stats(const float* const* xs, uint64_t d, uint32_t T,
-                                                   float* mean, float* sq) {
+                                                   float* mean, float* sq, StatsPeerArgs sp) {
   __shared__ float tile[kStatSG][33];
   const float* __restrict__ x = xs[blockIdx.y];
   const uint32_t sg0 = blockIdx.x * kStatSG;
@@ -59,16 +64,45 @@ __global__ void __launch_bounds__(kStatSG) k_stats(const float* const* xs, uint6
     __syncthreads();
   }
   const uint32_t sg = sg0 + threadIdx.x;
-  if (sg < T) {
-    mean[static_cast<uint64_t>(blockIdx.y) * T + sg] = static_cast<float>(__ddiv_rn(s, static_cast<double>(kS)));
-    sq[static_cast<uint64_t>(blockIdx.y) * T + sg] = static_cast<float>(q);
+  if constexpr (!PEER) {
+    if (sg < T) {
+      mean[static_cast<uint64_t>(blockIdx.y) * T + sg] = static_cast<float>(__ddiv_rn(s, static_cast<double>(kS)));
+      sq[static_cast<uint64_t>(blockIdx.y) * T + sg] = static_cast<float>(q);
+    }
+  } else {
+    if (sg < T) {
+      const float mv = static_cast<float>(__ddiv_rn(s, static_cast<double>(kS))), qv = static_cast<float>(q);
+      for (uint32_t r = 0; r < sp.n; ++r) {
+        sp.mean[r][sg] = mv;
+        sp.sq[r][sg] = qv;
+      }
+    }
+    __syncthreads();
+    __shared__ unsigned int last;
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      last = atomicAdd(sp.done, 1u) == gridDim.x - 1 ? 1u : 0u;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+      *sp.done = 0;  // reset for the next round (stream-ordered before its stats kernel)
+      __threadfence_system();
+      for (uint32_t r = 0; r < sp.n; ++r)
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(sp.flag[r]), "r"(sp.epoch) : "memory");
+    }
   }
 }
 
 void launch_stats(const float* const* xs, uint32_t n_workers, uint64_t d, uint32_t T, float* mean,
                   float* sq, cudaStream_t st) {
   if (T == 0) return;
-  k_stats<<<dim3((T + kStatSG - 1) / kStatSG, n_workers), kStatSG, 0, st>>>(xs, d, T, mean, sq);
+  k_stats<false><<<dim3((T + kStatSG - 1) / kStatSG, n_workers), kStatSG, 0, st>>>(xs, d, T, mean, sq,
+                                                                                    StatsPeerArgs{});
+}
+
+void launch_stats_peer(const float* const* xs, uint64_t d, uint32_t T, const StatsPeerArgs& sp, cudaStream_t st) {
+  if (T == 0) return;
+  k_stats<true><<<dim3((T + kStatSG - 1) / kStatSG, 1), kStatSG, 0, st>>>(xs, d, T, nullptr, nullptr, sp);
 }
 
 __global__ void k_reduce_stats(const float* mean, const float* sq, uint32_t n, uint32_t T,
@@ -88,6 +122,45 @@ void launch_reduce_stats(const float* mean, const float* sq, uint32_t n, uint32_
                          float* gs, cudaStream_t st) {
   if (T == 0) return;
   k_reduce_stats<<<(T + 255) / 256, 256, 0, st>>>(mean, sq, n, T, gm, gs);
+}
+
+// The rank-ordered reduction over the fused all-gather's rows: each block first waits
+// (thread 0, acquire at system scope, 20 s timeout -> trap) for every row's flag.
+__global__ void k_reduce_stats_peer(const float* mean, const float* sq, const uint32_t* flags, uint32_t epoch,
+                                    uint32_t n, uint32_t T, float* gm, float* gs) {
+  if (threadIdx.x == 0) {
+    for (uint32_t r = 0; r < n; ++r) {
+      uint32_t v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + r) : "memory");
+      if (v == epoch) continue;
+      uint64_t t0;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      for (;;) {
+        __nanosleep(64);
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + r) : "memory");
+        if (v == epoch) break;
+        uint64_t t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        if (t1 - t0 > 20ull * 1000 * 1000 * 1000) __trap();
+      }
+    }
+  }
+  __syncthreads();
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= T) return;
+  double a = 0.0, b = 0.0;
+  for (uint32_t r = 0; r < n; ++r) {
+    a = __dadd_rn(a, static_cast<double>(__ldcg(mean + static_cast<uint64_t>(r) * T + j)));
+    b = __dadd_rn(b, static_cast<double>(__ldcg(sq + static_cast<uint64_t>(r) * T + j)));
+  }
+  gm[j] = static_cast<float>(__ddiv_rn(a, static_cast<double>(n)));
+  gs[j] = static_cast<float>(b);
+}
+
+void launch_reduce_stats_peer(const float* mean, const float* sq, const uint32_t* flags, uint32_t epoch,
+                              uint32_t n, uint32_t T, float* gm, float* gs, cudaStream_t st) {
+  if (T == 0) return;
+  k_reduce_stats_peer<<<(T + 255) / 256, 256, 0, st>>>(mean, sq, flags, epoch, n, T, gm, gs);
 }
 
 // ------------------------------------------------------------ allocation
