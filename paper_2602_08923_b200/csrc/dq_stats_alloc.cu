@@ -40,43 +40,50 @@ __global__ void __launch_bounds__(kStatSG) k_stats(const float* const* xs, uint6
                                                    float* mean, float* sq, StatsPeerArgs sp) {
   __shared__ float tile[kStatSG][33];
   const float* __restrict__ x = xs[blockIdx.y];
-  const uint32_t sg0 = blockIdx.x * kStatSG;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double s = 0.0, q = 0.0;
+  // PEER: a persistent grid walks the tiles, so the one system-scope fence per block
+  // before the completion count is amortised over many tiles
+  const uint32_t ntiles = (T + kStatSG - 1) / kStatSG;
+  for (uint32_t tile_i = blockIdx.x; tile_i < ntiles; tile_i += PEER ? gridDim.x : ntiles) {
+    const uint32_t sg0 = tile_i * kStatSG;
+    double s = 0.0, q = 0.0;
 #pragma unroll 1
-  for (int part = 0; part < kS / 32; ++part) {
-    float v[32];
+    for (int part = 0; part < kS / 32; ++part) {
+      float v[32];
 #pragma unroll
-    for (int r = 0; r < 32; ++r) {
-      const uint32_t sg = sg0 + warp * 32 + r;
-      const uint64_t idx = static_cast<uint64_t>(sg) * kS + part * 32 + lane;
-      v[r] = (sg < T && idx < d) ? __ldcs(x + idx) : 0.0f;  // streaming: read once
-    }
+      for (int r = 0; r < 32; ++r) {
+        const uint32_t sg = sg0 + warp * 32 + r;
+        const uint64_t idx = static_cast<uint64_t>(sg) * kS + part * 32 + lane;
+        v[r] = (sg < T && idx < d) ? __ldcs(x + idx) : 0.0f;  // streaming: read once
+      }
 #pragma unroll
-    for (int r = 0; r < 32; ++r) tile[warp * 32 + r][lane] = v[r];
-    __syncthreads();
+      for (int r = 0; r < 32; ++r) tile[warp * 32 + r][lane] = v[r];
+      __syncthreads();
 #pragma unroll
-    for (int k = 0; k < 32; ++k) {
-      const double t = tile[threadIdx.x][k];
-      s = __dadd_rn(s, t);
-      q = __dadd_rn(q, __dmul_rn(t, t));
+      for (int k = 0; k < 32; ++k) {
+        const double t = tile[threadIdx.x][k];
+        s = __dadd_rn(s, t);
+        q = __dadd_rn(q, __dmul_rn(t, t));
+      }
+      __syncthreads();
     }
-    __syncthreads();
-  }
-  const uint32_t sg = sg0 + threadIdx.x;
-  if constexpr (!PEER) {
-    if (sg < T) {
-      mean[static_cast<uint64_t>(blockIdx.y) * T + sg] = static_cast<float>(__ddiv_rn(s, static_cast<double>(kS)));
-      sq[static_cast<uint64_t>(blockIdx.y) * T + sg] = static_cast<float>(q);
-    }
-  } else {
-    if (sg < T) {
-      const float mv = static_cast<float>(__ddiv_rn(s, static_cast<double>(kS))), qv = static_cast<float>(q);
-      for (uint32_t r = 0; r < sp.n; ++r) {
-        sp.mean[r][sg] = mv;
-        sp.sq[r][sg] = qv;
+    const uint32_t sg = sg0 + threadIdx.x;
+    if constexpr (!PEER) {
+      if (sg < T) {
+        mean[static_cast<uint64_t>(blockIdx.y) * T + sg] = static_cast<float>(__ddiv_rn(s, static_cast<double>(kS)));
+        sq[static_cast<uint64_t>(blockIdx.y) * T + sg] = static_cast<float>(q);
+      }
+    } else {
+      if (sg < T) {
+        const float mv = static_cast<float>(__ddiv_rn(s, static_cast<double>(kS))), qv = static_cast<float>(q);
+        for (uint32_t r = 0; r < sp.n; ++r) {
+          sp.mean[r][sg] = mv;
+          sp.sq[r][sg] = qv;
+        }
       }
     }
+  }
+  if constexpr (PEER) {
     __syncthreads();
     __shared__ unsigned int last;
     if (threadIdx.x == 0) {
@@ -102,7 +109,8 @@ void launch_stats(const float* const* xs, uint32_t n_workers, uint64_t d, uint32
 
 void launch_stats_peer(const float* const* xs, uint64_t d, uint32_t T, const StatsPeerArgs& sp, cudaStream_t st) {
   if (T == 0) return;
-  k_stats<true><<<dim3((T + kStatSG - 1) / kStatSG, 1), kStatSG, 0, st>>>(xs, d, T, nullptr, nullptr, sp);
+  const uint32_t ntiles = (T + kStatSG - 1) / kStatSG, cap = 148u * 12;  // ~12 resident 128-thread CTAs per SM
+  k_stats<true><<<dim3(ntiles < cap ? ntiles : cap, 1), kStatSG, 0, st>>>(xs, d, T, nullptr, nullptr, sp);
 }
 
 __global__ void k_reduce_stats(const float* mean, const float* sq, uint32_t n, uint32_t T,
