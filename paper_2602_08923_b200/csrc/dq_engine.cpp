@@ -532,11 +532,6 @@ AllocResult allocate_fast(dq_ctx* ctx, const dq_config& c, const float* dF, uint
   // Re-derive every candidate with the host libm exactly as fast_sample_points /
   // fast_threshold_* do (allocation.cpp:170-224).  Identical thresholds => identical
   // float-threshold counts => the device's choice is the reference's.
-  auto hflip = [](const FlipRec& r) {
-    float f;
-    std::memcpy(&f, &r.fbits, 4);
-    return (r.type ? 8.0 : 4.0) - kAlpha * std::log2(static_cast<double>(f));
-  };
   struct Sample {
     bool has_l = false, has_r = false;
     FlipRec l{}, r{};
@@ -550,7 +545,6 @@ AllocResult allocate_fast(dq_ctx* ctx, const dq_config& c, const float* dF, uint
       return (q.type ? 8.0 : 4.0) - kAlpha * std::log2(static_cast<double>(f));
     }
   };
-  (void)hflip;
   auto thr = [](double uu, float* a, float* b) {
     *a = static_cast<float>(std::exp2((4.0 - uu) / kAlpha));
     *b = static_cast<float>(std::exp2((8.0 - uu) / kAlpha));
