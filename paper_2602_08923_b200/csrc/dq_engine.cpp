@@ -838,6 +838,7 @@ void sim_round(dq_ctx* ctx, const float* const* xs, size_t d, float* out, int fl
   const size_t mb = p.max_chunk_bytes;
   ctx->msgs.reserve((n + 2 + n) * mb);
   std::vector<int> gslots(n, -1);
+  std::vector<char> decoded(n, 0);  // chunk decoded into `out` by its fused sink
   uint32_t max_nsg = 0;
   for (uint32_t i = 0; i < n; ++i) max_nsg = std::max(max_nsg, p.lo[i + 1] - p.lo[i]);
   const bool need_acc = c.topology == DQ_BUTTERFLY;
@@ -928,8 +929,13 @@ void sim_round(dq_ctx* ctx, const float* const* xs, size_t d, float* out, int fl
           g.pcache = ctx->pcache.p;
           g.pc_mode = 2;
         }
+        g.dec_out = out;  // fused decode of the chunk into the output where a variant exists
+        decoded[ch] = launch_quant_dec(g, gsrc, false, st, false);
         const double pcb = use_pc && gsrc == 0 ? 256.0 * pc_bytes * L.nsg : 0.0;
-        timed(ctx, K_DAR, quant_bytes(L, true) + pcb, st, [&] { launch_quant(g, gsrc, true, st); });
+        timed(ctx, K_DAR, quant_bytes(L, true) + pcb + (decoded[ch] ? 1032.0 * L.nsg : 0.0), st, [&] {
+          if (!decoded[ch]) launch_quant(g, gsrc, true, st);
+          else launch_quant_dec(g, gsrc, false, st);
+        });
         free_slots.push_back(os);
         gather_slot = gs;
       } else {
@@ -951,28 +957,31 @@ void sim_round(dq_ctx* ctx, const float* const* xs, size_t d, float* out, int fl
     H ^= hsh + 0x9e3779b97f4a7c15ULL + (H << 6) + (H >> 2);
   }
   if (collect_wire) info->wire_hash = H;
-  {
+  {  // the chunks whose sink had no fused decode
     GatherArgs g{};
     set_format(g, ctx->cfg);
-    uint32_t max_nsg_g = 0;
+    g.use_hi = 1;
+    uint32_t max_nsg_g = 0, k = 0;
+    double gbytes = 0;
     for (uint32_t ch = 0; ch < n; ++ch) {
+      if (decoded[ch]) continue;
       const Layout L = chunk_layout(p.a, p.lo[ch], p.lo[ch + 1]);
-      g.in[ch] = ctx->msgs.p + static_cast<size_t>(gslots[ch]) * mb;
-      g.lo[ch] = p.lo[ch];
-      g.n8[ch] = L.n8;
-      g.n4[ch] = L.n4;
+      g.in[k] = ctx->msgs.p + static_cast<size_t>(gslots[ch]) * mb;
+      g.lo[k] = p.lo[ch];
+      g.hi[k] = p.lo[ch + 1];
+      g.n8[k] = L.n8;
+      g.n4[k] = L.n4;
       max_nsg_g = std::max(max_nsg_g, L.nsg);
+      gbytes += 1032.0 * L.nsg + L.bytes();
+      ++k;
     }
-    g.lo[n] = p.lo[n];
     g.perm = ctx->perm.p;
     g.gmean = ctx->pmean.p;
     g.out = out;
     g.d = d;
     g.n_workers_f = static_cast<float>(n);
     g.uniform_books = c.non_uniform ? 0 : 1;
-    double gbytes = 0;
-    for (uint32_t ch = 0; ch < n; ++ch) gbytes += 1032.0 * (p.lo[ch + 1] - p.lo[ch]) + chunk_layout(p.a, p.lo[ch], p.lo[ch + 1]).bytes();
-    timed(ctx, K_DECODE, gbytes, st, [&] { launch_gather_decode(g, n, max_nsg_g, st); });
+    if (k) timed(ctx, K_DECODE, gbytes, st, [&] { launch_gather_decode(g, k, max_nsg_g, st); });
     DQ_CUDA(cudaGetLastError());
   }
   DQ_CUDA(cudaEventRecord(ctx->ev1, st));
@@ -1214,8 +1223,15 @@ bool stats_setup(dq_ctx* ctx, uint32_t T, cudaStream_t st) {
 // ranks therefore overlap at unit granularity.  The sink (hop n-1) stores its chunk
 // into gather slot r of every rank - the all-gather - and one decode launch per rank
 // consumes all n gather slots as their units land.
-void peer_gather_decode(dq_ctx* ctx, const Prepared& p, const std::vector<Layout>& lays, float* out, size_t d,
-                        uint32_t epoch, cudaStream_t st);
+void peer_gather_decode(dq_ctx* ctx, const Prepared& p, const std::vector<Layout>& lays,
+                        const std::vector<char>& decoded, float* out, size_t d, uint32_t epoch, cudaStream_t st);
+
+// Fused own-chunk decode in the peer sinks (launch_quant_dec) only up to this many ranks.
+// Measured at d = 2^28 per rank (profiles/r1_multi_gpu.md): N = 2 the gather decode is
+// HBM-bound and fusing saves 0.07 ms per round (2.73 -> 2.65 ms); N = 4 the gather decode
+// is paced by the remote sinks' arrival, the own chunk's decode hides inside that wait,
+// and the longer sink costs 0.05 ms (3.15 -> 3.20 ms ring, 3.32 -> 3.36 butterfly).
+constexpr uint32_t kFuseDecodeMaxRanks = 2;
 
 void ring_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>& bases,
                const std::vector<Layout>& lays, float* out, size_t d, cudaStream_t st) {
@@ -1223,6 +1239,7 @@ void ring_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>& bas
   const uint32_t right = (me + 1) % n;
   PeerMem& pm = ctx->pm;
   const uint32_t epoch = ++pm.epoch, par = epoch & 1u;
+  std::vector<char> decoded(n, 0);
   for (uint32_t h = 0; h < n; ++h) {
     const uint32_t ch = (me + 2 * n - 1 - h) % n;  // sink at h = n-1
     CodecArgs a = bases[ch];
@@ -1246,33 +1263,46 @@ void ring_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>& bas
       a.n_outs = static_cast<int>(n);
     }
     const bool dar = h > 0;
-    timed(ctx, dar ? K_DAR : K_LEAF, quant_bytes(lays[ch], dar), st, [&] { launch_quant_peer(a, 0, dar, st); });
+    if (h + 1 == n && n <= kFuseDecodeMaxRanks) {  // the sink also decodes its record into the output
+      a.dec_out = out;
+      decoded[ch] = launch_quant_dec(a, 0, true, st, false);
+    }
+    const double ob = decoded[ch] ? 1032.0 * lays[ch].nsg : 0.0;
+    timed(ctx, dar ? K_DAR : K_LEAF, quant_bytes(lays[ch], dar) + ob, st, [&] {
+      if (!decoded[ch]) launch_quant_peer(a, 0, dar, st);
+      else launch_quant_dec(a, 0, true, st);
+    });
   }
-  peer_gather_decode(ctx, p, lays, out, d, epoch, st);
+  peer_gather_decode(ctx, p, lays, decoded, out, d, epoch, st);
 }
 
-// Every rank decodes all n gather slots of this round's parity into the output, unit by
-// unit as the sinks' stores land (its own slot is complete: its sink ran earlier on st).
-void peer_gather_decode(dq_ctx* ctx, const Prepared& p, const std::vector<Layout>& lays, float* out, size_t d,
-                        uint32_t epoch, cudaStream_t st) {
+// Every rank decodes the n gather slots of this round's parity into the output, unit by
+// unit as the sinks' stores land (its own slot is complete: its sink ran earlier on st),
+// except the chunks its own sink already decoded (decoded[c], launch_quant_dec).
+void peer_gather_decode(dq_ctx* ctx, const Prepared& p, const std::vector<Layout>& lays,
+                        const std::vector<char>& decoded, float* out, size_t d, uint32_t epoch, cudaStream_t st) {
   const uint32_t n = ctx->cfg.n_workers, me = static_cast<uint32_t>(ctx->rank);
   const uint32_t par = epoch & 1u;
   PeerMem& pm = ctx->pm;
   GatherArgs g{};
   set_format(g, ctx->cfg);
-  uint32_t max_nsg = 0;
+  g.use_hi = 1;
+  uint32_t max_nsg = 0, k = 0;
   double gbytes = 0;
   for (uint32_t c = 0; c < n; ++c) {
-    g.in[c] = pm.base + pm.gather(par, c);
-    g.lo[c] = p.lo[c];
-    g.n8[c] = lays[c].n8;
-    g.n4[c] = lays[c].n4;
-    g.flags[c] = c == me ? nullptr : reinterpret_cast<const uint32_t*>(pm.base + pm.gflag(par, c));
-    g.unit[c] = peer_unit(lays[c].nsg);
+    if (decoded[c]) continue;
+    g.in[k] = pm.base + pm.gather(par, c);
+    g.lo[k] = p.lo[c];
+    g.hi[k] = p.lo[c + 1];
+    g.n8[k] = lays[c].n8;
+    g.n4[k] = lays[c].n4;
+    g.flags[k] = c == me ? nullptr : reinterpret_cast<const uint32_t*>(pm.base + pm.gflag(par, c));
+    g.unit[k] = peer_unit(lays[c].nsg);
     max_nsg = std::max(max_nsg, lays[c].nsg);
     gbytes += 1032.0 * lays[c].nsg + lays[c].bytes();
+    ++k;
   }
-  g.lo[n] = p.lo[n];
+  if (!k) return;
   g.epoch = epoch;
   g.perm = ctx->perm.p;
   g.gmean = ctx->pmean.p;
@@ -1280,7 +1310,7 @@ void peer_gather_decode(dq_ctx* ctx, const Prepared& p, const std::vector<Layout
   g.d = d;
   g.n_workers_f = static_cast<float>(n);
   g.uniform_books = ctx->cfg.non_uniform ? 0 : 1;
-  timed(ctx, K_DECODE, gbytes, st, [&] { launch_gather_decode(g, n, max_nsg, st); });
+  timed(ctx, K_DECODE, gbytes, st, [&] { launch_gather_decode(g, k, max_nsg, st); });
 }
 
 // halving stage of a butterfly reduce event (topology.cpp:46-54): partner bit n >> (stage + 1)
@@ -1308,7 +1338,7 @@ void butterfly_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>
   ctx->accs.reserve(static_cast<size_t>(n) * max_nsg * 256);
   auto acc_ptr = [&](uint32_t ch) { return ctx->accs.p + static_cast<size_t>(ch) * max_nsg * 256; };
   std::vector<int> held(n, -1);
-  std::vector<char> has_acc(n, 0);
+  std::vector<char> has_acc(n, 0), decoded(n, 0);
   auto prep = [&](uint32_t ch) {
     CodecArgs a = bases[ch];
     a.unit = peer_unit(lays[ch].nsg);
@@ -1365,7 +1395,13 @@ void butterfly_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>
             a.out_flags[j] = reinterpret_cast<uint32_t*>(pm.peer[q] + pm.gflag(par, ch));
           }
           a.n_outs = static_cast<int>(n);
-          timed(ctx, K_DAR, quant_bytes(lays[ch], true), st, [&] { launch_quant_peer(a, src, true, st); });
+          if (n <= kFuseDecodeMaxRanks) a.dec_out = out;  // and decoded into this rank's output
+          decoded[ch] = launch_quant_dec(a, src, true, st, false);
+          const double ob = decoded[ch] ? 1032.0 * lays[ch].nsg : 0.0;
+          timed(ctx, K_DAR, quant_bytes(lays[ch], true) + ob, st, [&] {
+            if (!decoded[ch]) launch_quant_peer(a, src, true, st);
+            else launch_quant_dec(a, src, true, st);
+          });
         } else {
           a.acc_out = acc_ptr(ch);
           timed(ctx, K_DA, 2048.0 * lays[ch].nsg + lays[ch].bytes(), st, [&] { launch_da_peer(a, src, st); });
@@ -1374,7 +1410,7 @@ void butterfly_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>
       }
     }
   }
-  peer_gather_decode(ctx, p, lays, out, d, epoch, st);
+  peer_gather_decode(ctx, p, lays, decoded, out, d, epoch, st);
 }
 
 void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info* info, cudaStream_t st) {

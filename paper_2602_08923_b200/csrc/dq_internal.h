@@ -41,6 +41,10 @@ struct CodecArgs {
   // (u8 per entry for n <= 4, u32 for n <= 8); pc_mode 1 = compute + store, 2 = read
   uint8_t* pcache;
   int pc_mode;
+  // sink DAR only (launch_quant_dec): also decode the finished record into the output
+  // gradient (unpermute + denormalize through perm / gmean / n_workers_f / d), i.e. the
+  // gather decode of this chunk fused into the hop that produces it
+  float* dec_out;
 };
 
 // All chunks of a round decoded into the output gradient in one launch.
@@ -73,6 +77,11 @@ void launch_from_wire(const uint8_t* in, const Layout& L, uint32_t fit, uint8_t*
                       cudaStream_t st);
 // one hop over peer memory (src 0: raw gradient, 1: acc_in); see CodecArgs peer fields
 void launch_quant_peer(const CodecArgs& a, int src, bool dar, cudaStream_t st);
+// Sink DAR with the chunk's decode fused in (a.dec_out); peer = k_quant_peer, else the
+// simulated round's permutation-cache kernel.  Returns false (nothing launched) when the
+// configuration has no fused variant: the caller runs the plain sink + gather decode.
+// launch = false: only report whether a fused variant exists.
+bool launch_quant_dec(const CodecArgs& a, int src, bool peer, cudaStream_t st, bool launch = true);
 // decompress-accumulate of a peer-delivered message (waits per unit) into acc_out
 void launch_da_peer(const CodecArgs& a, int src, cudaStream_t st);
 uint32_t peer_unit(uint32_t nsg);  // super-groups per flag unit of a chunk (same on every rank)
