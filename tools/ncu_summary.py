@@ -23,7 +23,8 @@ def family(name: str) -> str:
     if n.startswith("k_quant"):
         tmpl = name[name.find("<") + 1:name.find(">")]
         parts = [p.strip() for p in tmpl.split(",")]
-        return f"k_quant<NS={parts[0]},DAR={parts[3] if len(parts) > 3 else '?'}>"
+        dec = ",DEC" if len(parts) > 6 and parts[6] in ("1", "true") else ""
+        return f"k_quant<NS={parts[0]},DAR={parts[3] if len(parts) > 3 else '?'}{dec}>"
     return n
 
 
