@@ -12,6 +12,12 @@ template <int NS, bool CORR>
 void launch_peer_dec(const CodecArgs& a, int src, cudaStream_t st) {
   const uint32_t units = (a.L.nsg + a.unit - 1) / a.unit;
   const dim3 grid(persistent_grid(units, 64));
+  if constexpr (CORR && NS >= 2) {
+    if (a.pc_mode == 4 && src == 0) {  // ring sink reading its permutation slice
+      k_quant_peer<NS, true, 0, true, true, 4><<<grid, kThreads, 0, st>>>(a);
+      return;
+    }
+  }
   if (src == 0) k_quant_peer<NS, CORR, 0, true, true><<<grid, kThreads, 0, st>>>(a);
   else k_quant_peer<NS, CORR, 1, true, true><<<grid, kThreads, 0, st>>>(a);
 }

@@ -8,6 +8,16 @@ template <int NS, bool CORR>
 void launch_peer_ns(const CodecArgs& a, int src, bool dar, cudaStream_t st) {
   const uint32_t units = (a.L.nsg + a.unit - 1) / a.unit;
   const dim3 grid(persistent_grid(units, 64));  // one unit per warp (not persistent: see per_warp_sgs)
+  if constexpr (CORR && NS >= 2) {  // ring permutation slices (leaf writes, later hops read)
+    if (a.pc_mode == 3 && src == 0 && !dar) {
+      k_quant_peer<NS, true, 0, false, false, 3><<<grid, kThreads, 0, st>>>(a);
+      return;
+    }
+    if (a.pc_mode == 4 && src == 0 && dar) {
+      k_quant_peer<NS, true, 0, true, false, 4><<<grid, kThreads, 0, st>>>(a);
+      return;
+    }
+  }
   if (src == 0) {
     if (dar) k_quant_peer<NS, CORR, 0, true><<<grid, kThreads, 0, st>>>(a);
     else k_quant_peer<NS, CORR, 0, false><<<grid, kThreads, 0, st>>>(a);

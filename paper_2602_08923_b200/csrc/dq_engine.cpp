@@ -168,14 +168,17 @@ struct PeerMem {
   std::vector<uint8_t*> peer;  // rank q's region as mapped here (peer[me] == base)
   size_t cap = 0;              // bytes per chunk slot
   size_t cap_units = 0;        // flags per chunk slot
-  uint32_t n = 0, ninbox = 0, epoch = 0;
+  uint32_t n = 0, ninbox = 0, npin = 0, epoch = 0;
   size_t slots() const { return 2ull * ninbox + 2ull * n; }
   size_t inbox(uint32_t par, uint32_t h) const { return (static_cast<size_t>(par) * ninbox + h) * cap; }
   size_t gather(uint32_t par, uint32_t c) const { return (2ull * ninbox + static_cast<size_t>(par) * n + c) * cap; }
   size_t flags() const { return slots() * cap; }
   size_t iflag(uint32_t par, uint32_t h) const { return flags() + 4 * cap_units * inbox(par, h) / cap; }
   size_t gflag(uint32_t par, uint32_t c) const { return flags() + 4 * cap_units * gather(par, c) / cap; }
-  size_t total() const { return flags() + 4 * cap_units * slots(); }
+  // ring permutation slices: per parity npin areas of one u32 per (super-group, lane)
+  size_t pins() const { return (flags() + 4 * cap_units * slots() + 255) & ~static_cast<size_t>(255); }
+  size_t pin(uint32_t par, uint32_t k) const { return pins() + (static_cast<size_t>(par) * npin + k) * 128 * cap_units; }
+  size_t total() const { return pins() + 2ull * npin * 128 * cap_units; }
 };
 
 // Statistics exchange area of one rank (peer transport): per round parity the [n][T]
@@ -1166,20 +1169,22 @@ void peer_fallback(dq_ctx* ctx) {
   std::fprintf(stderr, "dynamiq_b200: peer mapping failed on some rank; using NCCL p2p\n");
 }
 
-bool peer_setup(dq_ctx* ctx, size_t mb, uint32_t max_nsg, uint32_t ninbox, cudaStream_t st) {
+bool peer_setup(dq_ctx* ctx, size_t mb, uint32_t max_nsg, uint32_t ninbox, uint32_t npin, cudaStream_t st) {
   PeerMem& pm = ctx->pm;
   const uint32_t n = ctx->cfg.n_workers;
-  if (pm.base && pm.n == n && pm.ninbox == ninbox && mb <= pm.cap && max_nsg <= pm.cap_units) return true;
+  if (pm.base && pm.n == n && pm.ninbox == ninbox && pm.npin == npin && mb <= pm.cap && max_nsg <= pm.cap_units)
+    return true;
   DQ_CUDA(cudaStreamSynchronize(st));
   ctx->close_peers();
   uint8_t* old = pm.base;
   pm.base = nullptr;
   pm.n = n;
   pm.ninbox = ninbox;
+  pm.npin = npin;
   pm.cap = (mb + mb / 4 + 4095) & ~static_cast<size_t>(4095);
   pm.cap_units = max_nsg + max_nsg / 4 + 64;
   DQ_CUDA(cudaMalloc(&pm.base, pm.total()));
-  DQ_CUDA(cudaMemsetAsync(pm.base + pm.flags(), 0, pm.total() - pm.flags(), st));
+  DQ_CUDA(cudaMemsetAsync(pm.base + pm.flags(), 0, pm.pins() - pm.flags(), st));
   const bool ok = ipc_map(ctx, pm.base, pm.peer, st);
   if (old) DQ_CUDA(cudaFree(old));  // every rank closed its mapping of it before the handle all-gather
   if (!ok) {
@@ -1233,6 +1238,15 @@ void peer_gather_decode(dq_ctx* ctx, const Prepared& p, const std::vector<Layout
 // and the longer sink costs 0.05 ms (3.15 -> 3.20 ms ring, 3.32 -> 3.36 butterfly).
 constexpr uint32_t kFuseDecodeMaxRanks = 2;
 
+// Ring permutation slices (peer transport, correlated rounding, 2 <= n <= 8): every
+// entry's Fisher-Yates permutation is computed once per round, by the chunk's leaf (whose
+// slot-0 trace draws all n-1 swaps anyway), and hop h's pi[h] is stored into the rank that
+// runs hop h; the later hops read 4 bits per entry instead of re-tracing the permutation.
+uint32_t ring_pins(const dq_config& c, const Plan& plan) {
+  const uint32_t n = c.n_workers;
+  return c.topology == DQ_RING && c.correlated && n >= 2 && n <= 8 && plan.n_slots == n ? n - 1 : 0;
+}
+
 void ring_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>& bases,
                const std::vector<Layout>& lays, float* out, size_t d, cudaStream_t st) {
   const uint32_t n = ctx->cfg.n_workers, me = static_cast<uint32_t>(ctx->rank);
@@ -1249,6 +1263,16 @@ void ring_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>& bas
     if (h > 0) {
       a.in = pm.base + pm.inbox(par, h - 1);
       a.in_flags = reinterpret_cast<const uint32_t*>(pm.base + pm.iflag(par, h - 1));
+    }
+    if (pm.npin) {  // hop s of this chunk runs on rank me + s - h
+      if (h == 0) {
+        a.pc_mode = 3;
+        for (uint32_t s = 1; s < n; ++s)
+          a.pin_out[s] = reinterpret_cast<uint32_t*>(pm.peer[(me + s) % n] + pm.pin(par, s - 1));
+      } else {
+        a.pc_mode = 4;
+        a.pin = reinterpret_cast<const uint32_t*>(pm.base + pm.pin(par, h - 1));
+      }
     }
     if (h + 1 < n) {
       a.outs[0] = pm.peer[right] + pm.inbox(par, h);
@@ -1267,7 +1291,8 @@ void ring_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>& bas
       a.dec_out = out;
       decoded[ch] = launch_quant_dec(a, 0, true, st, false);
     }
-    const double ob = decoded[ch] ? 1032.0 * lays[ch].nsg : 0.0;
+    const double ob = (decoded[ch] ? 1032.0 * lays[ch].nsg : 0.0) +
+                      (pm.npin ? 128.0 * lays[ch].nsg * (h == 0 ? n - 1 : 1) : 0.0);  // + permutation slices
     timed(ctx, dar ? K_DAR : K_LEAF, quant_bytes(lays[ch], dar) + ob, st, [&] {
       if (!decoded[ch]) launch_quant_peer(a, 0, dar, st);
       else launch_quant_dec(a, 0, true, st);
@@ -1505,7 +1530,7 @@ void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info
   while ((1u << stages) < n) ++stages;
   const uint32_t ninbox = c.topology == DQ_RING ? n - 1 : stages * n;
   if (ctx->transport == DQ_TRANSPORT_PEER && n <= static_cast<uint32_t>(kMaxPeers) && lays[0].default_format() &&
-      peer_setup(ctx, mb, max_nsg, ninbox, st)) {
+      peer_setup(ctx, mb, max_nsg, ninbox, ring_pins(c, plans[0]), st)) {
     if (c.topology == DQ_RING) ring_peer(ctx, p, bases, lays, out, d, st);
     else butterfly_peer(ctx, p, bases, lays, plans, max_nsg, out, d, st);
     for (uint32_t ch = 0; ch < n; ++ch) {

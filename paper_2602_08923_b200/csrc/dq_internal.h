@@ -41,6 +41,11 @@ struct CodecArgs {
   // (u8 per entry for n <= 4, u32 for n <= 8); pc_mode 1 = compute + store, 2 = read
   uint8_t* pcache;
   int pc_mode;
+  // distributed ring, peer transport (pc_mode 3 / 4): the leaf stores slot s's pi of
+  // every entry into pin_out[s] (rank running hop s; null = none), hop s reads a.pin.
+  // Layout: u32 per (super-group, lane), 4 bits per entry, entry j of the lane at bit 4j.
+  uint32_t* pin_out[kMaxPeers];
+  const uint32_t* pin;
   // sink DAR only (launch_quant_dec): also decode the finished record into the output
   // gradient (unpermute + denormalize through perm / gmean / n_workers_f / d), i.e. the
   // gather decode of this chunk fused into the hop that produces it
