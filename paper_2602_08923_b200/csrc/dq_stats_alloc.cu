@@ -109,7 +109,17 @@ void launch_stats(const float* const* xs, uint32_t n_workers, uint64_t d, uint32
 
 void launch_stats_peer(const float* const* xs, uint64_t d, uint32_t T, const StatsPeerArgs& sp, cudaStream_t st) {
   if (T == 0) return;
-  const uint32_t ntiles = (T + kStatSG - 1) / kStatSG, cap = 148u * 12;  // ~12 resident 128-thread CTAs per SM
+  // one wave of the persistent grid: exactly the CTAs that are resident at once (register-
+  // limited), so every CTA walks the same number of tiles and none waits for a second wave
+  static uint32_t cap = 0;
+  if (!cap) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stats<true>, kStatSG, 0);
+    cap = static_cast<uint32_t>((sms > 0 ? sms : 148) * (per_sm > 0 ? per_sm : 4));
+  }
+  const uint32_t ntiles = (T + kStatSG - 1) / kStatSG;
   k_stats<true><<<dim3(ntiles < cap ? ntiles : cap, 1), kStatSG, 0, st>>>(xs, d, T, nullptr, nullptr, sp);
 }
 
