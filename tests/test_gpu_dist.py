@@ -43,3 +43,20 @@ def test_back_to_back_async_rounds():
     assert lines, r.stdout[-3000:] + r.stderr[-3000:]
     res = json.loads(lines[-1])
     assert res["ok"], json.dumps(res, indent=1)
+
+
+def test_distributed_allreduce_three_ranks():
+    """N = 3 (non-power-of-two slot count: the float-threshold rounding decision, the ring
+    permutation slices with n = 3) on the peer transport, against the simulated round."""
+    torch = pytest.importorskip("torch")
+    if torch.cuda.device_count() < 3:
+        pytest.skip("needs >= 3 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=3",
+           "--master-addr=127.0.0.1", "--master-port=29535", os.path.join(ROOT, "tools", "dist_check.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900,
+                       env=dict(os.environ, DIST_CHECK_TRANSPORTS="peer"))
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert lines, r.stdout[-3000:] + r.stderr[-3000:]
+    res = json.loads(lines[-1])
+    assert res["ok"], json.dumps(res, indent=1)
+    assert res["world"] == 3
