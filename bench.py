@@ -130,23 +130,32 @@ def synth(torch, d, n, sigma_log, seed=1, device="cuda"):
     return out
 
 
-def roofline_of(prof, peak, peak_kind, kernel="quant_dar"):
+def roofline_of(prof, peak, peak_kind, kernel="quant_dar", traffic_ok=True):
     p = prof.get(kernel)
     if not p or p["ms"] <= 0:
         return None
     achieved = p["bytes"] / (p["ms"] * 1e-3) / 1e9
-    traffic = None
+    traffic = traffic_alg = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
             with open(tpath) as f:
-                traffic = json.load(f).get(kernel, {}).get("dram_bytes_per_launch")
+                nc = json.load(f).get(kernel, {})
+            # the capture is of an N=1 bench launch; other configs launch different sizes
+            if traffic_ok:
+                traffic = nc.get("dram_bytes_per_launch")
+                traffic_alg = nc.get("algorithmic_bytes_same_launch")
         except Exception:
             traffic = None
     out = {"bound": "hbm", "kernel": kernel, "achieved": round(achieved, 1), "peak": peak, "peak_source": peak_kind,
            "unit": "GB/s", "frac": round(achieved / peak, 4),
            "algorithmic_bytes_per_launch": p["bytes"] / max(p["launches"], 1),
            "avg_launch_ms": p["ms"] / max(p["launches"], 1), "launches": p["launches"], "traffic": traffic}
+    if traffic is not None:
+        out["traffic_source"] = {"capture": "profiles/ncu_traffic.json (one N=1 DAR hop launch)",
+                                 "algorithmic_bytes_same_launch": traffic_alg}
+    else:
+        out["traffic_source"] = "null: the committed ncu capture is of the N=1 bench's DAR launch, not this config's"
     # the fused hop is integer-issue-bound: the issue-side numbers of the
     # same kernel from the committed ncu capture
     try:
@@ -376,7 +385,7 @@ def bench_dist(args):
                             "GBps": round(v["bytes"] / max(v["ms"], 1e-9) / 1e6, 1)} for k, v in prof.items()},
             "kernels_region": {"steps": args.steps, "ms_per_step": round(prof_ms, 4),
                                "note": "second timed region, CUDA events around every launch"},
-            "roofline": roofline_of(prof, peak, pk), "gpu_launches": launches, "clocks": clk.summary(),
+            "roofline": roofline_of(prof, peak, pk, traffic_ok=False), "gpu_launches": launches, "clocks": clk.summary(),
         }
     # e2e: pinned host -> device, all-reduce, device -> host
     if not args.no_e2e:
