@@ -34,6 +34,7 @@ import time
 
 import numpy as np
 
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -473,6 +474,11 @@ def bench_reference(args):
 
 def main():
     args = parse()
+    # stdout carries only the JSON line: libraries that print to fd 1 directly (NCCL's
+    # version banner under NCCL_DEBUG=VERSION) are sent to stderr for the run.
+    sys.stdout.flush()
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
     if args.impl == "reference":
         line = bench_reference(args)
     elif int(os.environ.get("WORLD_SIZE", "1")) > 1:
@@ -480,7 +486,8 @@ def main():
     else:
         line = bench_sim(args)
     if line is not None:
-        print(json.dumps(line), flush=True)
+        sys.stdout.flush()
+        os.write(json_fd, (json.dumps(line) + "\n").encode())
 
 
 if __name__ == "__main__":
