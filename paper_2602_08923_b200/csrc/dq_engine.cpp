@@ -76,19 +76,26 @@ void fill_book(float* q, int width, bool uniform) {
     if (q[r] <= q[r - 1]) q[r] = std::nextafter(q[r - 1], 2.0f);
 }
 
-std::once_flag g_books_once;
+// The codebooks (__constant__ c_books) and the derived tables (__device__ g_qt, built by
+// k_init_tables) exist once per device: upload and build them on the first use of each
+// device of the process (the current device of the calling thread).
+std::mutex g_books_mu;
+int g_books_state[kMaxDevices] = {};  // 0 not yet, 1 ready, 2 failed
 void ensure_books() {
-  static int status = 0;
-  std::call_once(g_books_once, [] {
+  int dev = 0;
+  DQ_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) throw Error(DQ_ECUDA, "device index out of range");
+  std::lock_guard<std::mutex> lk(g_books_mu);
+  if (g_books_state[dev] == 0) {
     float books[2][138];
     for (int u = 0; u < 2; ++u) {
       fill_book(books[u], 2, u);
       fill_book(books[u] + 2, 4, u);
       fill_book(books[u] + 10, 8, u);
     }
-    status = upload_codebooks(&books[0][0]) == cudaSuccess ? 0 : 1;
-  });
-  if (status) throw Error(DQ_ECUDA, "codebook upload failed");
+    g_books_state[dev] = upload_codebooks(&books[0][0]) == cudaSuccess ? 1 : 2;
+  }
+  if (g_books_state[dev] != 1) throw Error(DQ_ECUDA, "codebook upload failed on device " + std::to_string(dev));
 }
 
 // alpha = 4 / log2(512/17)  (allocation.cpp:34-35)

@@ -93,6 +93,18 @@ uint32_t peer_unit(uint32_t nsg);  // super-groups per flag unit of a chunk (sam
 void launch_da(const CodecArgs& a, int src, cudaStream_t st);
 void launch_decode(const CodecArgs& a, int out_mode, cudaStream_t st);
 cudaError_t upload_codebooks(const float* books);
+// Per-device cached attribute (SM counts, occupancy-derived grid caps): the value for the
+// current device, computed once per device by `compute` (every device of a process has
+// its own cache slot; a second GPU must not inherit the first one's numbers).
+constexpr int kMaxDevices = 64;
+template <class F>
+inline int per_device(int (&cache)[kMaxDevices], F&& compute) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) return compute(dev);
+  if (!cache[dev]) cache[dev] = compute(dev);
+  return cache[dev];
+}
 void launch_selftest(int which, uint64_t n, uint64_t seed, unsigned long long* bad, float c1, float c2,
                      float* examples, cudaStream_t st);
 

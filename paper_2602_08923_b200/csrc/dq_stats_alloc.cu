@@ -111,14 +111,13 @@ void launch_stats_peer(const float* const* xs, uint64_t d, uint32_t T, const Sta
   if (T == 0) return;
   // one wave of the persistent grid: exactly the CTAs that are resident at once (register-
   // limited), so every CTA walks the same number of tiles and none waits for a second wave
-  static uint32_t cap = 0;
-  if (!cap) {
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
+  static int cache[kMaxDevices] = {};
+  const uint32_t cap = static_cast<uint32_t>(per_device(cache, [](int dev) {
+    int sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stats<true>, kStatSG, 0);
-    cap = static_cast<uint32_t>((sms > 0 ? sms : 148) * (per_sm > 0 ? per_sm : 4));
-  }
+    return (sms > 0 ? sms : 148) * (per_sm > 0 ? per_sm : 4);
+  }));
   const uint32_t ntiles = (T + kStatSG - 1) / kStatSG;
   k_stats<true><<<dim3(ntiles < cap ? ntiles : cap, 1), kStatSG, 0, st>>>(xs, d, T, nullptr, nullptr, sp);
 }
@@ -659,14 +658,13 @@ __global__ void __launch_bounds__(kAllocBins) k_alloc_coop(const float* __restri
 
 cudaError_t launch_alloc_search(const float* F, uint32_t T, double alpha, uint64_t wmax, double budget,
                                 uint32_t S, AllocWork w, cudaStream_t st) {
-  static int max_blocks = 0;
-  if (!max_blocks) {
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
+  static int cache[kMaxDevices] = {};
+  const int max_blocks = per_device(cache, [](int dev) {
+    int sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_alloc_coop, kAllocBins, 0);
-    max_blocks = sms * (per_sm > 0 ? per_sm : 1);
-  }
+    return (sms > 0 ? sms : 148) * (per_sm > 0 ? per_sm : 1);
+  });
   const uint32_t want = T ? (T + 4 * kAllocBins - 1) / (4 * kAllocBins) : 1;
   const uint32_t grid = want < static_cast<uint32_t>(max_blocks) ? want : static_cast<uint32_t>(max_blocks);
   void* args[] = {const_cast<float**>(&F), &T, &alpha, &wmax, &budget, &S, &w};

@@ -169,3 +169,22 @@ def test_full_size_properties(dq):
     assert a.vnmse < 1e-3
     assert a.payload_bits <= d * (4 - 0.5625)
     assert torch.isfinite(a_sync).all()
+
+
+def test_every_device_of_one_process(dq, port):
+    """Codebooks and codec tables exist once per device: a context on device 1 created
+    after device 0 was used in the same process must compute the same round."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs in one process")
+    d = 1 << 14
+    ws = _workers(port, 4, d, seed=77)
+    want = port.run_round(ws, port.round_cfg(4, 4, "ring", seed=1))
+    for dev in (0, 1):
+        cfg = _cfg(dq, 4, 4, "ring")
+        ctx = dq.Context(cfg, device=dev)
+        with torch.cuda.device(dev):
+            got = dq.run_round([torch.from_numpy(w).cuda(dev) for w in ws], cfg, collect_wire=True, ctx=ctx)
+            synced = got.synced.cpu().numpy()
+        assert np.array_equal(synced.view(np.uint32), want["synced"].view(np.uint32)), dev
+        assert got.wire_hash == want["wire_hash"], dev
+        ctx.close()
