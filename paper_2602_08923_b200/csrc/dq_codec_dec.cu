@@ -41,7 +41,7 @@ bool launch_pc_dec(const CodecArgs& a, cudaStream_t st, bool launch) {
   if (!launch) return true;
   const uint32_t per_warp = per_warp_sgs(a.L.nsg);
   const dim3 grid(persistent_grid((a.L.nsg + per_warp - 1) / per_warp, 64));
-  k_quant<NS, true, 0, true, false, 2, true><<<grid, kThreads, 0, st>>>(a);
+  k_quant<NS, true, 0, true, false, 4, true><<<grid, kThreads, 0, st>>>(a);
   return true;
 }
 }  // namespace
@@ -62,7 +62,7 @@ bool launch_quant_dec(const CodecArgs& a, int src, bool peer, cudaStream_t st, b
     else k_quant<1, false, 1, true, false, 0, true><<<grid, kThreads, 0, st>>>(a);
     return true;
   }
-  if (!a.pcache || a.pc_mode != 2 || src != 0) return false;  // correlated: the cache-reading sink only
+  if (a.pc_mode != 4 || src != 0) return false;  // correlated: the slice-reading sink only
   switch (a.n_slots) {
     case 2: return launch_pc_dec<2>(a, st, launch);
     case 3: return launch_pc_dec<3>(a, st, launch);

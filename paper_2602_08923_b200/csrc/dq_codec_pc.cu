@@ -1,6 +1,7 @@
-// dq_codec_pc.cu — simulated-round hop kernels with the per-chunk permutation cache
-// (dq_sim_round): the chunk's first compression stores every entry's Fisher-Yates
-// permutation, later simulated hops read their slot.  Worker counts 2..8, gather operand.
+// dq_codec_pc.cu — simulated-round hop kernels with permutation slices (dq_sim_round):
+// the chunk's first compression computes every entry's Fisher-Yates permutation and
+// stores each later slot's pi, later simulated hops read their slot.  Worker counts
+// 2..8, gather operand.
 #include "dq_codec.cuh"
 
 namespace dq {
@@ -9,13 +10,13 @@ template <int NS>
 bool launch_pc_ns(const CodecArgs& a, bool dar, cudaStream_t st) {
   const uint32_t per_warp = per_warp_sgs(a.L.nsg);
   const dim3 grid(persistent_grid((a.L.nsg + per_warp - 1) / per_warp, 64));
-  if (a.pc_mode == 1 && !dar) {
-    k_quant<NS, true, 0, false, false, 1><<<grid, kThreads, 0, st>>>(a);
+  if (a.pc_mode == 3 && !dar) {
+    k_quant<NS, true, 0, false, false, 3><<<grid, kThreads, 0, st>>>(a);
     return true;
   }
-  if (a.pc_mode == 2) {
-    if (dar) k_quant<NS, true, 0, true, false, 2><<<grid, kThreads, 0, st>>>(a);
-    else k_quant<NS, true, 0, false, false, 2><<<grid, kThreads, 0, st>>>(a);
+  if (a.pc_mode == 4) {
+    if (dar) k_quant<NS, true, 0, true, false, 4><<<grid, kThreads, 0, st>>>(a);
+    else k_quant<NS, true, 0, false, false, 4><<<grid, kThreads, 0, st>>>(a);
     return true;
   }
   return false;
@@ -23,7 +24,7 @@ bool launch_pc_ns(const CodecArgs& a, bool dar, cudaStream_t st) {
 }  // namespace
 
 bool launch_quant_pc(const CodecArgs& a, int src, bool dar, cudaStream_t st) {
-  if (!a.pcache || src != 0 || !a.correlated) return false;
+  if ((a.pc_mode != 3 && a.pc_mode != 4) || src != 0 || !a.correlated) return false;
   switch (a.n_slots) {
     case 2: return launch_pc_ns<2>(a, dar, st);
     case 3: return launch_pc_ns<3>(a, dar, st);

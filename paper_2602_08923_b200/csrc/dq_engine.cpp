@@ -226,7 +226,7 @@ struct dq_ctx {
   DevBuf<double> vn;
   DevBuf<uint8_t> msgs;   // message pool
   DevBuf<float> accs;     // per-worker chunk accumulators (butterfly)
-  DevBuf<uint8_t> pcache; // simulated round: the chunk's per-entry permutations
+  DevBuf<uint32_t> pcache; // simulated round: the chunk's permutation slices (slots 1..n-1)
   DevBuf<float> stage;    // host-round staging of inputs / output
   AllocState* h_state = nullptr;
   uint32_t* h_counts = nullptr;
@@ -855,14 +855,15 @@ void sim_round(dq_ctx* ctx, const float* const* xs, size_t d, float* out, int fl
   if (need_acc) ctx->accs.reserve(static_cast<size_t>(n) * max_nsg * 256);
   std::vector<uint8_t> host_soa, host_ref;
   uint64_t H = 0xcbf29ce484222325ULL;
-  // Permutation cache: every simulated hop of a chunk draws from the same per-entry
+  // Permutation slices: every simulated hop of a chunk draws from the same per-entry
   // Fisher-Yates permutation (keyed by chunk, super-group, entry; random.cpp:53-90) and
   // only reads a different slot of it, so the chunk's first compression computes the
-  // whole permutation once and the later hops read their slot.  One-rank-per-GPU rounds
-  // (dq_allreduce) compute their slot per hop as before.
+  // whole permutation once and stores slot s's pi (4 bits per entry) into slice s, which
+  // hop s reads - the same slices the distributed ring ships to the rank running hop s.
   const bool use_pc = c.correlated && n >= 2 && n <= 8 && p.a.gs == 16 && p.a.ss == 2 && p.a.gshift == 1;
-  const size_t pc_bytes = n <= 4 ? 1 : 4;
-  if (use_pc) ctx->pcache.reserve(static_cast<size_t>(max_nsg) * 256 * pc_bytes);
+  const size_t slice_words = static_cast<size_t>(max_nsg) * 32;  // u32 per (super-group, lane)
+  if (use_pc) ctx->pcache.reserve((n - 1) * slice_words);
+  auto slice = [&](uint32_t s) { return ctx->pcache.p + (s - 1) * slice_words; };
 
   for (uint32_t ch = 0; ch < n; ++ch) {
     const Plan plan = make_plan(n, ch, c.topology);
@@ -912,12 +913,14 @@ void sim_round(dq_ctx* ctx, const float* const* xs, size_t d, float* out, int fl
       const int src = operand(ev.snd, a);
       const bool dar = pend_slot[ev.snd] >= 0;
       if (dar) a.in = slot_ptr(pend_slot[ev.snd]);
-      if (use_pc) {
-        a.pcache = ctx->pcache.p;
-        a.pc_mode = e == 0 ? 1 : 2;  // event 0 is the chunk's first (leaf) compression
+      if (use_pc) {  // event 0 (slot 0) is the chunk's first (leaf) compression
+        a.pc_mode = e == 0 ? 3 : 4;
+        if (e == 0)
+          for (uint32_t s = 1; s < plan.n_slots; ++s) a.pin_out[s] = slice(s);
+        else
+          a.pin = slice(ev.slot);
       }
-      const double pcb = use_pc && src == 0 ? 256.0 * pc_bytes * L.nsg : 0.0;
-      timed(ctx, dar ? K_DAR : K_LEAF, quant_bytes(L, dar) + pcb, st, [&] { launch_quant(a, src, dar, st); });
+      timed(ctx, dar ? K_DAR : K_LEAF, quant_bytes(L, dar), st, [&] { launch_quant(a, src, dar, st); });
       if (dar) {
         free_slots.push_back(pend_slot[ev.snd]);
         pend_slot[ev.snd] = -1;
@@ -936,13 +939,12 @@ void sim_round(dq_ctx* ctx, const float* const* xs, size_t d, float* out, int fl
         g.in = slot_ptr(os);
         const int gsrc = operand(r, g);
         if (use_pc) {
-          g.pcache = ctx->pcache.p;
-          g.pc_mode = 2;
+          g.pc_mode = 4;
+          g.pin = slice(plan.sink_slot);
         }
         g.dec_out = out;  // fused decode of the chunk into the output where a variant exists
         decoded[ch] = launch_quant_dec(g, gsrc, false, st, false);
-        const double pcb = use_pc && gsrc == 0 ? 256.0 * pc_bytes * L.nsg : 0.0;
-        timed(ctx, K_DAR, quant_bytes(L, true) + pcb + (decoded[ch] ? 1032.0 * L.nsg : 0.0), st, [&] {
+        timed(ctx, K_DAR, quant_bytes(L, true) + (decoded[ch] ? 1032.0 * L.nsg : 0.0), st, [&] {
           if (!decoded[ch]) launch_quant(g, gsrc, true, st);
           else launch_quant_dec(g, gsrc, false, st);
         });

@@ -37,12 +37,10 @@ struct CodecArgs {
   uint32_t* out_flags[kMaxPeers];
   int n_outs;
   uint32_t unit, epoch;
-  // simulated round only: per-entry Fisher-Yates permutations of this chunk
-  // (u8 per entry for n <= 4, u32 for n <= 8); pc_mode 1 = compute + store, 2 = read
-  uint8_t* pcache;
+  // permutation slices (pc_mode 3 / 4, correlated, n <= 8): the chunk's leaf stores slot
+  // s's pi of every entry into pin_out[s] (null = none): the rank running hop s (ring,
+  // peer transport) or the simulated round's slice buffer; hop s reads a.pin.
   int pc_mode;
-  // distributed ring, peer transport (pc_mode 3 / 4): the leaf stores slot s's pi of
-  // every entry into pin_out[s] (rank running hop s; null = none), hop s reads a.pin.
   // Layout: u32 per (super-group, lane), 4 bits per entry, entry j of the lane at bit 4j.
   uint32_t* pin_out[kMaxPeers];
   const uint32_t* pin;
