@@ -11,6 +11,8 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libdynamiq_b200.so")
+if os.environ.get("DQ_LIB_VARIANT"):  # experiments: an in-tree build variant (variants/<name>.so)
+    LIB_PATH = os.path.join(HERE, "variants", os.environ["DQ_LIB_VARIANT"] + ".so")
 
 DQ_OK, DQ_EINVAL, DQ_EINFEASIBLE, DQ_EMALFORMED, DQ_ECUDA, DQ_ENCCL = 0, 2, 3, 4, 5, 6
 
