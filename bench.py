@@ -118,6 +118,22 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def make_inputs(n, d, sigma_log, seed=1, ranks=None):
+    """The bench workload's n worker gradients (host fp32): Llama-like heavy-tailed, i.e. a
+    per-super-group log-normal scale shared by every worker (the reference generator's
+    locality structure, proj/src/synth.cpp:31-54) times per-worker N(0, 1) entries.  Both
+    arms (ours and --impl reference) all-reduce exactly these arrays."""
+    T = (d + 255) // 256
+    rng = np.random.default_rng(seed)
+    scale = np.exp(sigma_log * rng.standard_normal(T)).astype(np.float32)
+    out = []
+    for r in (range(n) if ranks is None else ranks):
+        x = np.random.default_rng([seed, 1000 + r]).standard_normal((T, 256), dtype=np.float32)
+        x *= scale[:, None]
+        out.append(x.reshape(-1)[:d])
+    return out
+
+
 def synth(torch, d, n, sigma_log, seed=1, device="cuda"):
     """Llama-like heavy-tailed gradients: per-super-group log-normal scale shared
     across workers (proj/src/synth.cpp:46-53), entries N(0, sigma_j^2) per worker."""
@@ -128,6 +144,27 @@ def synth(torch, d, n, sigma_log, seed=1, device="cuda"):
     for r in range(n):
         x = torch.randn(T, 256, device=device, generator=g) * scale[:, None]
         out.append(x.reshape(-1)[:d].contiguous())
+    return out
+
+
+# algorithmic bytes per entry of each kernel family (c = compressed bits per
+# entry incl. scales): what the engine books per launch (dq_engine.cpp quant_bytes & co.)
+FAMILY_BYTES = {"stats": "4 (+ 8/256 per worker row)", "reduce_stats": "8(n+1)/256",
+                "quant_leaf": "4 + 8/256 + c/8", "quant_dar": "4 + 8/256 + 2c/8 (+4 output for fused sinks)",
+                "decompress_accumulate": "8 + c/8", "decode_out": "c/8 + 4 + 8/256",
+                "alloc_search": "8/256 per pass", "alloc_assign": "13/256"}
+
+
+def roofline_families(prof, peak):
+    """Achieved GB/s of every kernel family (algorithmic bytes / live CUDA-event time)."""
+    out = {}
+    for k, p in prof.items():
+        if p["ms"] <= 0 or k == "nccl":
+            continue
+        gbs = p["bytes"] / (p["ms"] * 1e-3) / 1e9
+        out[k] = {"achieved_gbs": round(gbs, 1), "frac": round(gbs / peak, 4), "launches": p["launches"],
+                  "avg_launch_ms": round(p["ms"] / max(p["launches"], 1), 5),
+                  "bytes_per_entry": FAMILY_BYTES.get(k)}
     return out
 
 
@@ -170,15 +207,15 @@ def roofline_of(prof, peak, peak_kind, kernel="quant_dar", traffic_ok=True):
     return out
 
 
-def cpu_baseline(n, d_sample, budget, topology, sigma_log, steps=1):
-    """The reference's own run_round (oracle/_ref) on a bounded sample, all chunk threads."""
+def cpu_baseline(hw, d_sample, budget, topology, sigma_log, gpu_vnmse_fn=None, steps=1):
+    """The reference's own run_round (oracle/_ref) on a bounded sample of the SAME inputs
+    (the first d_sample entries of every worker), all chunk threads; with gpu_vnmse_fn the
+    device round on that sample too, so both vNMSEs are on identical inputs."""
     from oracle.oracle import Oracle, available
     kind = "reference" if available("reference") else "port"
     ora = Oracle(kind)
-    rng = np.random.default_rng(1)
-    T = (d_sample + 255) // 256
-    scale = np.exp(sigma_log * rng.standard_normal(T)).astype(np.float64)
-    ws = [(rng.standard_normal((T, 256)) * scale[:, None]).astype(np.float32).ravel()[:d_sample] for _ in range(n)]
+    n = len(hw)
+    ws = [np.ascontiguousarray(w[:d_sample]) for w in hw]
     threads = min(n, os.cpu_count() or 1) if kind == "reference" else 1
     cfg = ora.round_cfg(n, budget, topology, seed=1, threads=threads)
     times = []
@@ -187,10 +224,13 @@ def cpu_baseline(n, d_sample, budget, topology, sigma_log, steps=1):
         res = ora.run_round(ws, cfg)
         times.append(time.perf_counter() - t0)
     t = statistics.median(times)
-    return {"value": round(n * 4 * d_sample / t / 1e9, 6), "unit": UNIT, "cores": threads, "kind": kind,
-            "sample": f"run_round n={n} {topology} d={d_sample} b={budget} sigma_log={sigma_log} "
-                      f"(1/{max(1, 1)} of the per-worker size scaled by entries), median of {steps}",
-            "seconds_per_round": round(t, 4), "vnmse": res["vnmse"]}
+    out = {"value": round(n * 4 * d_sample / t / 1e9, 6), "unit": UNIT, "cores": threads, "kind": kind,
+           "sample": f"run_round n={n} {topology} b={budget} on the first {d_sample} entries of each of the "
+                     f"bench's {n} worker gradients (same inputs as the timed arm), median of {steps}",
+           "seconds_per_round": round(t, 4), "vnmse": res["vnmse"]}
+    if gpu_vnmse_fn is not None:
+        out["gpu_vnmse_same_sample"] = gpu_vnmse_fn(ws)
+    return out
 
 
 # --------------------------------------------------------------------- N = 1
@@ -203,7 +243,8 @@ def bench_sim(args):
                             topology=dq.BUTTERFLY if args.topology == "butterfly" else dq.RING,
                             seed=dq.SharedSeed(1, 0))
     ctx = dq.Context(cfg)
-    ws = synth(torch, d, n, args.sigma_log)
+    hw = make_inputs(n, d, args.sigma_log)
+    ws = [torch.from_numpy(w).cuda() for w in hw]
     out = torch.empty(d, device="cuda")
     st = torch.cuda.current_stream()
     r = dq.run_round(ws, cfg, out=out, ctx=ctx)  # with metrics (vNMSE vs fp64 sum), untimed
@@ -255,8 +296,8 @@ def bench_sim(args):
                         "GBps": round(v["bytes"] / max(v["ms"], 1e-9) / 1e6, 1)} for k, v in prof.items()},
         "kernels_region": {"steps": args.steps, "ms_per_step": round(prof_ms, 4),
                            "note": "second timed region, CUDA events around every launch"},
-        "roofline": roofline_of(prof, peak, pk), "gpu_launches": launches,
-        "clocks": clk.summary(),
+        "roofline": roofline_of(prof, peak, pk), "roofline_families": roofline_families(prof, peak),
+        "gpu_launches": launches, "clocks": clk.summary(),
     }
     if not args.no_e2e:
         hosts = [torch.empty(d, dtype=torch.float32, pin_memory=True) for _ in range(n)]
@@ -283,7 +324,10 @@ def bench_sim(args):
                        "h2d_bytes_per_step": n * 4 * d, "d2h_bytes_per_step": 4 * d,
                        "api": "dq_run_round_host (C-ABI, pinned host buffers)"}
     if not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(n, args.cpu_sample_d, args.budget, args.topology, args.sigma_log)
+        def gpu_vnmse(sample):
+            return dq.run_round([torch.from_numpy(w).cuda() for w in sample], cfg).vnmse
+        line["cpu_baseline"] = cpu_baseline(hw, args.cpu_sample_d, args.budget, args.topology, args.sigma_log,
+                                            gpu_vnmse)
     return line
 
 
@@ -301,12 +345,8 @@ def bench_dist(args):
                             topology=dq.BUTTERFLY if args.topology == "butterfly" else dq.RING,
                             seed=dq.SharedSeed(1, 0))
     comm = dq.Communicator(cfg, rank, world)
-    # each rank's synthetic gradient: shared per-SG scale, rank-keyed entries
-    g = torch.Generator(device="cuda").manual_seed(1)
-    T = (d + 255) // 256
-    scale = torch.exp(args.sigma_log * torch.randn(T, device="cuda", generator=g))
-    g.manual_seed(1000 + rank)
-    x = (torch.randn(T, 256, device="cuda", generator=g) * scale[:, None]).reshape(-1)[:d].contiguous()
+    # this rank's worker gradient of the shared workload (the same arrays --impl reference reduces)
+    x = torch.from_numpy(make_inputs(world, d, args.sigma_log, ranks=[rank])[0]).cuda()
     out = torch.empty_like(x)
     st = torch.cuda.current_stream()
     for _ in range(args.warmup):
@@ -421,29 +461,34 @@ def bench_dist(args):
 
 
 def bench_reference(args):
-    """--impl reference: the reference's CPU run_round on the host cores (rank 0 only)."""
+    """--impl reference: the reference's CPU run_round (oracle/_ref) on the host cores, rank 0
+    only, on the SAME inputs as our arm (make_inputs).  Every step is the full workload when
+    the whole --steps/--warmup run fits in about four minutes (the warm-up round measures
+    it), else the first entries of every worker - stated in config and cpu_baseline."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
     n = args.n_sim if args.gpus <= 1 else args.gpus
     d_full = args.d or ((1 << 26) if args.gpus <= 1 else (1 << 28))
-    # Honour --steps K --warmup W exactly; keep the whole run to a few minutes by
-    # shrinking the per-step sample (~0.7 s per step at the default sample) instead.
-    total = max(1, args.steps) + max(0, args.warmup)
-    dsamp = min(args.cpu_sample_d, d_full)
-    if total > 60:
-        dsamp = max(1 << 16, (dsamp * 60 // total) // 256 * 256)
     from oracle.oracle import Oracle, available
     kind = "reference" if available("reference") else "port"
     ora = Oracle(kind)
-    rng = np.random.default_rng(1)
-    T = (dsamp + 255) // 256
-    scale = np.exp(args.sigma_log * rng.standard_normal(T))
-    ws = [(rng.standard_normal((T, 256)) * scale[:, None]).astype(np.float32).ravel()[:dsamp] for _ in range(n)]
     threads = min(n, os.cpu_count() or 1) if kind == "reference" else 1
     cfg = ora.round_cfg(n, args.budget, args.topology, seed=1, threads=threads)
     steps = max(1, args.steps)
-    for _ in range(args.warmup):
+    total = steps + max(0, args.warmup)
+    hw = make_inputs(n, d_full, args.sigma_log)
+    dsamp = d_full
+    # the reference holds ~10 copies of the inputs (grads, normalized, permuted, exact sum, ...)
+    if n * d_full * 4 * 10 > 0.6 * _host_ram_bytes():
+        dsamp = max(1 << 16, int(0.6 * _host_ram_bytes() / (n * 4 * 10)) // 256 * 256)
+    t0 = time.perf_counter()
+    res = ora.run_round([np.ascontiguousarray(w[:dsamp]) for w in hw], cfg)  # first warm-up round
+    t1 = time.perf_counter() - t0
+    if t1 * (total - 1) > 240.0:  # keep the run to a few minutes: a per-step prefix sample
+        dsamp = max(1 << 16, int(dsamp * 240.0 / (t1 * max(total - 1, 1))) // 256 * 256)
+    ws = [np.ascontiguousarray(w[:dsamp]) for w in hw]
+    for _ in range(max(0, args.warmup) - 1):
         ora.run_round(ws, cfg)
     times = []
     for _ in range(steps):
@@ -452,24 +497,35 @@ def bench_reference(args):
         times.append(time.perf_counter() - t0)
     t = statistics.median(times)
     value = n * 4 * dsamp / t / 1e9
-    sample = (f"run_round n={n} {args.topology} d={dsamp} per worker (full workload d={d_full}), "
-              f"b={args.budget}, sigma_log={args.sigma_log}, median of {steps}")
+    full = dsamp == d_full
+    sample = (f"run_round n={n} {args.topology} b={args.budget}, " +
+              (f"the full workload ({d_full} entries per worker)" if full else
+               f"the first {dsamp} of the {d_full} entries of every worker") +
+              f" of the same inputs as our arm, median of {steps}")
+    if args.gpus <= 1:
+        config = {"workload": f"configs[1]: single-B200 simulated {args.topology} all-reduce round, "
+                              f"{n} workers x {d_full} entries, b={args.budget}, sigma_log={args.sigma_log}",
+                  "global_batch": n, "entries_per_worker": dsamp, "parallelism": f"sim{n}",
+                  "l2": "inputs larger than L2 (>= 1 GiB resident)"}
+    else:
+        config = {"workload": f"configs[2]: {args.topology} all-reduce over {n} B200, {d_full} fp32 entries "
+                              f"per rank, b={args.budget}, sigma_log={args.sigma_log}",
+                  "global_batch": n, "entries_per_worker": dsamp, "parallelism": f"dp{n}", "l2": "inputs larger than L2"}
     return {"impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": UNIT, "n_gpus": args.gpus,
             "steps": steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 2),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            # Same workload/config as our arm; the per-step sample is stated in cpu_baseline.
-            "config": ({"workload": f"configs[1]: single-B200 simulated {args.topology} all-reduce round, "
-                                    f"{n} workers x {d_full} entries, b={args.budget}, sigma_log={args.sigma_log}",
-                        "global_batch": n, "entries_per_worker": d_full, "parallelism": f"sim{n}"}
-                       if args.gpus <= 1 else
-                       {"workload": f"configs[2]: {args.topology} all-reduce over {n} B200, {d_full} fp32 entries "
-                                    f"per rank, b={args.budget}, sigma_log={args.sigma_log}",
-                        "global_batch": n, "entries_per_worker": d_full, "parallelism": f"dp{n}"})
-            | {"reference_host_threads": threads, "reference_entries_per_step": dsamp},
+            "config": config, "reference_host_threads": threads,
             "vnmse": res["vnmse"],
             "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": threads, "kind": kind,
                              "sample": sample},
             "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def _host_ram_bytes():
+    try:
+        return os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+    except (ValueError, OSError):
+        return 64 << 30
 
 
 def main():

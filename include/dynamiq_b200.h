@@ -184,7 +184,9 @@ int dq_schedule(uint32_t n_workers, int topology, uint32_t chunk, dq_event* even
  * GPU (simulated hops, BASELINE config 2).  d_workers: host array of n device
  * pointers.  flags: DQ_SIM_COLLECT_WIRE hashes every message in reference wire
  * format (wire_hash parity; slow, for tests); DQ_SIM_NO_METRICS skips the
- * vNMSE pass against the fp64 sum of the inputs. */
+ * vNMSE pass against the fp64 sum of the inputs and returns without a host
+ * synchronisation (fast allocator: the round allocates on the device; dq_round_wait
+ * then fills the allocation and accounting fields). */
 enum { DQ_SIM_COLLECT_WIRE = 1, DQ_SIM_NO_METRICS = 2 };
 int dq_sim_round(dq_ctx* ctx, const float* const* d_workers, size_t d, float* d_synced,
                  int flags, dq_round_info* info, void* stream);
@@ -208,29 +210,45 @@ int dq_profile_read(dq_ctx* ctx, dq_kernel_profile* out, int cap, int* count, in
 
 /* Device self-checks of internal arithmetic (tests only): which = 0 compares
  * the shared-reciprocal division with IEEE div.rn on n hashed pairs; which = 1
- * compares the O(1) codebook bracket with binary search.  *mismatches = count. */
+ * compares the O(1) codebook bracket with binary search; which = 2 compares the
+ * decode's code * sg_scale / 255 fast path with div.rn for every code and every
+ * bf16 scale.  *mismatches = count. */
 int dq_selftest(int which, uint64_t n, uint64_t seed, uint64_t* mismatches);
+/* Test hook: make every asynchronous allocation hand its decision to the host
+ * function (the path of rounds whose thresholds the device cannot certify). */
+int dq_debug_force_host_alloc(int on);
 
 /* Multi-GPU: one process per GPU.  Rank 0 creates the id, the caller ships the
  * 128 bytes to every rank (e.g. torch.distributed), every rank joins. */
 int dq_comm_unique_id(uint8_t out[128]);
 int dq_comm_init(dq_ctx* ctx, int rank, int nranks, const uint8_t id[128]);
-/* Ring transport.  PEER (default): the fused hop kernels store compressed units
- * straight into the neighbour's memory over NVLink (CUDA IPC mapping of one
- * region per rank, per-unit flags; a flag missing for 20 s aborts the kernel),
- * and the sink stores into every rank's gather slot.  NCCL: point-to-point
- * sends of tile-aligned pieces on a communication stream.  Same bytes, same
- * result.  Env DQ_TRANSPORT=nccl selects NCCL at context creation; if any rank
- * cannot map its peers, all ranks switch to NCCL at the first round.  The
- * butterfly topology always uses NCCL. */
+/* Transport (ring and butterfly).  PEER (default): the fused hop kernels store
+ * compressed units straight into the receiver's memory over NVLink (CUDA IPC
+ * mapping of one region per rank, per-unit flags; a flag missing for
+ * DQ_WAIT_TIMEOUT_S seconds, default 600, aborts the kernel), and the sink
+ * stores into every rank's gather slot.  NCCL: point-to-point sends on a
+ * communication stream (ring: tile-aligned pieces; butterfly: per stage).  Same
+ * bytes, same result.  Env DQ_TRANSPORT=nccl selects NCCL at context creation;
+ * if any rank cannot map its peers, all ranks switch to NCCL at the first
+ * round.  The ablation scale formats (group size != 16, flat scales) always use
+ * NCCL. */
 enum { DQ_TRANSPORT_PEER = 0, DQ_TRANSPORT_NCCL = 1 };
 int dq_comm_set_transport(dq_ctx* ctx, int transport);
 int dq_comm_get_transport(const dq_ctx* ctx, int* transport);
 /* [engine.hpp:63-64 run_round, distributed] d_in: this rank's gradient; d_out:
  * the SUM estimate over ranks (caller divides by n for a mean, as the
- * reference's caller does). */
+ * reference's caller does).  Stream-ordered: with the peer transport and the
+ * fast allocator the whole round is enqueued without a host synchronisation
+ * (the allocation is decided and certified on the device; the class counts stay
+ * on the device) and can be captured in a CUDA graph.  info = NULL returns at
+ * once; info != NULL waits for the round and fills the allocation / accounting
+ * fields (the reference's RoundResult), as dq_round_wait does later. */
 int dq_allreduce(dq_ctx* ctx, const float* d_in, float* d_out, size_t d, dq_round_info* info,
                  void* stream);
+/* Wait for the context's last round (dq_allreduce or dq_sim_round) and fill the
+ * fields that need its device results: u, payload_bits, n8/n4/n2, the wire
+ * accounting and ms_total. */
+int dq_round_wait(dq_ctx* ctx, dq_round_info* info);
 
 #ifdef __cplusplus
 }

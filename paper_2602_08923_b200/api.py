@@ -335,6 +335,13 @@ class Context:
         return {arr[i].name.decode(): {"launches": arr[i].launches, "ms": arr[i].ms, "bytes": arr[i].bytes}
                 for i in range(min(n.value, 16))}
 
+    def wait(self) -> dict:
+        """Wait for this context's last round and return its full info (allocation,
+        accounting, device time) - what an asynchronous round leaves unfilled."""
+        info = RoundInfo()
+        check(lib().dq_round_wait(self.h, C.byref(info)))
+        return _info_dict(info)
+
     def close(self) -> None:
         if getattr(self, "h", None):
             lib().dq_ctx_destroy(self.h)
@@ -536,7 +543,9 @@ class Communicator:
         if rank == 0:
             check(lib().dq_comm_unique_id(uid.ctypes.data_as(C.POINTER(C.c_uint8))))
         obj = [uid.tobytes()]
-        dist.broadcast_object_list(obj, src=0, group=group)
+        # src is a global rank: the group's rank 0 (a subgroup need not contain rank 0)
+        src = 0 if group is None else dist.get_global_rank(group, 0)
+        dist.broadcast_object_list(obj, src=src, group=group)
         uid = np.frombuffer(obj[0], np.uint8).copy()
         check(lib().dq_comm_init(self.ctx.h, rank, world_size, uid.ctypes.data_as(C.POINTER(C.c_uint8))))
         if transport is not None:
@@ -552,11 +561,18 @@ class Communicator:
         check(lib().dq_comm_get_transport(self.ctx.h, C.byref(t)))
         return "peer" if t.value == TRANSPORT_PEER else "nccl"
 
-    def allreduce(self, x: torch.Tensor, out: Optional[torch.Tensor] = None) -> tuple:
-        """SUM estimate of every rank's ``x`` (caller divides by n for a mean)."""
+    def allreduce(self, x: torch.Tensor, out: Optional[torch.Tensor] = None, async_op: bool = False):
+        """SUM estimate of every rank's ``x`` (caller divides by n for a mean).
+
+        ``async_op=False``: waits for the round, returns ``(out, info)``.  ``async_op=True``:
+        enqueues the round on the current stream without any host synchronisation (it can be
+        captured in a CUDA graph) and returns ``out``; ``self.ctx.wait()`` gives the info."""
         x = _f32(x, x.numel(), "gradient")
         if out is None:
             out = torch.empty_like(x)
+        if async_op:
+            check(lib().dq_allreduce(self.ctx.h, _ptr(x), _ptr(out), x.numel(), None, _stream()))
+            return out
         info = RoundInfo()
         check(lib().dq_allreduce(self.ctx.h, _ptr(x), _ptr(out), x.numel(), C.byref(info), _stream()))
         return out, _info_dict(info)

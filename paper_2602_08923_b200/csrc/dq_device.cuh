@@ -23,6 +23,17 @@ constexpr uint64_t kSeedSalt = 0x6a09e667f3bcc909ULL;
 
 enum Purpose : uint32_t { kEntryQuant = 1, kScaleQuant = 2, kPermutation = 3 };
 
+// Spin-wait budget of every kernel that waits on another GPU or on the host (peer flags,
+// the statistics exchange, a host allocation answer): a wait longer than this traps the
+// kernel instead of hanging the GPU.  Per device; set from DQ_WAIT_TIMEOUT_S (default
+// 600 s, the scale of PyTorch's NCCL timeout) when the device is first used.
+extern __device__ uint64_t g_spin_ns;
+__device__ __forceinline__ uint64_t dq_globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // ---------------------------------------------------------------- PRNG
 __host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 33)) * 0xff51afd7ed558ccdULL;
@@ -145,6 +156,15 @@ struct Layout {
     SG s = locate_at(i);
     s.width = i < n8 ? 8 : (i < n8 + n4 ? 4 : 2);
     return s;
+  }
+  // width runs of the super-groups [lo, lo + nsg) of a round whose permuted order holds
+  // n8 width-8 then n4 width-4 super-groups (then width 2): asynchronous rounds read the
+  // round's class counts on the device instead of the host
+  __host__ __device__ void runs_from_counts(uint32_t lo, uint32_t c8, uint32_t c4) {
+    const uint32_t hi = lo + nsg;
+    const uint32_t e8 = hi < c8 ? hi : c8, e4 = hi < c8 + c4 ? hi : c8 + c4, s4 = lo > c8 ? lo : c8;
+    n8 = e8 > lo ? e8 - lo : 0;
+    n4 = e4 > s4 ? e4 - s4 : 0;
   }
   __host__ __device__ SG locate(uint32_t i) const {
     SG s = locate_at(i);

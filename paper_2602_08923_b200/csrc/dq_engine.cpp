@@ -8,6 +8,7 @@
 // stream.  Two executors share the plan: dq_sim_round runs every worker of a
 // chunk on one GPU (BASELINE config 2), dq_allreduce runs one rank per GPU and
 // moves the compressed chunks over NVLink with NCCL point-to-point.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -94,6 +95,10 @@ void ensure_books() {
       fill_book(books[u] + 10, 8, u);
     }
     g_books_state[dev] = upload_codebooks(&books[0][0]) == cudaSuccess ? 1 : 2;
+    // spin-wait budget of the peer / host waits (DQ_WAIT_TIMEOUT_S seconds, default 600)
+    double secs = 600.0;
+    if (const char* t = std::getenv("DQ_WAIT_TIMEOUT_S")) secs = std::atof(t) > 0 ? std::atof(t) : secs;
+    if (g_books_state[dev] == 1 && set_spin_ns(static_cast<uint64_t>(secs * 1e9)) != cudaSuccess) g_books_state[dev] = 2;
   }
   if (g_books_state[dev] != 1) throw Error(DQ_ECUDA, "codebook upload failed on device " + std::to_string(dev));
 }
@@ -228,8 +233,28 @@ struct dq_ctx {
   DevBuf<float> accs;     // per-worker chunk accumulators (butterfly)
   DevBuf<uint32_t> pcache; // simulated round: the chunk's permutation slices (slots 1..n-1)
   DevBuf<float> stage;    // host-round staging of inputs / output
+  dq_round_info last_info{};  // the last round's host-known info (dq_round_wait)
   AllocState* h_state = nullptr;
   uint32_t* h_counts = nullptr;
+  // asynchronous allocation (no host sync inside a round): per round parity a mapped
+  // mailbox the search mirrors its state into, a mapped copy of F for the rare rounds the
+  // host must finish, and the side stream running the host function that does so
+  HostMsg* hmsg = nullptr;   // [2]
+  float* hF = nullptr;
+  size_t hF_cap = 0;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  uint32_t apar = 0;
+  bool async_alloc = true;   // env DQ_SYNC_ALLOC=1: host-synchronous allocation (round-1 behaviour)
+  const float** h_xptrs = nullptr;  // pinned worker-pointer tables [2][64] (capture-safe H2D)
+  uint32_t xpar = 0;
+  // what the last round needs to fill dq_round_info once it has completed
+  struct RoundRec {
+    bool valid = false, async = false;
+    uint32_t par = 0, T = 0, n = 0, S = 256, gs = 16, ss = 2, gshift = 1;
+    int topology = 0;
+    std::vector<uint32_t> lo;
+  } rec;
   double* h_vn = nullptr;
   uint32_t last_T = 0;
   uint64_t alloc_redos = 0;  // rounds where the device thresholds differed from glibc's
@@ -272,6 +297,12 @@ struct dq_ctx {
     if (pm.base) cudaFree(pm.base);
     if (sm.base) cudaFree(sm.base);
     if (h_state) cudaFreeHost(h_state);
+    if (hmsg) cudaFreeHost(hmsg);
+    if (hF) cudaFreeHost(hF);
+    if (h_xptrs) cudaFreeHost(h_xptrs);
+    if (side) cudaStreamDestroy(side);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
     if (h_counts) cudaFreeHost(h_counts);
     if (h_vn) cudaFreeHost(h_vn);
     if (ev0) cudaEventDestroy(ev0);
@@ -348,7 +379,13 @@ void harvest(dq_ctx* ctx) {
 // A round returned without a host sync: keep its boundary events for the next sync
 // (ev0/ev1 are re-recorded by the next round, so copy them into lr0/lr1 on the GPU
 // timeline by recording the copies right here) and report the previous round's time.
-void finish_async(dq_ctx* ctx, dq_round_info* info) {
+void finish_async(dq_ctx* ctx, dq_round_info* info, cudaStream_t st) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  DQ_CUDA(cudaStreamIsCapturing(st, &cap));
+  if (cap != cudaStreamCaptureStatusNone) {  // recorded into a graph: nothing to time on the host
+    info->ms_total = 0.0;
+    return;
+  }
   if (!ctx->lr0) {
     DQ_CUDA(cudaEventCreate(&ctx->lr0));
     DQ_CUDA(cudaEventCreate(&ctx->lr1));
@@ -397,7 +434,10 @@ double payload_budget(const dq_config& c) {  // allocation.cpp:45-58
 
 AllocWork work_of(dq_ctx* ctx, uint32_t T) {
   ctx->level.reserve(T);
-  ctx->astate.reserve(1);
+  if (!ctx->astate.p) {
+    ctx->astate.reserve(1);
+    DQ_CUDA(cudaMemset(ctx->astate.p, 0, sizeof(AllocState)));  // epoch 0: no mailbox answer matches
+  }
   ctx->bins.reserve(4 * kAllocBins);
   ctx->blockcnt.reserve(4 * (alloc_blocks(T) + 1));
   ctx->counts.reserve(4);
@@ -414,6 +454,8 @@ struct AllocResult {
   double u = 0.0;
   uint64_t payload = 0;
   uint32_t n8 = 0, n4 = 0, n2 = 0, passes = 0;
+  bool async = false;  // counts live on the device only (ctx->counts), host mailbox parity `par`
+  uint32_t par = 0;
 };
 
 // allocate_general for W = {2,4,8} (allocation.cpp:121-168), the round path's general
@@ -681,6 +723,157 @@ AllocResult allocate_fast(dq_ctx* ctx, const dq_config& c, const float* dF, uint
   return r;
 }
 
+// u of the search's chosen candidate, re-derived with the host libm exactly as
+// fast_sample_points does (allocation.cpp:201-224) from the flips the search identified.
+double host_u_of(const AllocState& s) {
+  auto hflip = [](const FlipRec& q) {
+    float f;
+    std::memcpy(&f, &q.fbits, 4);
+    return (q.type ? 8.0 : 4.0) - kAlpha * std::log2(static_cast<double>(f));
+  };
+  auto clampu = [](double v) { return v < -1e6 ? -1e6 : (v > 1e6 ? 1e6 : v); };
+  const int c = s.choice >= 0 ? s.choice : 1;
+  const FlipRec* l = nullptr;
+  const FlipRec* r = nullptr;
+  if (s.status == 2) {
+    if (c == 1) l = &s.slot[1];
+    else { r = &s.slot[1]; if (s.slot[0].present) l = &s.slot[0]; }
+  } else if (s.status == 1) {
+    if (c == 1) { r = &s.slot[2]; if (s.slot[1].present) l = &s.slot[1]; }
+    else if (c == 0) { r = &s.slot[1]; if (s.slot[0].present) l = &s.slot[0]; }
+    else { l = &s.slot[2]; if (s.slot[3].present) r = &s.slot[3]; }
+  }
+  if (l && r) return clampu(0.5 * (hflip(*l) + hflip(*r)));
+  if (r) return clampu(hflip(*r) - 1.0);
+  if (l) return clampu(hflip(*l) + 1.0);
+  return 0.0;
+}
+
+// allocate_fast on the host (allocation.cpp:195-260, the same sorted samples and the same
+// bisection): the rare asynchronous rounds whose thresholds the device could not certify.
+// Returns false when even the first sample is over budget (InfeasibleBudget).
+bool host_allocate_fast(const float* F, uint32_t T, uint32_t S, double budget, double* u, float* t24, float* t48) {
+  std::vector<double> flips;
+  flips.reserve(2ull * T);
+  for (uint32_t j = 0; j < T; ++j) {
+    if (!(F[j] > 0.0f)) continue;
+    const double l = kAlpha * std::log2(static_cast<double>(F[j]));
+    flips.push_back(4.0 - l);
+    flips.push_back(8.0 - l);
+  }
+  std::sort(flips.begin(), flips.end());
+  flips.erase(std::unique(flips.begin(), flips.end()), flips.end());
+  std::vector<double> samples;
+  if (flips.empty()) {
+    samples.push_back(0.0);
+  } else {
+    samples.push_back(flips.front() - 1.0);
+    for (size_t i = 0; i + 1 < flips.size(); ++i) samples.push_back(0.5 * (flips[i] + flips[i + 1]));
+    samples.push_back(flips.back() + 1.0);
+  }
+  for (double& v : samples) v = v < -1e6 ? -1e6 : (v > 1e6 ? 1e6 : v);
+  auto thr = [](double uu, float* a, float* b) {
+    *a = static_cast<float>(std::exp2((4.0 - uu) / kAlpha));
+    *b = static_cast<float>(std::exp2((8.0 - uu) / kAlpha));
+  };
+  auto payload = [&](double uu) {
+    float a, b;
+    thr(uu, &a, &b);
+    uint64_t w = 0;
+    for (uint32_t j = 0; j < T; ++j) w += F[j] >= b ? 8 : (F[j] >= a ? 4 : 2);
+    return static_cast<double>(w * S);
+  };
+  size_t lo = 0, hi = samples.size() - 1;
+  if (payload(samples[lo]) > budget) return false;
+  if (payload(samples[hi]) <= budget) {
+    lo = hi;
+  } else {
+    while (lo + 1 < hi) {
+      const size_t mid = (lo + hi) / 2;
+      if (payload(samples[mid]) <= budget) lo = mid;
+      else hi = mid;
+    }
+  }
+  *u = samples[lo];
+  thr(*u, t24, t48);
+  return true;
+}
+
+// Host function of an asynchronous round (side stream, after the search): nothing to do
+// unless the search handed the decision to the host; then finish it from the exported F
+// and release the assignment kernel, which waits for `resolved` to reach the round's epoch.
+void CUDART_CB host_alloc_resolve(void* p) {
+  HostMsg* m = static_cast<HostMsg*>(p);
+  const AllocState& s = m->state;
+  if (!s.need_host) return;
+  double u = 0.0;
+  float a = INFINITY, b = INFINITY;  // infeasible: all width 2 (the round is reported as failed)
+  const bool ok = host_allocate_fast(m->hF, s.T, s.S, s.budget, &u, &a, &b);
+  m->u = u;
+  m->t24 = a;
+  m->t48 = b;
+  m->host_status = ok ? 0 : DQ_EINFEASIBLE;
+  __atomic_store_n(const_cast<uint32_t*>(&m->resolved), s.epoch, __ATOMIC_RELEASE);
+}
+
+void ensure_mailbox(dq_ctx* ctx, uint32_t T) {
+  if (!ctx->hmsg) {
+    DQ_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx->hmsg), 2 * sizeof(HostMsg), cudaHostAllocMapped));
+    std::memset(static_cast<void*>(ctx->hmsg), 0, 2 * sizeof(HostMsg));
+    DQ_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+    DQ_CUDA(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+    DQ_CUDA(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+  }
+  if (ctx->hF_cap < T) {
+    DQ_CUDA(cudaDeviceSynchronize());  // growing: no round may still write the old copy
+    if (ctx->hF) DQ_CUDA(cudaFreeHost(ctx->hF));
+    ctx->hF = nullptr;
+    const size_t cap = T + T / 4 + 1024;
+    DQ_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx->hF), cap * sizeof(float), cudaHostAllocMapped));
+    ctx->hF_cap = cap;
+    ctx->hmsg[0].hF = ctx->hF;
+    ctx->hmsg[1].hF = ctx->hF;
+  }
+}
+
+// allocate_fast + build_permutation with no host synchronisation: the search decides and
+// certifies on the device; the assignment follows in stream order (waiting for the host
+// function only on the rare need_host rounds); the class counts stay on the device
+// (ctx->counts) for the kernels and are mirrored to the mailbox for dq_round_info.
+AllocResult allocate_fast_async(dq_ctx* ctx, const dq_config& c, const float* dF, uint32_t T, uint8_t* dW,
+                                uint32_t* dP, cudaStream_t st) {
+  AllocResult r;
+  r.async = true;
+  const uint32_t S = c.super_group_size;
+  AllocWork w = work_of(ctx, T);
+  const double bbar = payload_budget(c);
+  const double budget = static_cast<double>(T) * S * bbar;
+  auto fits = [&](int64_t W) { return static_cast<double>(static_cast<uint64_t>(S) * (2ull * T + W)) <= budget; };
+  int64_t W = static_cast<int64_t>(std::floor(budget / S)) - 2 * static_cast<int64_t>(T);
+  if (W < -1) W = -1;
+  while (fits(W + 1)) ++W;
+  while (W >= 0 && !fits(W)) --W;
+  if (W < 0) throw Error(DQ_EINFEASIBLE, "bit allocation infeasible within budget");
+  ensure_mailbox(ctx, T);
+  const uint32_t par = ctx->apar ^= 1u;
+  r.par = par;
+  HostMsg* m = ctx->hmsg + par;
+  void* dm = nullptr;
+  void* dF_host = nullptr;
+  DQ_CUDA(cudaHostGetDevicePointer(&dm, m, 0));
+  DQ_CUDA(cudaHostGetDevicePointer(&dF_host, ctx->hF, 0));
+  w.hmsg = static_cast<HostMsg*>(dm);
+  w.hF = static_cast<float*>(dF_host);
+  DQ_CUDA(launch_alloc_search(dF, T, kAlpha, static_cast<uint64_t>(W), budget, S, w, st));
+  DQ_CUDA(cudaEventRecord(ctx->ev_fork, st));
+  DQ_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+  DQ_CUDA(cudaLaunchHostFunc(ctx->side, host_alloc_resolve, m));
+  DQ_CUDA(cudaEventRecord(ctx->ev_join, ctx->side));
+  launch_alloc_assign(dF, T, 0.f, 0.f, true, w, dW, dP, st);
+  DQ_CUDA(cudaGetLastError());
+  return r;
+}
+
 // scale format of the codec config (codec.cpp:88-116): s = 8 << gshift entries per
 // group; hierarchical: 256/s u8 codes + bf16 sg_scale, flat: 256/s bf16 per super-group
 template <class T>
@@ -770,23 +963,47 @@ struct Prepared {
   size_t max_chunk_bytes;
 };
 
-// stats (already reduced into ctx->gsq / gmean) -> allocation -> chunk plan
-Prepared prepare(dq_ctx* ctx, uint32_t T, cudaStream_t st) {
+// Rounds that allocate asynchronously: the fast allocator without the instrumentation or
+// wire-hash modes (both read per-chunk sizes on the host); DQ_SYNC_ALLOC=1 turns it off.
+bool async_alloc_ok(const dq_ctx* ctx, bool collect_wire) {
+  const dq_config& c = ctx->cfg;
+  return ctx->async_alloc && !ctx->profile && !collect_wire && c.variable_width && c.allocator == DQ_ALLOC_FAST;
+}
+
+// stats (already reduced into ctx->gsq / gmean) -> allocation -> chunk plan.  Async: the
+// class counts stay on the device, every chunk is sized for the worst case (all width 8)
+// and the kernels derive their width runs from ctx->counts.
+Prepared prepare(dq_ctx* ctx, uint32_t T, cudaStream_t st, bool async = false) {
   Prepared p;
   p.T = T;
   const dq_config& c = ctx->cfg;
-  p.a = allocate(ctx, c, ctx->gsq.p, T, ctx->widths.p, ctx->perm.p, st);
+  p.a = async ? allocate_fast_async(ctx, c, ctx->gsq.p, T, ctx->widths.p, ctx->perm.p, st)
+              : allocate(ctx, c, ctx->gsq.p, T, ctx->widths.p, ctx->perm.p, st);
   set_format(p.a, c);
   const uint32_t n = c.n_workers;
   p.lo.resize(n + 1);
   for (uint32_t i = 0; i <= n; ++i) p.lo[i] = static_cast<uint32_t>(static_cast<uint64_t>(T) * i / n);
   p.max_chunk_bytes = 0;
   for (uint32_t i = 0; i < n; ++i) {
-    const size_t b = chunk_layout(p.a, p.lo[i], p.lo[i + 1]).bytes();
+    Layout L = chunk_layout(p.a, p.lo[i], p.lo[i + 1]);
+    if (async) L.n8 = L.nsg;  // worst case
+    const size_t b = L.bytes();
     p.max_chunk_bytes = b > p.max_chunk_bytes ? b : p.max_chunk_bytes;
   }
   p.max_chunk_bytes = (p.max_chunk_bytes + 255) / 256 * 256;
   ctx->last_T = T;
+  ctx->rec = dq_ctx::RoundRec{};
+  ctx->rec.valid = true;
+  ctx->rec.async = async;
+  ctx->rec.par = p.a.par;
+  ctx->rec.T = T;
+  ctx->rec.n = n;
+  ctx->rec.S = c.super_group_size;
+  ctx->rec.gs = p.a.gs;
+  ctx->rec.ss = p.a.ss;
+  ctx->rec.gshift = p.a.gshift;
+  ctx->rec.topology = c.topology;
+  ctx->rec.lo = p.lo;
   return p;
 }
 
@@ -806,6 +1023,58 @@ void fill_info_alloc(dq_round_info* info, const Prepared& p) {
   info->n4 = p.a.n4;
   info->n2 = p.a.n2;
   info->alloc_passes = p.a.passes;
+}
+
+// wire accounting of a whole round (engine.cpp:135-160,368-396): every reduce event sends
+// one fresh message of its chunk, the all-gather forwards the sink's bytes n_gat times
+void account_round(dq_round_info* info, const AllocResult& a, const std::vector<uint32_t>& lo, uint32_t n,
+                   int topology) {
+  for (uint32_t ch = 0; ch < n; ++ch) {
+    const Plan plan = make_plan(n, ch, topology);
+    const Layout L = chunk_layout(a, lo[ch], lo[ch + 1]);
+    for (size_t e = 0; e < plan.red.size(); ++e) account(info, L, true);
+    for (uint32_t g = 0; g < plan.n_gat; ++g) account(info, L, g == 0);
+    info->stats_bits += static_cast<uint64_t>(plan.red.size() + plan.n_gat) * 64ull * L.nsg;
+  }
+}
+
+// Allocation + accounting fields of the last asynchronous round, from the mailbox it
+// filled (call only once the round has completed on the device).
+void finish_info(dq_ctx* ctx, dq_round_info* info) {
+  const dq_ctx::RoundRec& rec = ctx->rec;
+  if (!rec.valid || !rec.async) return;
+  const HostMsg& m = ctx->hmsg[rec.par];
+  if (m.state.need_host && m.host_status)
+    throw Error(m.host_status, "bit allocation infeasible within budget (host finish)");
+  AllocResult a;
+  a.gs = rec.gs;
+  a.ss = rec.ss;
+  a.gshift = rec.gshift;
+  a.n8 = m.counts[0];
+  a.n4 = m.counts[1];
+  a.n2 = m.counts[2];
+  a.u = m.state.need_host ? m.u : host_u_of(m.state);
+  a.passes = m.state.passes;
+  a.payload = static_cast<uint64_t>(rec.S) * (8ull * a.n8 + 4ull * a.n4 + 2ull * a.n2);
+  info->u = a.u;
+  info->payload_bits = a.payload;
+  info->n8 = a.n8;
+  info->n4 = a.n4;
+  info->n2 = a.n2;
+  info->alloc_passes = a.passes;
+  info->stats_bits = info->wire_payload_bits = info->scale_bits = info->header_bits = 0;
+  info->repr_bits = info->compressed_coordinates = info->transmitted_coordinates = 0;
+  account_round(info, a, rec.lo, rec.n, rec.topology);
+}
+
+// Worker-pointer table of a round -> device (parity-double-buffered, through pinned host
+// memory so the copy is stream-ordered and capturable in a CUDA graph)
+void upload_ptrs(dq_ctx* ctx, const float* const* xs, uint32_t n, cudaStream_t st) {
+  if (!ctx->h_xptrs) DQ_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_xptrs), 2 * 64 * sizeof(float*)));
+  ctx->xpar ^= 1u;
+  const float** h = ctx->h_xptrs + 64 * ctx->xpar;
+  for (uint32_t r = 0; r < n; ++r) h[r] = xs[r];
+  DQ_CUDA(cudaMemcpyAsync(ctx->xptrs.p + 64 * ctx->xpar, h, n * sizeof(float*), cudaMemcpyHostToDevice, st));
 }
 
 // ---------------------------------------------------------- simulation
@@ -833,15 +1102,16 @@ void sim_round(dq_ctx* ctx, const float* const* xs, size_t d, float* out, int fl
   }
   DQ_CUDA(cudaEventRecord(ctx->ev0, st));
   reserve_round(ctx, T, n);
-  ctx->xptrs.reserve(n);
-  DQ_CUDA(cudaMemcpyAsync(ctx->xptrs.p, xs, n * sizeof(float*), cudaMemcpyHostToDevice, st));
+  ctx->xptrs.reserve(2 * 64);
+  upload_ptrs(ctx, xs, n, st);
   timed(ctx, K_STATS, 4.0 * n * d + 8.0 * n * T, st,
-        [&] { launch_stats(ctx->xptrs.p, n, d, T, ctx->mean_all.p, ctx->sq_all.p, st); });
+        [&] { launch_stats(ctx->xptrs.p + 64 * ctx->xpar, n, d, T, ctx->mean_all.p, ctx->sq_all.p, st); });
   timed(ctx, K_REDUCE, 8.0 * (n + 1) * T, st,
         [&] { launch_reduce_stats(ctx->mean_all.p, ctx->sq_all.p, n, T, ctx->gmean.p, ctx->gsq.p, st); });
   DQ_CUDA(cudaGetLastError());
-  Prepared p = prepare(ctx, T, st);
-  fill_info_alloc(info, p);
+  const bool async = async_alloc_ok(ctx, collect_wire);
+  Prepared p = prepare(ctx, T, st, async);
+  if (!async) fill_info_alloc(info, p);
 
   // message pool: per-worker pending slots + scratch, reused per chunk; plus one gather
   // (sink output) buffer per chunk, decoded together at the end of the round
@@ -870,6 +1140,7 @@ void sim_round(dq_ctx* ctx, const float* const* xs, size_t d, float* out, int fl
     const Layout L = chunk_layout(p.a, p.lo[ch], p.lo[ch + 1]);
     CodecArgs base = base_args(c, ch);
     base.L = L;
+    base.counts = async ? ctx->counts.p : nullptr;
     base.first_sg = p.lo[ch];
     base.perm = ctx->perm.p;
     base.gmean = ctx->pmean.p;
@@ -925,7 +1196,7 @@ void sim_round(dq_ctx* ctx, const float* const* xs, size_t d, float* out, int fl
         free_slots.push_back(pend_slot[ev.snd]);
         pend_slot[ev.snd] = -1;
       }
-      account(info, L, true);
+      if (!async) account(info, L, true);
       hash_msg(slot_ptr(os), 1);
       const uint32_t r = ev.rcv;
       if (static_cast<int>(e) == last_in[r] && r != plan.sink) {
@@ -963,8 +1234,10 @@ void sim_round(dq_ctx* ctx, const float* const* xs, size_t d, float* out, int fl
     DQ_CUDA(cudaGetLastError());
     // all-gather of the sink's bytes: hashed once per forward (engine.cpp:219-229)
     if (collect_wire) hash_msg(slot_ptr(gather_slot), static_cast<int>(plan.n_gat));
-    for (uint32_t g = 0; g < plan.n_gat; ++g) account(info, L, g == 0);
-    info->stats_bits += static_cast<uint64_t>(plan.red.size() + plan.n_gat) * 64ull * L.nsg;
+    if (!async) {
+      for (uint32_t g = 0; g < plan.n_gat; ++g) account(info, L, g == 0);
+      info->stats_bits += static_cast<uint64_t>(plan.red.size() + plan.n_gat) * 64ull * L.nsg;
+    }
     gslots[ch] = gather_slot;
     H ^= hsh + 0x9e3779b97f4a7c15ULL + (H << 6) + (H >> 2);
   }
@@ -973,6 +1246,7 @@ void sim_round(dq_ctx* ctx, const float* const* xs, size_t d, float* out, int fl
     GatherArgs g{};
     set_format(g, ctx->cfg);
     g.use_hi = 1;
+    g.counts = async ? ctx->counts.p : nullptr;
     uint32_t max_nsg_g = 0, k = 0;
     double gbytes = 0;
     for (uint32_t ch = 0; ch < n; ++ch) {
@@ -996,19 +1270,21 @@ void sim_round(dq_ctx* ctx, const float* const* xs, size_t d, float* out, int fl
     if (k) timed(ctx, K_DECODE, gbytes, st, [&] { launch_gather_decode(g, k, max_nsg_g, st); });
     DQ_CUDA(cudaGetLastError());
   }
+  if (async) DQ_CUDA(cudaStreamWaitEvent(st, ctx->ev_join, 0));  // the round's host function has returned
   DQ_CUDA(cudaEventRecord(ctx->ev1, st));
   if (flags & DQ_SIM_NO_METRICS) {  // asynchronous return: timing resolved at the next sync point
-    finish_async(ctx, info);
+    finish_async(ctx, info, st);
     return;
   }
   // vNMSE against the fp64 sum of the inputs (metrics, not part of the timed path)
   ctx->vn.reserve(2);
   if (!ctx->h_vn) DQ_CUDA(cudaMallocHost(&ctx->h_vn, 2 * sizeof(double)));
   DQ_CUDA(cudaMemsetAsync(ctx->vn.p, 0, 2 * sizeof(double), st));
-  launch_vnmse(ctx->xptrs.p, n, out, d, ctx->vn.p, st);
+  launch_vnmse(ctx->xptrs.p + 64 * ctx->xpar, n, out, d, ctx->vn.p, st);
   DQ_CUDA(cudaMemcpyAsync(ctx->h_vn, ctx->vn.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
   DQ_CUDA(cudaStreamSynchronize(st));
   harvest(ctx);
+  if (async) finish_info(ctx, info);
   info->mse = ctx->h_vn[0] / static_cast<double>(d);
   info->vnmse = ctx->h_vn[1] > 0 ? ctx->h_vn[0] / ctx->h_vn[1] : 0.0;
   float ms = 0.f;
@@ -1321,6 +1597,7 @@ void peer_gather_decode(dq_ctx* ctx, const Prepared& p, const std::vector<Layout
   GatherArgs g{};
   set_format(g, ctx->cfg);
   g.use_hi = 1;
+  g.counts = p.a.async ? ctx->counts.p : nullptr;
   uint32_t max_nsg = 0, k = 0;
   double gbytes = 0;
   for (uint32_t c = 0; c < n; ++c) {
@@ -1467,8 +1744,9 @@ void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info
   }
   DQ_CUDA(cudaEventRecord(ctx->ev0, st));
   reserve_round(ctx, T, n);
-  ctx->xptrs.reserve(1);
-  DQ_CUDA(cudaMemcpyAsync(ctx->xptrs.p, &x, sizeof(float*), cudaMemcpyHostToDevice, st));
+  ctx->xptrs.reserve(2 * 64);
+  upload_ptrs(ctx, &x, 1, st);
+  const float* const* dxp = ctx->xptrs.p + 64 * ctx->xpar;
   // (a) local stats into this rank's row, (b) all-gather rows, fixed-order fp64 reduce (H4).
   // Peer transport: the all-gather is fused into the statistics kernel (each block stores
   // its rows into every rank's exchange area over NVLink, the last block raises the row
@@ -1486,7 +1764,7 @@ void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info
     sp.done = ctx->sdone.p;
     sp.n = n;
     sp.epoch = ep;
-    timed(ctx, K_STATS, 4.0 * d + 8.0 * T * n, st, [&] { launch_stats_peer(ctx->xptrs.p, d, T, sp, st); });
+    timed(ctx, K_STATS, 4.0 * d + 8.0 * T * n, st, [&] { launch_stats_peer(dxp, d, T, sp, st); });
     timed(ctx, K_REDUCE, 8.0 * (n + 1) * T, st, [&] {
       launch_reduce_stats_peer(sm.mean(sm.base, par, 0), sm.sq(sm.base, par, 0), sm.flags(sm.base, par), ep, n, T,
                                ctx->gmean.p, ctx->gsq.p, st);
@@ -1494,7 +1772,7 @@ void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info
   } else {
     float* my_mean = ctx->mean_all.p + static_cast<size_t>(me) * T;
     float* my_sq = ctx->sq_all.p + static_cast<size_t>(me) * T;
-    timed(ctx, K_STATS, 4.0 * d + 8.0 * T, st, [&] { launch_stats(ctx->xptrs.p, 1, d, T, my_mean, my_sq, st); });
+    timed(ctx, K_STATS, 4.0 * d + 8.0 * T, st, [&] { launch_stats(dxp, 1, d, T, my_mean, my_sq, st); });
     timed(ctx, K_NCCL, 8.0 * T * n, st, [&] {
       DQ_NCCL(ncclGroupStart());
       DQ_NCCL(ncclAllGather(my_mean, ctx->mean_all.p, T, ncclFloat, ctx->comm, st));
@@ -1505,10 +1783,14 @@ void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info
           [&] { launch_reduce_stats(ctx->mean_all.p, ctx->sq_all.p, n, T, ctx->gmean.p, ctx->gsq.p, st); });
   }
   DQ_CUDA(cudaGetLastError());
-  Prepared p = prepare(ctx, T, st);
-  fill_info_alloc(info, p);
+  // peer transport (default scale format): the round allocates asynchronously; the NCCL
+  // transport and the ablation formats size their messages on the host (synchronous)
+  const bool peer_pre = ctx->transport == DQ_TRANSPORT_PEER && n <= static_cast<uint32_t>(kMaxPeers) &&
+                        c.group_size == 16 && c.hierarchical_scales;
+  Prepared p = prepare(ctx, T, st, peer_pre && async_alloc_ok(ctx, false));
+  if (!p.a.async) fill_info_alloc(info, p);
 
-  const size_t mb = p.max_chunk_bytes;
+  size_t mb = p.max_chunk_bytes;
   uint32_t max_nsg = 0;
   for (uint32_t i = 0; i < n; ++i) max_nsg = std::max(max_nsg, p.lo[i + 1] - p.lo[i]);
   // per chunk: outgoing, incoming, held, gather; accumulators for butterfly receivers
@@ -1526,6 +1808,7 @@ void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info
     lays[ch] = chunk_layout(p.a, p.lo[ch], p.lo[ch + 1]);
     CodecArgs b = base_args(c, ch);
     b.L = lays[ch];
+    b.counts = p.a.async ? ctx->counts.p : nullptr;
     b.first_sg = p.lo[ch];
     b.perm = ctx->perm.p;
     b.gmean = ctx->pmean.p;
@@ -1538,19 +1821,37 @@ void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info
   uint32_t stages = 0;
   while ((1u << stages) < n) ++stages;
   const uint32_t ninbox = c.topology == DQ_RING ? n - 1 : stages * n;
-  if (ctx->transport == DQ_TRANSPORT_PEER && n <= static_cast<uint32_t>(kMaxPeers) && lays[0].default_format() &&
-      peer_setup(ctx, mb, max_nsg, ninbox, ring_pins(c, plans[0]), st)) {
+  if (peer_pre && peer_setup(ctx, mb, max_nsg, ninbox, ring_pins(c, plans[0]), st)) {
     if (c.topology == DQ_RING) ring_peer(ctx, p, bases, lays, out, d, st);
     else butterfly_peer(ctx, p, bases, lays, plans, max_nsg, out, d, st);
-    for (uint32_t ch = 0; ch < n; ++ch) {
-      for (uint32_t g = 0; g < plans[ch].n_gat; ++g) account(info, lays[ch], g == 0);
-      for (size_t e = 0; e < plans[ch].red.size(); ++e) account(info, lays[ch], true);
-      info->stats_bits += static_cast<uint64_t>(plans[ch].red.size() + plans[ch].n_gat) * 64ull * lays[ch].nsg;
-    }
+    if (!p.a.async) account_round(info, p.a, p.lo, n, c.topology);
     DQ_CUDA(cudaGetLastError());
+    if (p.a.async) DQ_CUDA(cudaStreamWaitEvent(st, ctx->ev_join, 0));  // the round's host function has returned
     DQ_CUDA(cudaEventRecord(ctx->ev1, st));
-    finish_async(ctx, info);
+    finish_async(ctx, info, st);
     return;
+  }
+  if (p.a.async) {  // peer mapping failed on some rank: bring the allocation to the host (NCCL sizes messages)
+    DQ_CUDA(cudaStreamSynchronize(st));
+    dq_round_info tmp{};
+    finish_info(ctx, &tmp);
+    p.a.async = false;
+    p.a.u = tmp.u;
+    p.a.n8 = tmp.n8;
+    p.a.n4 = tmp.n4;
+    p.a.n2 = tmp.n2;
+    p.a.payload = tmp.payload_bits;
+    p.a.passes = tmp.alloc_passes;
+    ctx->rec.async = false;
+    fill_info_alloc(info, p);
+    mb = 0;
+    for (uint32_t ch = 0; ch < n; ++ch) {
+      lays[ch] = chunk_layout(p.a, p.lo[ch], p.lo[ch + 1]);
+      bases[ch].L = lays[ch];
+      bases[ch].counts = nullptr;
+      mb = std::max<size_t>(mb, lays[ch].bytes());
+    }
+    mb = (mb + 255) / 256 * 256;
   }
   ctx->msgs.reserve(4ull * n * mb);
   uint8_t* mysink = buf(3, me);
@@ -1708,7 +2009,7 @@ void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info
   }
   DQ_CUDA(cudaGetLastError());
   DQ_CUDA(cudaEventRecord(ctx->ev1, st));
-  finish_async(ctx, info);
+  finish_async(ctx, info, st);
 }
 
 }  // namespace
@@ -1749,6 +2050,8 @@ int dq_ctx_create(const dq_config* cfg, int device, dq_ctx** out) {
     c->device = device;
     if (const char* t = std::getenv("DQ_TRANSPORT"))
       if (std::strcmp(t, "nccl") == 0) c->transport = DQ_TRANSPORT_NCCL;
+    if (const char* t = std::getenv("DQ_SYNC_ALLOC"))
+      if (std::strcmp(t, "1") == 0) c->async_alloc = false;
     *out = c;
   });
 }
@@ -2106,6 +2409,7 @@ int dq_sim_round(dq_ctx* ctx, const float* const* d_workers, size_t d, float* d_
     if (!ctx || !d_workers || !d_synced || !info) invalid("null argument");
     DQ_CUDA(cudaSetDevice(ctx->device));
     sim_round(ctx, d_workers, d, d_synced, flags, info, S(stream));
+    ctx->last_info = *info;
   });
 }
 
@@ -2141,9 +2445,39 @@ int dq_round_allocation(dq_ctx* ctx, uint8_t* h_widths, uint32_t* h_perm, size_t
 
 int dq_allreduce(dq_ctx* ctx, const float* d_in, float* d_out, size_t d, dq_round_info* info, void* stream) {
   return guarded([&] {
-    if (!ctx || !d_in || !d_out || !info) invalid("null argument");
+    if (!ctx || !d_in || !d_out) invalid("null argument");
     DQ_CUDA(cudaSetDevice(ctx->device));
-    dist_round(ctx, d_in, d, d_out, info, S(stream));
+    dq_round_info scratch{};
+    dist_round(ctx, d_in, d, d_out, info ? info : &scratch, S(stream));
+    ctx->last_info = info ? *info : scratch;
+    if (info) {  // the caller wants the round's allocation and accounting: wait for it
+      DQ_CUDA(cudaStreamSynchronize(S(stream)));
+      harvest(ctx);
+      finish_info(ctx, info);
+      info->ms_total = ctx->last_round_ms;
+    }
+  });
+}
+
+int dq_round_wait(dq_ctx* ctx, dq_round_info* info) {
+  return guarded([&] {
+    if (!ctx || !info) invalid("null argument");
+    DQ_CUDA(cudaSetDevice(ctx->device));
+    if (ctx->lr_pending) DQ_CUDA(cudaEventSynchronize(ctx->lr1));
+    else if (ctx->ev1) DQ_CUDA(cudaEventSynchronize(ctx->ev1));
+    harvest(ctx);
+    if (!ctx->rec.valid) invalid("no round has been run on this context");
+    *info = ctx->last_info;
+    if (ctx->rec.async) finish_info(ctx, info);
+    info->ms_total = ctx->last_round_ms;
+  });
+}
+
+int dq_debug_force_host_alloc(int on) {
+  return guarded([&] {
+    ensure_books();
+    set_force_host_alloc(on);
+    DQ_CUDA(cudaGetLastError());
   });
 }
 

@@ -13,6 +13,9 @@ constexpr int kMaxPeers = 8;  // peer transport: ring of up to 8 GPUs (one NVSwi
 
 struct CodecArgs {
   Layout L;                 // geometry of the chunk being processed
+  // asynchronous rounds: the round's class counts (n8, n4 over all super-groups) in device
+  // memory; the kernel derives L.n8 / L.n4 of [first_sg, first_sg + L.nsg) from them
+  const uint32_t* counts;
   uint32_t first_sg;        // permuted index of the chunk's first super-group (RNG key, perm lookup)
   const float* x;           // raw gradient, original order (gather source)
   const uint32_t* perm;     // permuted position -> original super-group
@@ -57,6 +60,7 @@ struct GatherArgs {
   uint32_t hi[64];           // explicit end of chunk c when use_hi (non-adjacent chunk lists)
   int use_hi;
   uint32_t n8[64], n4[64];   // width runs of chunk c
+  const uint32_t* counts;    // asynchronous rounds: derive n8 / n4 of chunk c from the round's class counts
   const uint32_t* perm;
   const float* gmean;        // permuted order
   float* out;
@@ -91,6 +95,7 @@ uint32_t peer_unit(uint32_t nsg);  // super-groups per flag unit of a chunk (sam
 void launch_da(const CodecArgs& a, int src, cudaStream_t st);
 void launch_decode(const CodecArgs& a, int out_mode, cudaStream_t st);
 cudaError_t upload_codebooks(const float* books);
+cudaError_t set_spin_ns(uint64_t ns);  // g_spin_ns of the current device
 // Per-device cached attribute (SM counts, occupancy-derived grid caps): the value for the
 // current device, computed once per device by `compute` (every device of a process has
 // its own cache slot; a second GPU must not inherit the first one's numbers).
@@ -160,6 +165,26 @@ struct AllocState {
   // chosen u and thresholds (read by the assignment kernels)
   double u;
   float t24, t48;
+  // Asynchronous rounds: every present candidate threshold certified equal to glibc's
+  // (its float rounding is stable under a relative perturbation of 2^-40, far above the
+  // libm error chain; dq_stats_alloc.cu alloc_candidates).  need_host = !certified or no
+  // decision among L-1..L+1: the host finishes (host function on a side stream, F
+  // exported to mapped host memory) and the assignment waits for its answer.
+  uint32_t certified, need_host, epoch, T;
+  double budget, alpha;
+  uint32_t S, pad2_;
+};
+// Mapped (zero-copy) host memory shared by the allocation kernels and the host: the
+// search mirrors its final state here, the assignment its class counts; on need_host
+// rounds the search exports F and the host answers through `resolved`.
+struct HostMsg {
+  AllocState state;           // mirror of the search's final state (written by the kernel)
+  const float* hF;            // host view of the exported F (set by the host)
+  uint32_t counts[4];         // mirror of n8, n4, n2 (written by k_assign_scan)
+  volatile uint32_t resolved; // epoch of the last host answer
+  int32_t host_status;        // 0 ok, 3 infeasible budget, 5 internal error (reported at the next sync)
+  double u;                   // host answer: u, t24, t48
+  float t24, t48;
 };
 constexpr int kAllocBins = 1024;
 constexpr int kAllocMaxPasses = 8;
@@ -171,12 +196,16 @@ struct AllocWork {           // device scratch owned by the context
   uint32_t* counts;          // [4]: n8, n4, n2, payload_units
   const float* gmean;        // global means, original order (input of the permuted copy)
   float* pmean;              // pmean[k] = gmean[perm[k]]
+  HostMsg* hmsg;             // asynchronous rounds: mapped host mailbox (null: synchronous rounds)
+  float* hF;                 // asynchronous rounds: mapped host copy of F (need_host rounds only)
 };
 uint32_t alloc_blocks(uint32_t T);
 // Search for the crossing flip and the plateau midpoint u, fully on device: one
 // cooperative launch (grid-wide syncs between histogram passes), no host sync.
 cudaError_t launch_alloc_search(const float* F, uint32_t T, double alpha, uint64_t wmax, double budget,
                                 uint32_t S, AllocWork w, cudaStream_t st);
+// test hook: make every asynchronous search hand its decision to the host (need_host)
+void set_force_host_alloc(int on);
 // Slow exact path helpers (rare): neighbour flip of `key` (dir -1: largest key below,
 // +1: smallest key above) -> rec; float-threshold counts -> counts[0] = #F>=t48,
 // counts[1] = #F>=t24.  Both asynchronous on st.

@@ -142,7 +142,7 @@ void launch_reduce_stats(const float* mean, const float* sq, uint32_t n, uint32_
 }
 
 // The rank-ordered reduction over the fused all-gather's rows: each block first waits
-// (thread 0, acquire at system scope, 20 s timeout -> trap) for every row's flag.
+// (thread 0, acquire at system scope, g_spin_ns timeout -> trap) for every row's flag.
 __global__ void k_reduce_stats_peer(const float* mean, const float* sq, const uint32_t* flags, uint32_t epoch,
                                     uint32_t n, uint32_t T, float* gm, float* gs) {
   if (threadIdx.x == 0) {
@@ -150,15 +150,12 @@ __global__ void k_reduce_stats_peer(const float* mean, const float* sq, const ui
       uint32_t v;
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + r) : "memory");
       if (v == epoch) continue;
-      uint64_t t0;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      const uint64_t t0 = dq_globaltimer();
       for (;;) {
         __nanosleep(64);
         asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + r) : "memory");
         if (v == epoch) break;
-        uint64_t t1;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-        if (t1 - t0 > 20ull * 1000 * 1000 * 1000) __trap();
+        if (dq_globaltimer() - t0 > g_spin_ns) __trap();
       }
     }
   }
@@ -221,7 +218,9 @@ __device__ void alloc_init(AllocState* s, uint64_t* bins, uint64_t wmax) {
     bins[4 * b + 3] = 0;
   }
   if (t == 0) {
+    const uint32_t epoch = s->epoch;  // the mailbox tag survives the reset (one per round)
     *s = AllocState{};
+    s->epoch = epoch;
     s->kmin = ~0ull;
     s->kmax = 0;
     s->wmax = wmax;
@@ -545,15 +544,27 @@ __device__ void alloc_candidates(AllocState* s, double alpha) {
     s->cand_present[2] = 1;
     s->cand_u[2] = s->slot[3].present ? mid(f2, flip(3)) : __dadd_rn(f2, 1.0);
   }
+  // certification: float(d) is the same float for every d' with |d' - d| <= 2^-40 |d|,
+  // while glibc's double (log2 and exp2 within ~0.5 ulp, CUDA's within 1-2 ulp, five
+  // rounded double operations between them on |log2 F| <= 150) differs from the device
+  // double by far less than 2^-43 relative
+  auto stable = [](double d) {
+    const float lo = __double2float_rn(__dmul_rd(d, 1.0 - 0x1p-40)), hi = __double2float_rn(__dmul_ru(d, 1.0 + 0x1p-40));
+    return __float_as_uint(lo) == __float_as_uint(hi);
+  };
+  uint32_t cert = 1;
   for (int c = 0; c < 3; ++c) {
     double u = s->cand_u[c];
     u = u < -1e6 ? -1e6 : (u > 1e6 ? 1e6 : u);
     s->cand_u[c] = u;
-    s->cand_t24[c] = static_cast<float>(exp2(__ddiv_rn(__dsub_rn(4.0, u), alpha)));
-    s->cand_t48[c] = static_cast<float>(exp2(__ddiv_rn(__dsub_rn(8.0, u), alpha)));
+    const double d24 = exp2(__ddiv_rn(__dsub_rn(4.0, u), alpha)), d48 = exp2(__ddiv_rn(__dsub_rn(8.0, u), alpha));
+    s->cand_t24[c] = static_cast<float>(d24);
+    s->cand_t48[c] = static_cast<float>(d48);
+    if (s->cand_present[c]) cert &= stable(d24) && stable(d48) ? 1u : 0u;
     s->cand_n8[c] = 0;
     s->cand_n48[c] = 0;
   }
+  s->certified = cert;
 }
 
 __device__ void alloc_count(const float* __restrict__ F, uint32_t T, AllocState* s) {
@@ -583,6 +594,8 @@ __device__ void alloc_count(const float* __restrict__ F, uint32_t T, AllocState*
     }
 }
 
+__device__ int g_force_host_alloc;  // test hook (set_force_host_alloc)
+
 // the reference's choice: the largest sample whose float-threshold payload fits
 __device__ void alloc_decide(AllocState* s, double budget, uint32_t S, uint32_t T) {
   auto ok = [&](int c) {
@@ -599,6 +612,7 @@ __device__ void alloc_decide(AllocState* s, double budget, uint32_t S, uint32_t 
   s->u = s->cand_u[c];
   s->t24 = s->cand_t24[c];
   s->t48 = s->cand_t48[c];
+  s->need_host = (!s->certified || ch < 0 || g_force_host_alloc) ? 1u : 0u;
 }
 
 // The whole search in one cooperative launch: prep -> up to kAllocMaxPasses x
@@ -653,8 +667,29 @@ __global__ void __launch_bounds__(kAllocBins) k_alloc_coop(const float* __restri
   grid.sync();
   alloc_count(F, T, st);
   grid.sync();
-  if (blockIdx.x == 0 && threadIdx.x == 0) alloc_decide(st, budget, S, T);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    alloc_decide(st, budget, S, T);
+    st->T = T;
+    st->S = S;
+    st->budget = budget;
+    st->alpha = alpha;
+    st->epoch += 1;  // per-round tag of the host mailbox (device-side: graph replays advance it too)
+  }
+  if (!w.hmsg) return;  // synchronous round: the host reads the state after a stream sync
+  grid.sync();
+  // asynchronous round: export F for the host on need_host rounds, then mirror the state
+  if (st->need_host)
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < T; j += gridDim.x * blockDim.x) w.hF[j] = F[j];
+  grid.sync();
+  if (blockIdx.x == 0) {
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(st);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(&w.hmsg->state);
+    for (uint32_t k = threadIdx.x; k < sizeof(AllocState) / 4; k += blockDim.x) dst[k] = src[k];
+    __threadfence_system();
+  }
 }
+
+void set_force_host_alloc(int on) { cudaMemcpyToSymbol(g_force_host_alloc, &on, sizeof on); }
 
 cudaError_t launch_alloc_search(const float* F, uint32_t T, double alpha, uint64_t wmax, double budget,
                                 uint32_t S, AllocWork w, cudaStream_t st) {
@@ -779,10 +814,35 @@ __device__ __forceinline__ int class_of(const float* F, uint32_t j, float t24, f
 template <int MODE>
 __global__ void __launch_bounds__(256) k_assign_count(const float* __restrict__ F, uint32_t T, float t24,
                                                       float t48, const AllocState* st_thr, int fixed_cls,
-                                                      double g0, double g1, uint8_t* widths, uint32_t* blockcnt) {
+                                                      double g0, double g1, uint8_t* widths, uint32_t* blockcnt,
+                                                      HostMsg* hmsg) {
   if (st_thr) {
     t24 = st_thr->t24;
     t48 = st_thr->t48;
+    if (hmsg && st_thr->need_host) {  // asynchronous round the device could not certify: host answer
+      __shared__ float ht[2];
+      if (threadIdx.x == 0) {
+        const uint32_t ep = st_thr->epoch;
+        const uint64_t t0 = dq_globaltimer();
+        for (;;) {
+          uint32_t v;
+          asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(&hmsg->resolved) : "memory");
+          if (v == ep) break;
+          __nanosleep(1000);
+          if (dq_globaltimer() - t0 > g_spin_ns) __trap();
+        }
+        ht[0] = *reinterpret_cast<volatile float*>(&hmsg->t24);
+        ht[1] = *reinterpret_cast<volatile float*>(&hmsg->t48);
+        if (blockIdx.x == 0) {  // for the scatter kernel that follows
+          AllocState* w = const_cast<AllocState*>(st_thr);
+          w->t24 = ht[0];
+          w->t48 = ht[1];
+        }
+      }
+      __syncthreads();
+      t24 = ht[0];
+      t48 = ht[1];
+    }
   }
   const uint32_t j0 = blockIdx.x * 2048 + threadIdx.x * 8;
   uint64_t packed = 0;  // 16-bit counts per class
@@ -803,7 +863,8 @@ __global__ void __launch_bounds__(256) k_assign_count(const float* __restrict__ 
 }
 
 // exclusive scan of the per-block class counts (one CTA), totals -> counts[0..2]
-__global__ void __launch_bounds__(1024) k_assign_scan(uint32_t nb, uint32_t* blockcnt, uint32_t* counts) {
+__global__ void __launch_bounds__(1024) k_assign_scan(uint32_t nb, uint32_t* blockcnt, uint32_t* counts,
+                                                      HostMsg* hmsg) {
   __shared__ uint64_t carry[3];
   if (threadIdx.x < 3) carry[threadIdx.x] = 0;
   __syncthreads();
@@ -837,6 +898,12 @@ __global__ void __launch_bounds__(1024) k_assign_scan(uint32_t nb, uint32_t* blo
     counts[0] = static_cast<uint32_t>(carry[0]);
     counts[1] = static_cast<uint32_t>(carry[1]);
     counts[2] = static_cast<uint32_t>(carry[2]);
+    if (hmsg) {  // asynchronous round: the host reads the class counts lazily
+      hmsg->counts[0] = counts[0];
+      hmsg->counts[1] = counts[1];
+      hmsg->counts[2] = counts[2];
+      __threadfence_system();
+    }
   }
 }
 
@@ -879,8 +946,9 @@ static void assign_impl(int mode, const float* F, uint32_t T, float t24, float t
   if (nb == 0) return;
 #define DQ_ASSIGN(M)                                                                                     \
   do {                                                                                                   \
-    k_assign_count<M><<<nb, 256, 0, st>>>(F, T, t24, t48, thr, fixed_cls, g0, g1, widths, w.blockcnt);    \
-    k_assign_scan<<<1, 1024, 0, st>>>(nb, w.blockcnt, w.counts);                                         \
+    k_assign_count<M><<<nb, 256, 0, st>>>(F, T, t24, t48, thr, fixed_cls, g0, g1, widths, w.blockcnt,     \
+                                          w.hmsg);                                                       \
+    k_assign_scan<<<1, 1024, 0, st>>>(nb, w.blockcnt, w.counts, w.hmsg);                                 \
     k_assign_scatter<M><<<nb, 256, 0, st>>>(F, T, t24, t48, thr, fixed_cls, g0, g1, w.blockcnt, w.counts, \
                                             perm, w.gmean, w.pmean);                                     \
   } while (0)

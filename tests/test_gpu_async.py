@@ -1,0 +1,113 @@
+"""Asynchronous rounds: the fast allocation decided and certified on the device, no host
+synchronisation inside a round.
+
+* bit-identical to the oracle's run_round (proj/src/engine.cpp:269-418): synced gradient,
+  widths, permutation, u, payload and wire accounting - without the wire-hash mode, which
+  forces the host-synchronous path;
+* the rare rounds the device cannot certify, forced: the host function finishes the
+  allocation from the exported F (allocation.cpp:195-260) and releases the assignment;
+* metrics=False returns at once; Context.wait() fills the allocation fields later;
+* a whole round captured in a CUDA graph and replayed on new inputs equals direct rounds.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def dq():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2602_08923_b200 as dq
+    return dq
+
+
+def _workers(port, n, d, seed, sigma_log=4.0):
+    return [port.generate_worker(d, seed=seed, sigma_log=sigma_log, rank=r) for r in range(n)]
+
+
+def _cfg(dq, n, b, topo="ring", seed=1):
+    return dq.PipelineConfig(n_workers=n, budget_bits=b, topology=dq.BUTTERFLY if topo == "butterfly" else dq.RING,
+                             seed=dq.SharedSeed(seed, 0))
+
+
+def _check(dq, got, want):
+    synced = got.synced.cpu().numpy()
+    assert np.array_equal(synced.view(np.uint32), want["synced"].view(np.uint32))
+    assert np.array_equal(got.widths, want["widths"])
+    assert np.array_equal(got.permutation, want["perm"])
+    assert got.u == want["u"]
+    assert got.payload_bits == want["payload_bits"]
+    for k in ("stats_bits", "wire_payload_bits", "scale_bits", "header_bits", "repr_bits",
+              "compressed_coordinates", "transmitted_coordinates"):
+        assert got.info[k] == want[k], k
+
+
+@pytest.mark.parametrize("n,b,topo,d", [(4, 4.0, "ring", 1 << 16), (8, 3.0, "butterfly", (1 << 15) + 77),
+                                        (3, 5.0, "ring", 1 << 14), (2, 6.0, "ring", 3000)])
+def test_async_round_matches_oracle(dq, port, n, b, topo, d):
+    ws = _workers(port, n, d, seed=11 + n)
+    want = port.run_round(ws, port.round_cfg(n, b, topo, seed=1))
+    got = dq.run_round([torch.from_numpy(w).cuda() for w in ws], _cfg(dq, n, b, topo), with_allocation=True)
+    _check(dq, got, want)
+
+
+@pytest.mark.parametrize("n,b,d", [(4, 4.0, 1 << 16), (4, 5.0, (1 << 14) + 9), (8, 4.0, 1 << 15)])
+def test_host_finished_allocation(dq, port, n, b, d):
+    """need_host forced on every round: the side-stream host function answers, the
+    assignment kernel waits for it; results unchanged."""
+    from paper_2602_08923_b200._lib import check, lib
+    ws = _workers(port, n, d, seed=23 + n)
+    want = port.run_round(ws, port.round_cfg(n, b, "ring", seed=1))
+    check(lib().dq_debug_force_host_alloc(1))
+    try:
+        got = dq.run_round([torch.from_numpy(w).cuda() for w in ws], _cfg(dq, n, b), with_allocation=True)
+    finally:
+        check(lib().dq_debug_force_host_alloc(0))
+    _check(dq, got, want)
+
+
+def test_no_metrics_round_then_wait(dq, port):
+    n, d = 4, 1 << 15
+    ws = _workers(port, n, d, seed=5)
+    want = port.run_round(ws, port.round_cfg(n, 4.0, "ring", seed=1))
+    cfg = _cfg(dq, n, 4.0)
+    ctx = dq.Context(cfg)
+    r = dq.run_round([torch.from_numpy(w).cuda() for w in ws], cfg, ctx=ctx, metrics=False)
+    info = ctx.wait()
+    assert np.array_equal(r.synced.cpu().numpy().view(np.uint32), want["synced"].view(np.uint32))
+    assert info["u"] == want["u"] and info["payload_bits"] == want["payload_bits"]
+    assert info["repr_bits"] == want["repr_bits"]
+    assert info["n8"] * 8 + info["n4"] * 4 + info["n2"] * 2 == want["payload_bits"] // 256
+    ctx.close()
+
+
+def test_round_captured_in_cuda_graph(dq, port):
+    """A simulated round (stats -> device allocation -> hops -> decode) captured once and
+    replayed on new inputs equals direct rounds on those inputs."""
+    n, d = 4, 1 << 16
+    cfg = _cfg(dq, n, 4.0)
+    ctx = dq.Context(cfg)
+    xs = [torch.empty(d, device="cuda") for _ in range(n)]
+    out = torch.empty(d, device="cuda")
+    first = _workers(port, n, d, seed=41)
+    for x, w in zip(xs, first):
+        x.copy_(torch.from_numpy(w))
+    dq.run_round(xs, cfg, out=out, ctx=ctx, metrics=False)  # sizes every buffer
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        dq.run_round(xs, cfg, out=out, ctx=ctx, metrics=False)
+    for seed in (41, 42, 43):
+        ws = _workers(port, n, d, seed=seed)
+        for x, w in zip(xs, ws):
+            x.copy_(torch.from_numpy(w))
+        g.replay()
+        torch.cuda.synchronize()
+        want = port.run_round(ws, port.round_cfg(n, 4.0, "ring", seed=1))
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), want["synced"].view(np.uint32)), seed
+    del g
+    ctx.close()

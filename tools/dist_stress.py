@@ -43,7 +43,7 @@ def main():
         torch.cuda.synchronize()
         dist.barrier()
         for k, d in enumerate(sizes):  # no host sync in between
-            out, _ = comm.allreduce(inputs[k][rank])
+            out = comm.allreduce(inputs[k][rank], async_op=True)
             outs.append(out)
         torch.cuda.synchronize()
         bad = []
