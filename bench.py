@@ -350,7 +350,7 @@ def bench_dist(args):
     out = torch.empty_like(x)
     st = torch.cuda.current_stream()
     for _ in range(args.warmup):
-        comm.allreduce(x, out)
+        comm.allreduce(x, out, async_op=True)
     torch.cuda.synchronize()
     # accuracy vs exact fp32 sum (outside the timed region)
     truth = x.clone()
@@ -367,7 +367,7 @@ def bench_dist(args):
         torch.cuda.synchronize()
         e0.record(st)
         for _ in range(args.steps):
-            _, info = comm.allreduce(x, out)
+            comm.allreduce(x, out, async_op=True)
         e1.record(st)
         torch.cuda.synchronize()
         dist.barrier()
@@ -381,7 +381,7 @@ def bench_dist(args):
     p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     p0.record(st)
     for _ in range(args.steps):
-        comm.allreduce(x, out)
+        comm.allreduce(x, out, async_op=True)
     p1.record(st)
     torch.cuda.synchronize()
     prof = comm.ctx.read_profile(reset=True)
@@ -437,14 +437,14 @@ def bench_dist(args):
         k = max(3, args.steps // 4)
         for _ in range(2):
             dx.copy_(hx, non_blocking=True)
-            comm.allreduce(dx, out)
+            comm.allreduce(dx, out, async_op=True)
             hy.copy_(out, non_blocking=True)
         torch.cuda.synchronize()
         dist.barrier()
         a.record(st)
         for _ in range(k):
             dx.copy_(hx, non_blocking=True)
-            comm.allreduce(dx, out)
+            comm.allreduce(dx, out, async_op=True)
             hy.copy_(out, non_blocking=True)
         b.record(st)
         torch.cuda.synchronize()

@@ -47,9 +47,12 @@ enum dq_topology { DQ_RING = 0, DQ_BUTTERFLY = 1 };
 enum dq_allocator { DQ_ALLOC_GENERAL = 0, DQ_ALLOC_FAST = 1, DQ_ALLOC_FIXED = 2 };
 
 /* [proj/include/dynamiq/engine.hpp:22-43 PipelineConfig] — same fields and
- * defaults (dq_config_default).  Supported on device: group_size 16,
- * super_group_size 256, hierarchical scales, quantized codec, fast, general
- * or fixed allocator; non_uniform and correlated may be toggled. */
+ * defaults (dq_config_default).  Supported on device by the rounds
+ * (dq_sim_round, dq_allreduce): super_group_size 256, group_size 8/16/32/64/128,
+ * hierarchical (u8 + bf16) or flat bf16 scales, the quantized codec, the fast,
+ * general or fixed allocator, ring or butterfly; non_uniform and correlated may
+ * be toggled.  The chunk primitives below use the default format (s = 16,
+ * hierarchical). */
 typedef struct dq_config {
   uint32_t n_workers;
   uint32_t group_size;
@@ -110,6 +113,12 @@ size_t dq_chunk_bytes(uint32_t n8, uint32_t n4, uint32_t n2, uint32_t n16);
 /* [codec.cpp:268-291 compressed_size_bits / 8] reference wire bytes incl. the 24-byte
  * header (== dq_chunk_bytes + 24 when n16 == 0; passthrough records carry no scales) */
 size_t dq_wire_bytes(uint32_t n8, uint32_t n4, uint32_t n2, uint32_t n16);
+/* [codec.hpp:26-31 CodecConfig{group_size, hierarchical_scales}] scale format of
+ * this thread's chunk primitives (sizes, codec kernels, wire converters) until
+ * the next call: group_size 8/16/32/64/128, hierarchical u8 + bf16 or flat bf16
+ * group scales (default 16, hierarchical).  prev_* (may be NULL) receive the
+ * previous format, so a caller can scope it like cudaSetDevice. */
+int dq_codec_format_set(uint32_t group_size, int hierarchical, uint32_t* prev_group_size, int* prev_hierarchical);
 /* [codec.hpp:64-69 compress_chunk] values: n_sg*256 fp32 */
 int dq_compress_chunk(const float* d_values, uint32_t n8, uint32_t n4, uint32_t n2, uint32_t n16,
                       const dq_qctx* q, uint32_t first_sg_index, int non_uniform, void* d_out,

@@ -98,7 +98,7 @@ struct QuantContext {  // codec.hpp:33-40
   bool correlated = true;
 };
 
-struct CodecConfig {  // codec.hpp:26-31 (device: s = 16, S = 256, hierarchical)
+struct CodecConfig {  // codec.hpp:26-31 (device: S = 256, s in {8,16,32,64,128}, hierarchical or flat)
   std::uint32_t group_size = 16;
   std::uint32_t super_group_size = 256;
   bool hierarchical_scales = true;
@@ -106,8 +106,9 @@ struct CodecConfig {  // codec.hpp:26-31 (device: s = 16, S = 256, hierarchical)
     if (group_size == 0 || super_group_size % group_size != 0)
       throw std::invalid_argument("super-group size must be a positive multiple of the group size");
     if (super_group_size % 4 != 0) throw std::invalid_argument("super-group size must be a multiple of 4 for byte alignment");
-    if (group_size != 16 || super_group_size != 256 || !hierarchical_scales)
-      throw std::invalid_argument("device codec supports s=16, S=256 with hierarchical scales");
+    if (super_group_size != 256 ||
+        (group_size != 8 && group_size != 16 && group_size != 32 && group_size != 64 && group_size != 128))
+      throw std::invalid_argument("device codec supports S=256 with s in {8, 16, 32, 64, 128}");
   }
 };
 
@@ -161,12 +162,24 @@ inline CompressedChunk download(const uint8_t* dsoa, uint32_t chunk_index, Runs 
 inline dq_qctx qctx(const QuantContext& q) {
   return dq_qctx{q.seed.seed, q.seed.round, q.chunk_index, q.hop_slot, q.n_slots, q.correlated ? 1 : 0};
 }
+// the chunk primitives' scale format (CodecConfig) for the scope of one call
+struct FormatScope {
+  std::uint32_t gs = 16;
+  int hier = 1;
+  explicit FormatScope(const CodecConfig& c) {
+    check(dq_codec_format_set(c.group_size, c.hierarchical_scales ? 1 : 0, &gs, &hier));
+  }
+  ~FormatScope() { dq_codec_format_set(gs, hier, nullptr, nullptr); }
+  FormatScope(const FormatScope&) = delete;
+  FormatScope& operator=(const FormatScope&) = delete;
+};
 }  // namespace detail
 
 inline CompressedChunk compress_chunk(std::span<const float> values, std::span<const std::uint8_t> widths,
                                       const CodebookSet& books, const CodecConfig& cfg, const QuantContext& q,
                                       std::uint32_t first_sg_index) {
   cfg.validate();
+  const detail::FormatScope fmt(cfg);
   if (values.size() != widths.size() * cfg.super_group_size)
     throw std::invalid_argument("chunk length does not match widths");
   const detail::Runs r = detail::runs_of(widths);
@@ -183,6 +196,7 @@ inline CompressedChunk decompress_accumulate_recompress(const CompressedChunk& c
                                                         const CodebookSet& books, const CodecConfig& cfg,
                                                         const QuantContext& q, std::uint32_t first_sg_index) {
   cfg.validate();
+  const detail::FormatScope fmt(cfg);
   detail::Runs r;
   auto in = detail::upload(chunk, &r);
   if (local.size() != r.count() * 256) throw std::invalid_argument("local buffer length does not match chunk");
@@ -198,6 +212,7 @@ inline CompressedChunk decompress_accumulate_recompress(const CompressedChunk& c
 inline void decompress_chunk(const CompressedChunk& chunk, const CodebookSet& books, const CodecConfig& cfg,
                              std::span<float> out) {
   cfg.validate();
+  const detail::FormatScope fmt(cfg);
   detail::Runs r;
   auto in = detail::upload(chunk, &r);
   if (out.size() != r.count() * 256) throw std::invalid_argument("output length does not match chunk");
@@ -209,6 +224,7 @@ inline void decompress_chunk(const CompressedChunk& chunk, const CodebookSet& bo
 inline void decompress_accumulate(const CompressedChunk& chunk, std::span<float> acc, const CodebookSet& books,
                                   const CodecConfig& cfg) {
   cfg.validate();
+  const detail::FormatScope fmt(cfg);
   detail::Runs r;
   auto in = detail::upload(chunk, &r);
   if (acc.size() != r.count() * 256) throw std::invalid_argument("accumulator length does not match chunk");
@@ -220,11 +236,13 @@ inline void decompress_accumulate(const CompressedChunk& chunk, std::span<float>
 
 inline std::vector<std::uint8_t> serialize_chunk(const CompressedChunk& chunk, const CodecConfig& cfg) {
   cfg.validate();
+  const detail::FormatScope fmt(cfg);
   return chunk.wire;
 }
 
 inline CompressedChunk parse_chunk(std::span<const std::uint8_t> bytes, const CodecConfig& cfg) {  // strict
   cfg.validate();
+  const detail::FormatScope fmt(cfg);
   CompressedChunk c;
   c.wire.assign(bytes.begin(), bytes.end());
   std::vector<uint8_t> soa(bytes.size() * 2 + 64);
@@ -359,10 +377,33 @@ struct PipelineConfig {  // engine.hpp:22-43
   unsigned threads = 1;
 };
 
+// metrics.hpp:20-40 WireVolume: the round's wire accounting by phase and field
+struct WireVolume {
+  std::uint64_t stats_bits = 0;    // stats all-reduce, 2 x 32 per super-group per hop
+  std::uint64_t payload_bits = 0;  // packed entries over all transmissions
+  std::uint64_t scale_bits = 0;    // group + super-group scales over all transmissions
+  std::uint64_t header_bits = 0;   // chunk headers over all transmissions
+  std::uint64_t repr_bits = 0;     // per compression event (forwarded copies excluded)
+  std::uint64_t compressed_coordinates = 0;
+  std::uint64_t transmitted_coordinates = 0;
+  std::uint64_t total_bits() const { return stats_bits + payload_bits + scale_bits + header_bits; }
+  // metrics.cpp:39-43 (also as the free function below)
+  double bits_per_coordinate() const {
+    return compressed_coordinates == 0 ? 0.0
+                                       : static_cast<double>(repr_bits) / static_cast<double>(compressed_coordinates);
+  }
+};
+inline double bits_per_coordinate(const WireVolume& w) { return w.bits_per_coordinate(); }
+inline double stats_phase_fraction(const WireVolume& w) {  // metrics.cpp:45-49
+  return w.transmitted_coordinates == 0 ? 0.0
+                                        : static_cast<double>(w.stats_bits) / (16.0 * static_cast<double>(w.transmitted_coordinates));
+}
+
 struct RoundResult {  // engine.hpp:45-54 (exact sum / hop errors: reference-side diagnostics)
   std::vector<float> synced;
   double vnmse = 0.0;
   double mse = 0.0;
+  WireVolume wire;
   std::uint64_t wire_hash = 0;
   BitAllocation allocation;
   dq_round_info info{};
@@ -411,6 +452,13 @@ inline RoundResult run_round(const std::vector<std::vector<float>>& worker_value
   r.vnmse = r.info.vnmse;
   r.mse = r.info.mse;
   r.wire_hash = r.info.wire_hash;
+  r.wire.stats_bits = r.info.stats_bits;
+  r.wire.payload_bits = r.info.wire_payload_bits;
+  r.wire.scale_bits = r.info.scale_bits;
+  r.wire.header_bits = r.info.header_bits;
+  r.wire.repr_bits = r.info.repr_bits;
+  r.wire.compressed_coordinates = r.info.compressed_coordinates;
+  r.wire.transmitted_coordinates = r.info.transmitted_coordinates;
   r.allocation.u = r.info.u;
   r.allocation.payload_bits = r.info.payload_bits;
   if (n > 1) {

@@ -64,7 +64,8 @@ class QuantContext:
 
 @dataclass
 class CodecConfig:
-    """proj/include/dynamiq/codec.hpp:26-31 (device: s=16, S=256, hierarchical)"""
+    """proj/include/dynamiq/codec.hpp:26-31 (device: S = 256, s in {8,16,32,64,128},
+    hierarchical u8 + bf16 or flat bf16 group scales)"""
     group_size: int = 16
     super_group_size: int = 256
     hierarchical_scales: bool = True
@@ -73,8 +74,25 @@ class CodecConfig:
     def validate(self) -> None:
         if self.group_size == 0 or self.super_group_size % self.group_size or self.super_group_size % 4:
             raise InvalidArgument(2, "super-group size must be a positive multiple of the group size")
-        if (self.group_size, self.super_group_size, self.hierarchical_scales) != (16, 256, True):
-            raise InvalidArgument(2, "device codec supports s=16, S=256 with hierarchical scales")
+        if self.super_group_size != 256 or self.group_size not in (8, 16, 32, 64, 128):
+            raise InvalidArgument(2, "device codec supports S=256 with s in {8, 16, 32, 64, 128}")
+
+
+class _Format:
+    """Scale format of this thread's chunk primitives for the duration of a call
+    (dq_codec_format_set)."""
+
+    def __init__(self, group_size: int = 16, hierarchical: bool = True):
+        self.gs, self.hier = group_size, hierarchical
+
+    def __enter__(self):
+        pg, ph = C.c_uint32(), C.c_int()
+        check(lib().dq_codec_format_set(self.gs, int(self.hier), C.byref(pg), C.byref(ph)))
+        self.prev = (pg.value, ph.value)
+        return self
+
+    def __exit__(self, *exc):
+        lib().dq_codec_format_set(self.prev[0], self.prev[1], None, None)
 
 
 @dataclass
@@ -115,6 +133,11 @@ class DeviceChunk:
     n2: int
     data: torch.Tensor  # uint8, dq_chunk_bytes(n8, n4, n2, n16)
     n16: int = 0
+    group_size: int = 16         # scale format (CodecConfig) the chunk was written with
+    hierarchical: bool = True
+
+    def fmt(self) -> _Format:
+        return _Format(self.group_size, self.hierarchical)
 
     @property
     def n_sg(self) -> int:
@@ -165,14 +188,20 @@ def _f32(t: torch.Tensor, n: int, what: str) -> torch.Tensor:
     return t
 
 
-def chunk_bytes(n8: int, n4: int, n2: int, n16: int = 0) -> int:
-    """Device chunk bytes (dq tiled SoA)."""
-    return lib().dq_chunk_bytes(n8, n4, n2, n16)
+def chunk_bytes(n8: int, n4: int, n2: int, n16: int = 0, cfg: Optional[CodecConfig] = None) -> int:
+    """Device chunk bytes (dq tiled SoA) in cfg's scale format (default s=16 hierarchical)."""
+    with _fmt_of(cfg):
+        return lib().dq_chunk_bytes(n8, n4, n2, n16)
 
 
-def wire_bytes(n8: int, n4: int, n2: int, n16: int = 0) -> int:
+def wire_bytes(n8: int, n4: int, n2: int, n16: int = 0, cfg: Optional[CodecConfig] = None) -> int:
     """Reference serialize_chunk bytes incl. the 24-byte header (codec.cpp:268-291)."""
-    return lib().dq_wire_bytes(n8, n4, n2, n16)
+    with _fmt_of(cfg):
+        return lib().dq_wire_bytes(n8, n4, n2, n16)
+
+
+def _fmt_of(cfg: Optional[CodecConfig]) -> _Format:
+    return _Format() if cfg is None else _Format(cfg.group_size, cfg.hierarchical_scales)
 
 
 def compressed_size_bits(widths, S: int = 256, s: int = 16, hierarchical_scales: bool = True) -> int:
@@ -187,11 +216,12 @@ def compress_chunk(values: torch.Tensor, widths, cfg: CodecConfig, qctx: QuantCo
     cfg.validate()
     n8, n4, n2, n16 = _runs(widths)
     v = _f32(values, (n8 + n4 + n2 + n16) * 256, "chunk")
-    out = torch.empty(max(chunk_bytes(n8, n4, n2, n16), 1), dtype=torch.uint8, device=v.device)
+    out = torch.empty(max(chunk_bytes(n8, n4, n2, n16, cfg), 1), dtype=torch.uint8, device=v.device)
     q = qctx._c()
-    check(lib().dq_compress_chunk(_ptr(v), n8, n4, n2, n16, C.byref(q), first_sg_index, int(cfg.non_uniform),
-                                  _ptr(out), _stream()))
-    return DeviceChunk(qctx.chunk_index, n8, n4, n2, out, n16)
+    with _fmt_of(cfg):
+        check(lib().dq_compress_chunk(_ptr(v), n8, n4, n2, n16, C.byref(q), first_sg_index, int(cfg.non_uniform),
+                                      _ptr(out), _stream()))
+    return DeviceChunk(qctx.chunk_index, n8, n4, n2, out, n16, cfg.group_size, cfg.hierarchical_scales)
 
 
 def decompress_accumulate_recompress(chunk: DeviceChunk, local: torch.Tensor, cfg: CodecConfig,
@@ -200,9 +230,11 @@ def decompress_accumulate_recompress(chunk: DeviceChunk, local: torch.Tensor, cf
     loc = _f32(local, chunk.n_sg * 256, "local buffer")
     out = torch.empty_like(chunk.data)
     q = qctx._c()
-    check(lib().dq_dar_chunk(_ptr(chunk.data), _ptr(loc), *chunk.runs, C.byref(q),
-                             first_sg_index, int(cfg.non_uniform), _ptr(out), _stream()))
-    return DeviceChunk(qctx.chunk_index, chunk.n8, chunk.n4, chunk.n2, out, chunk.n16)
+    with _fmt_of(cfg):
+        check(lib().dq_dar_chunk(_ptr(chunk.data), _ptr(loc), *chunk.runs, C.byref(q),
+                                 first_sg_index, int(cfg.non_uniform), _ptr(out), _stream()))
+    return DeviceChunk(qctx.chunk_index, chunk.n8, chunk.n4, chunk.n2, out, chunk.n16, cfg.group_size,
+                       cfg.hierarchical_scales)
 
 
 def decompress_accumulate(chunk: DeviceChunk, acc: torch.Tensor, cfg: CodecConfig) -> None:
@@ -212,8 +244,9 @@ def decompress_accumulate(chunk: DeviceChunk, acc: torch.Tensor, cfg: CodecConfi
         raise InvalidArgument(2, "accumulator must be a contiguous, aligned CUDA float32 tensor")
     if acc.numel() != chunk.n_sg * 256:
         raise InvalidArgument(2, "accumulator length does not match chunk")
-    check(lib().dq_da_chunk(_ptr(chunk.data), _ptr(acc), *chunk.runs, int(cfg.non_uniform),
-                            _stream()))
+    with _fmt_of(cfg):
+        check(lib().dq_da_chunk(_ptr(chunk.data), _ptr(acc), *chunk.runs, int(cfg.non_uniform),
+                                _stream()))
 
 
 def decompress_chunk(chunk: DeviceChunk, cfg: CodecConfig, out: Optional[torch.Tensor] = None) -> torch.Tensor:
@@ -222,60 +255,66 @@ def decompress_chunk(chunk: DeviceChunk, cfg: CodecConfig, out: Optional[torch.T
         out = torch.empty(chunk.n_sg * 256, dtype=torch.float32, device=chunk.data.device)
     elif out.numel() != chunk.n_sg * 256:
         raise InvalidArgument(2, "output length does not match chunk")
-    check(lib().dq_decompress_chunk(_ptr(chunk.data), _ptr(out), *chunk.runs,
-                                    int(cfg.non_uniform), _stream()))
+    with _fmt_of(cfg):
+        check(lib().dq_decompress_chunk(_ptr(chunk.data), _ptr(out), *chunk.runs,
+                                        int(cfg.non_uniform), _stream()))
     return out
 
 
 def serialize_chunk(chunk: DeviceChunk, device: bool = False):
     """Reference wire bytes (proj/src/codec.cpp:319-343): host ``bytes``, or with
     ``device=True`` a CUDA uint8 tensor serialized on the GPU (dq_serialize_chunk)."""
-    if device:
-        out = torch.empty(wire_bytes(*chunk.runs), dtype=torch.uint8,
-                          device=chunk.data.device)
-        check(lib().dq_serialize_chunk(_ptr(chunk.data), chunk.chunk_index, *chunk.runs,
-                                       _ptr(out), _stream()))
-        return out
-    soa = chunk.data.cpu().numpy()
-    out = np.zeros(wire_bytes(*chunk.runs), np.uint8)
-    check(lib().dq_to_reference_wire(soa.ctypes.data_as(C.c_void_p), chunk.chunk_index, *chunk.runs,
-                                     out.ctypes.data_as(C.c_void_p)))
-    return out.tobytes()
+    with chunk.fmt():
+        if device:
+            out = torch.empty(lib().dq_wire_bytes(*chunk.runs), dtype=torch.uint8, device=chunk.data.device)
+            check(lib().dq_serialize_chunk(_ptr(chunk.data), chunk.chunk_index, *chunk.runs,
+                                           _ptr(out), _stream()))
+            return out
+        soa = chunk.data.cpu().numpy()
+        out = np.zeros(lib().dq_wire_bytes(*chunk.runs), np.uint8)
+        check(lib().dq_to_reference_wire(soa.ctypes.data_as(C.c_void_p), chunk.chunk_index, *chunk.runs,
+                                         out.ctypes.data_as(C.c_void_p)))
+        return out.tobytes()
 
 
-def soa_from_reference(buf: bytes):
+def soa_from_reference(buf: bytes, cfg: Optional[CodecConfig] = None):
     """Strict parse of reference wire bytes into the device layout (host numpy array)
     -> (chunk_index, n8, n4, n2, n16, soa)."""
     b = np.frombuffer(buf, np.uint8).copy()
     count = int(np.frombuffer(b[4:8].tobytes(), np.uint32)[0]) if b.size >= 8 else 0
-    cap = max(len(buf) + 32 * min(count, len(buf)), 1)  # passthrough records carry no scales on the wire
+    cap = max(len(buf) + 64 * min(count, len(buf)), 1)  # passthrough records carry no scales on the wire
     soa = np.zeros(cap, np.uint8)
     ci, n8, n4, n2, n16 = (C.c_uint32() for _ in range(5))
-    check(lib().dq_from_reference_wire(b.ctypes.data_as(C.c_void_p), b.size, soa.ctypes.data_as(C.c_void_p),
-                                       soa.size, C.byref(ci), C.byref(n8), C.byref(n4), C.byref(n2), C.byref(n16)))
+    with _fmt_of(cfg):
+        check(lib().dq_from_reference_wire(b.ctypes.data_as(C.c_void_p), b.size, soa.ctypes.data_as(C.c_void_p),
+                                           soa.size, C.byref(ci), C.byref(n8), C.byref(n4), C.byref(n2),
+                                           C.byref(n16)))
     runs = (n8.value, n4.value, n2.value, n16.value)
-    return (ci.value,) + runs + (soa[: chunk_bytes(*runs)],)
+    return (ci.value,) + runs + (soa[: chunk_bytes(*runs, cfg=cfg)],)
 
 
-def parse_chunk(buf, device="cuda") -> DeviceChunk:
+def parse_chunk(buf, device="cuda", cfg: Optional[CodecConfig] = None) -> DeviceChunk:
     """proj/src/codec.cpp:345-399 — raises MalformedBuffer on any malformed buffer.
 
     ``buf``: host bytes (parsed on the host), or a CUDA uint8 tensor (parsed and
-    validated on the GPU by dq_parse_chunk)."""
+    validated on the GPU by dq_parse_chunk); ``cfg``: the scale format (default s=16,
+    hierarchical), like the reference's CodecConfig argument."""
+    gs, hier = (16, True) if cfg is None else (cfg.group_size, cfg.hierarchical_scales)
     if isinstance(buf, torch.Tensor):
         if not (buf.is_cuda and buf.dtype == torch.uint8 and buf.is_contiguous()):
             raise InvalidArgument(2, "device wire buffer must be a contiguous CUDA uint8 tensor")
         ci, n8, n4, n2, n16 = (C.c_uint32() for _ in range(5))
         outs = (C.byref(ci), C.byref(n8), C.byref(n4), C.byref(n2), C.byref(n16))
         # validate and read the run lengths, then parse into a buffer of the device size
-        check(lib().dq_parse_chunk(_ptr(buf), buf.numel(), None, 0, *outs, _stream()))
-        runs = (n8.value, n4.value, n2.value, n16.value)
-        data = torch.empty(max(chunk_bytes(*runs), 1), dtype=torch.uint8, device=buf.device)
-        check(lib().dq_parse_chunk(_ptr(buf), buf.numel(), _ptr(data), data.numel(), *outs, _stream()))
-        return DeviceChunk(ci.value, n8.value, n4.value, n2.value, data, n16.value)
-    ci, n8, n4, n2, n16, soa = soa_from_reference(buf)
+        with _fmt_of(cfg):
+            check(lib().dq_parse_chunk(_ptr(buf), buf.numel(), None, 0, *outs, _stream()))
+            runs = (n8.value, n4.value, n2.value, n16.value)
+            data = torch.empty(max(lib().dq_chunk_bytes(*runs), 1), dtype=torch.uint8, device=buf.device)
+            check(lib().dq_parse_chunk(_ptr(buf), buf.numel(), _ptr(data), data.numel(), *outs, _stream()))
+        return DeviceChunk(ci.value, n8.value, n4.value, n2.value, data, n16.value, gs, hier)
+    ci, n8, n4, n2, n16, soa = soa_from_reference(buf, cfg)
     data = torch.from_numpy(soa.copy() if soa.size else np.zeros(1, np.uint8)).to(device)
-    return DeviceChunk(ci, n8, n4, n2, data, n16)
+    return DeviceChunk(ci, n8, n4, n2, data, n16, gs, hier)
 
 
 def compute_stats(x: torch.Tensor):

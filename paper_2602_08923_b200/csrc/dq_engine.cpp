@@ -13,7 +13,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
+#include <chrono>
 #include <mutex>
+#include <thread>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -198,7 +201,7 @@ struct PeerMem {
 struct StatsMem {
   uint8_t* base = nullptr;
   std::vector<uint8_t*> peer;
-  uint32_t n = 0, T = 0, epoch = 0;
+  uint32_t n = 0, T = 0, epoch = 0;  // T: row capacity (grow-only, headroom): rounds of any T <= it reuse the area
   size_t rows() const { return 4ull * n * T; }  // bytes of one [n][T] float array
   float* mean(uint8_t* b, uint32_t par, uint32_t r) const {
     return reinterpret_cast<float*>(b + 2ull * par * rows()) + static_cast<size_t>(r) * T;
@@ -238,12 +241,12 @@ struct dq_ctx {
   uint32_t* h_counts = nullptr;
   // asynchronous allocation (no host sync inside a round): per round parity a mapped
   // mailbox the search mirrors its state into, a mapped copy of F for the rare rounds the
-  // host must finish, and the side stream running the host function that does so
+  // host must finish, and the service thread that does so
   HostMsg* hmsg = nullptr;   // [2]
   float* hF = nullptr;
   size_t hF_cap = 0;
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  std::thread svc;           // answers need_host requests (polls the mailboxes; idle otherwise)
+  std::atomic<bool> svc_stop{false};
   uint32_t apar = 0;
   bool async_alloc = true;   // env DQ_SYNC_ALLOC=1: host-synchronous allocation (round-1 behaviour)
   const float** h_xptrs = nullptr;  // pinned worker-pointer tables [2][64] (capture-safe H2D)
@@ -297,12 +300,13 @@ struct dq_ctx {
     if (pm.base) cudaFree(pm.base);
     if (sm.base) cudaFree(sm.base);
     if (h_state) cudaFreeHost(h_state);
+    if (svc.joinable()) {
+      svc_stop = true;
+      svc.join();
+    }
     if (hmsg) cudaFreeHost(hmsg);
     if (hF) cudaFreeHost(hF);
     if (h_xptrs) cudaFreeHost(h_xptrs);
-    if (side) cudaStreamDestroy(side);
-    if (ev_fork) cudaEventDestroy(ev_fork);
-    if (ev_join) cudaEventDestroy(ev_join);
     if (h_counts) cudaFreeHost(h_counts);
     if (h_vn) cudaFreeHost(h_vn);
     if (ev0) cudaEventDestroy(ev0);
@@ -799,13 +803,10 @@ bool host_allocate_fast(const float* F, uint32_t T, uint32_t S, double budget, d
   return true;
 }
 
-// Host function of an asynchronous round (side stream, after the search): nothing to do
-// unless the search handed the decision to the host; then finish it from the exported F
-// and release the assignment kernel, which waits for `resolved` to reach the round's epoch.
-void CUDART_CB host_alloc_resolve(void* p) {
-  HostMsg* m = static_cast<HostMsg*>(p);
+// The host side of a need_host round: finish the allocation from the exported F and
+// release the assignment kernel, which waits for `resolved` to reach the round's epoch.
+void host_alloc_resolve(HostMsg* m) {
   const AllocState& s = m->state;
-  if (!s.need_host) return;
   double u = 0.0;
   float a = INFINITY, b = INFINITY;  // infeasible: all width 2 (the round is reported as failed)
   const bool ok = host_allocate_fast(m->hF, s.T, s.S, s.budget, &u, &a, &b);
@@ -816,13 +817,27 @@ void CUDART_CB host_alloc_resolve(void* p) {
   __atomic_store_n(const_cast<uint32_t*>(&m->resolved), s.epoch, __ATOMIC_RELEASE);
 }
 
+// Per-context host service thread: polls both mailboxes for a request newer than its
+// answer (no CUDA calls, no per-round callbacks: the common round never involves the host).
+void alloc_service(dq_ctx* ctx) {
+  while (!ctx->svc_stop.load(std::memory_order_relaxed)) {
+    bool busy = false;
+    for (int p = 0; p < 2; ++p) {
+      HostMsg* m = ctx->hmsg + p;
+      const uint32_t req = __atomic_load_n(const_cast<uint32_t*>(&m->request), __ATOMIC_ACQUIRE);
+      if (req != 0 && req != m->resolved && req == m->state.epoch) {
+        host_alloc_resolve(m);
+        busy = true;
+      }
+    }
+    if (!busy) std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+}
+
 void ensure_mailbox(dq_ctx* ctx, uint32_t T) {
   if (!ctx->hmsg) {
     DQ_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx->hmsg), 2 * sizeof(HostMsg), cudaHostAllocMapped));
     std::memset(static_cast<void*>(ctx->hmsg), 0, 2 * sizeof(HostMsg));
-    DQ_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
-    DQ_CUDA(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
-    DQ_CUDA(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
   }
   if (ctx->hF_cap < T) {
     DQ_CUDA(cudaDeviceSynchronize());  // growing: no round may still write the old copy
@@ -834,6 +849,7 @@ void ensure_mailbox(dq_ctx* ctx, uint32_t T) {
     ctx->hmsg[0].hF = ctx->hF;
     ctx->hmsg[1].hF = ctx->hF;
   }
+  if (!ctx->svc.joinable()) ctx->svc = std::thread(alloc_service, ctx);
 }
 
 // allocate_fast + build_permutation with no host synchronisation: the search decides and
@@ -865,10 +881,6 @@ AllocResult allocate_fast_async(dq_ctx* ctx, const dq_config& c, const float* dF
   w.hmsg = static_cast<HostMsg*>(dm);
   w.hF = static_cast<float*>(dF_host);
   DQ_CUDA(launch_alloc_search(dF, T, kAlpha, static_cast<uint64_t>(W), budget, S, w, st));
-  DQ_CUDA(cudaEventRecord(ctx->ev_fork, st));
-  DQ_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
-  DQ_CUDA(cudaLaunchHostFunc(ctx->side, host_alloc_resolve, m));
-  DQ_CUDA(cudaEventRecord(ctx->ev_join, ctx->side));
   launch_alloc_assign(dF, T, 0.f, 0.f, true, w, dW, dP, st);
   DQ_CUDA(cudaGetLastError());
   return r;
@@ -1270,7 +1282,6 @@ void sim_round(dq_ctx* ctx, const float* const* xs, size_t d, float* out, int fl
     if (k) timed(ctx, K_DECODE, gbytes, st, [&] { launch_gather_decode(g, k, max_nsg_g, st); });
     DQ_CUDA(cudaGetLastError());
   }
-  if (async) DQ_CUDA(cudaStreamWaitEvent(st, ctx->ev_join, 0));  // the round's host function has returned
   DQ_CUDA(cudaEventRecord(ctx->ev1, st));
   if (flags & DQ_SIM_NO_METRICS) {  // asynchronous return: timing resolved at the next sync point
     finish_async(ctx, info, st);
@@ -1481,17 +1492,18 @@ bool peer_setup(dq_ctx* ctx, size_t mb, uint32_t max_nsg, uint32_t ninbox, uint3
 }
 
 // The statistics exchange area (collective, same decision on every rank: T and n are
-// round-global).  Rebuilt when T or n changes.
+// round-global).  Sized by capacity with headroom (rows stride sm.T >= the round's T), so
+// the varying bucket sizes of a DDP step reuse it; rebuilt only when n changes or T outgrows it.
 bool stats_setup(dq_ctx* ctx, uint32_t T, cudaStream_t st) {
   StatsMem& sm = ctx->sm;
   const uint32_t n = ctx->cfg.n_workers;
-  if (sm.base && sm.n == n && sm.T == T) return true;
+  if (sm.base && sm.n == n && T <= sm.T) return true;
   DQ_CUDA(cudaStreamSynchronize(st));
   dq_ctx::close_map(sm.peer, sm.base);
   uint8_t* old = sm.base;
   sm.base = nullptr;
   sm.n = n;
-  sm.T = T;
+  sm.T = std::max<uint32_t>(T + T / 4 + 64, 4096u);
   DQ_CUDA(cudaMalloc(&sm.base, sm.total()));
   DQ_CUDA(cudaMemsetAsync(sm.base + 4 * sm.rows(), 0, sm.total() - 4 * sm.rows(), st));
   ctx->sdone.reserve(1);
@@ -1724,6 +1736,17 @@ void butterfly_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>
   peer_gather_decode(ctx, p, lays, decoded, out, d, epoch, st);
 }
 
+// NCCL reports errors of enqueued work (a dead peer, a network failure) asynchronously
+// (§5 failure detection): poll the communicator before each round and after the NCCL
+// transport's last enqueue.
+void check_nccl_async(dq_ctx* ctx) {
+  if (!ctx->comm) return;
+  ncclResult_t e = ncclSuccess;
+  DQ_NCCL(ncclCommGetAsyncError(ctx->comm, &e));
+  if (e != ncclSuccess && e != ncclInProgress)
+    throw Error(DQ_ENCCL, std::string("NCCL asynchronous error: ") + ncclGetErrorString(e));
+}
+
 void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info* info, cudaStream_t st) {
   const dq_config& c = ctx->cfg;
   const uint32_t n = c.n_workers, me = static_cast<uint32_t>(ctx->rank);
@@ -1734,6 +1757,8 @@ void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info
     return;
   }
   if (!ctx->comm) invalid("dq_comm_init has not been called");
+  if (n != static_cast<uint32_t>(ctx->nranks)) invalid("n_workers must equal the communicator's rank count");
+  check_nccl_async(ctx);  // a failure of an earlier round's NCCL work surfaces here
   if (reinterpret_cast<uintptr_t>(x) % 16 || reinterpret_cast<uintptr_t>(out) % 16)
     invalid("buffers must be 16-byte aligned");
   const uint32_t T = static_cast<uint32_t>((d + 255) / 256);
@@ -1766,7 +1791,7 @@ void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info
     sp.epoch = ep;
     timed(ctx, K_STATS, 4.0 * d + 8.0 * T * n, st, [&] { launch_stats_peer(dxp, d, T, sp, st); });
     timed(ctx, K_REDUCE, 8.0 * (n + 1) * T, st, [&] {
-      launch_reduce_stats_peer(sm.mean(sm.base, par, 0), sm.sq(sm.base, par, 0), sm.flags(sm.base, par), ep, n, T,
+      launch_reduce_stats_peer(sm.mean(sm.base, par, 0), sm.sq(sm.base, par, 0), sm.flags(sm.base, par), ep, n, T, sm.T,
                                ctx->gmean.p, ctx->gsq.p, st);
     });
   } else {
@@ -1826,7 +1851,6 @@ void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info
     else butterfly_peer(ctx, p, bases, lays, plans, max_nsg, out, d, st);
     if (!p.a.async) account_round(info, p.a, p.lo, n, c.topology);
     DQ_CUDA(cudaGetLastError());
-    if (p.a.async) DQ_CUDA(cudaStreamWaitEvent(st, ctx->ev_join, 0));  // the round's host function has returned
     DQ_CUDA(cudaEventRecord(ctx->ev1, st));
     finish_async(ctx, info, st);
     return;
@@ -2008,6 +2032,7 @@ void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info
     info->stats_bits += static_cast<uint64_t>(plans[ch].red.size() + plans[ch].n_gat) * 64ull * lays[ch].nsg;
   }
   DQ_CUDA(cudaGetLastError());
+  check_nccl_async(ctx);
   DQ_CUDA(cudaEventRecord(ctx->ev1, st));
   finish_async(ctx, info, st);
 }
@@ -2065,15 +2090,39 @@ int dq_ctx_set_config(dq_ctx* ctx, const dq_config* cfg) {
   return guarded([&] {
     if (!ctx || !cfg) invalid("null argument");
     validate(*cfg);
+    // a communicator fixes the worker count: its regions, handles and NCCL ranks are sized by it
+    if (ctx->comm && cfg->n_workers != static_cast<uint32_t>(ctx->nranks))
+      invalid("n_workers must equal the communicator's rank count");
     ctx->cfg = *cfg;
   });
 }
+
+// Scale format of this thread's chunk primitives (dq_codec_format_set; default s = 16,
+// hierarchical): the reference's CodecConfig{group_size, hierarchical_scales}.
+thread_local uint32_t t_prim_gs = 16;
+thread_local int t_prim_hier = 1;
 
 static Layout runs_layout(uint32_t n8, uint32_t n4, uint32_t n2, uint32_t n16) {
   if (static_cast<uint64_t>(n8) + n4 + n2 + n16 > 0xffffffffull) invalid("too many super-groups");
   Layout L{n8 + n4 + n2 + n16, n8, n4};
   L.n16 = n16;
+  dq_config c;
+  dq_config_default(&c);
+  c.group_size = t_prim_gs;
+  c.hierarchical_scales = t_prim_hier;
+  set_format(L, c);
   return L;
+}
+
+int dq_codec_format_set(uint32_t group_size, int hierarchical, uint32_t* prev_group_size, int* prev_hierarchical) {
+  return guarded([&] {
+    if (group_size != 8 && group_size != 16 && group_size != 32 && group_size != 64 && group_size != 128)
+      invalid("device codec supports group_size 8, 16, 32, 64 or 128");
+    if (prev_group_size) *prev_group_size = t_prim_gs;
+    if (prev_hierarchical) *prev_hierarchical = t_prim_hier;
+    t_prim_gs = group_size;
+    t_prim_hier = hierarchical ? 1 : 0;
+  });
 }
 
 size_t dq_chunk_bytes(uint32_t n8, uint32_t n4, uint32_t n2, uint32_t n16) {
@@ -2193,8 +2242,7 @@ int dq_parse_chunk(const void* d_wire, size_t len, void* d_soa, size_t soa_cap, 
     DQ_CUDA(cudaStreamSynchronize(st));
     const uint32_t count = h[1], r8 = h[2], r4 = h[3], r2 = h[4], r16 = h[5];
     if (static_cast<uint64_t>(r8) + r4 + r2 + r16 != count) mal("width run-lengths do not sum to the super-group count");
-    Layout L{count, r8, r4};
-    L.n16 = r16;
+    const Layout L = runs_layout(r8, r4, r2, r16);
     // super-groups whose record fits in len (codec.cpp:371-383 checks each before reading it)
     const uint64_t body = len - 24;
     uint32_t fit = count;
@@ -2231,7 +2279,8 @@ int dq_parse_chunk(const void* d_wire, size_t len, void* d_soa, size_t soa_cap, 
 
 int dq_from_reference_wire(const void* h_ref, size_t len, void* h_soa, size_t soa_cap,
                            uint32_t* chunk_index, uint32_t* n8, uint32_t* n4, uint32_t* n2, uint32_t* n16) {
-  // strict parser with the reference's checks (codec.cpp:345-399), S=256, s=16, hierarchical
+  // strict parser with the reference's checks (codec.cpp:345-399), S=256, this thread's scale
+  // format (dq_codec_format_set: s, hierarchical u8 + bf16 or flat bf16 group scales)
   return guarded([&] {
     const uint8_t* b = static_cast<const uint8_t*>(h_ref);
     auto mal = [](const char* m) { throw Error(DQ_EMALFORMED, std::string("malformed compressed buffer: ") + m); };
@@ -2243,8 +2292,8 @@ int dq_from_reference_wire(const void* h_ref, size_t len, void* h_soa, size_t so
     const uint32_t count = get32(4);
     const uint32_t r8 = get32(8), r4 = get32(12), r2 = get32(16), r16 = get32(20);
     if (static_cast<uint64_t>(r8) + r4 + r2 + r16 != count) mal("width run-lengths do not sum to the super-group count");
-    Layout L{count, r8, r4};
-    L.n16 = r16;
+    const Layout L = runs_layout(r8, r4, r2, r16);
+    const size_t meta = L.ss + L.gs;  // 2 + 16 default; flat: 0 + 2 * 256 / s
     size_t at = 24;
     for (uint32_t i = 0; i < count; ++i) {
       const uint32_t w = L.width(i);
@@ -2253,12 +2302,12 @@ int dq_from_reference_wire(const void* h_ref, size_t len, void* h_soa, size_t so
         at += 512;
         continue;
       }
-      const size_t rec = 18 + 32 * w;
+      const size_t rec = meta + 32 * w;
       if (len - at < rec) mal("truncated super-group body");
-      if ((b[at] | b[at + 1] << 8) == 0) {
-        for (size_t k = 2; k < 18; ++k)
+      if (L.ss && (b[at] | b[at + 1] << 8) == 0) {
+        for (size_t k = L.ss; k < meta; ++k)
           if (b[at + k]) mal("zero super-group scale with nonzero group scale");
-        for (size_t k = 18; k < rec; ++k)
+        for (size_t k = meta; k < rec; ++k)
           if (b[at + k]) mal("zero super-group scale with nonzero payload");
       }
       at += rec;
@@ -2270,16 +2319,16 @@ int dq_from_reference_wire(const void* h_ref, size_t len, void* h_soa, size_t so
     for (uint32_t i = 0; i < count; ++i) {
       const Layout::SG g = L.locate(i);
       if (g.width == 16) {  // reserved scale slots read as zero
-        std::memset(o + g.scale, 0, 2);
-        std::memset(o + g.codes, 0, 16);
+        std::memset(o + g.scale, 0, L.ss);
+        std::memset(o + g.codes, 0, L.gs);
         std::memcpy(o + g.payload, b + at, 512);
         at += 512;
         continue;
       }
-      std::memcpy(o + g.scale, b + at, 2);
-      std::memcpy(o + g.codes, b + at + 2, 16);
-      std::memcpy(o + g.payload, b + at + 18, 32 * g.width);
-      at += 18 + 32 * g.width;
+      std::memcpy(o + g.scale, b + at, L.ss);
+      std::memcpy(o + g.codes, b + at + L.ss, L.gs);
+      std::memcpy(o + g.payload, b + at + meta, 32 * g.width);
+      at += meta + 32 * g.width;
     }
     *chunk_index = get32(0);
     *n8 = r8;

@@ -129,7 +129,7 @@ struct StatsPeerArgs {
 void launch_stats_peer(const float* const* xs, uint64_t d, uint32_t T, const StatsPeerArgs& sp, cudaStream_t st);
 // reduction of the fused all-gather's rows after waiting for all n row flags == epoch
 void launch_reduce_stats_peer(const float* mean, const float* sq, const uint32_t* flags, uint32_t epoch,
-                              uint32_t n, uint32_t T, float* gm, float* gs, cudaStream_t st);
+                              uint32_t n, uint32_t T, uint32_t stride, float* gm, float* gs, cudaStream_t st);
 // rank-ordered fp64 reduction of [n][T] stats -> global [T]
 void launch_reduce_stats(const float* mean, const float* sq, uint32_t n, uint32_t T, float* gmean,
                          float* gsq, cudaStream_t st);
@@ -176,11 +176,13 @@ struct AllocState {
 };
 // Mapped (zero-copy) host memory shared by the allocation kernels and the host: the
 // search mirrors its final state here, the assignment its class counts; on need_host
-// rounds the search exports F and the host answers through `resolved`.
+// rounds the search exports F and raises `request`, the context's host service thread
+// answers through `resolved`.
 struct HostMsg {
   AllocState state;           // mirror of the search's final state (written by the kernel)
   const float* hF;            // host view of the exported F (set by the host)
   uint32_t counts[4];         // mirror of n8, n4, n2 (written by k_assign_scan)
+  volatile uint32_t request;  // epoch of a round that needs the host (written by the search kernel)
   volatile uint32_t resolved; // epoch of the last host answer
   int32_t host_status;        // 0 ok, 3 infeasible budget, 5 internal error (reported at the next sync)
   double u;                   // host answer: u, t24, t48

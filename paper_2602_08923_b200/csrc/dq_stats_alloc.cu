@@ -144,7 +144,7 @@ void launch_reduce_stats(const float* mean, const float* sq, uint32_t n, uint32_
 // The rank-ordered reduction over the fused all-gather's rows: each block first waits
 // (thread 0, acquire at system scope, g_spin_ns timeout -> trap) for every row's flag.
 __global__ void k_reduce_stats_peer(const float* mean, const float* sq, const uint32_t* flags, uint32_t epoch,
-                                    uint32_t n, uint32_t T, float* gm, float* gs) {
+                                    uint32_t n, uint32_t T, uint32_t stride, float* gm, float* gs) {
   if (threadIdx.x == 0) {
     for (uint32_t r = 0; r < n; ++r) {
       uint32_t v;
@@ -164,17 +164,17 @@ __global__ void k_reduce_stats_peer(const float* mean, const float* sq, const ui
   if (j >= T) return;
   double a = 0.0, b = 0.0;
   for (uint32_t r = 0; r < n; ++r) {
-    a = __dadd_rn(a, static_cast<double>(__ldcg(mean + static_cast<uint64_t>(r) * T + j)));
-    b = __dadd_rn(b, static_cast<double>(__ldcg(sq + static_cast<uint64_t>(r) * T + j)));
+    a = __dadd_rn(a, static_cast<double>(__ldcg(mean + static_cast<uint64_t>(r) * stride + j)));
+    b = __dadd_rn(b, static_cast<double>(__ldcg(sq + static_cast<uint64_t>(r) * stride + j)));
   }
   gm[j] = static_cast<float>(__ddiv_rn(a, static_cast<double>(n)));
   gs[j] = static_cast<float>(b);
 }
 
 void launch_reduce_stats_peer(const float* mean, const float* sq, const uint32_t* flags, uint32_t epoch,
-                              uint32_t n, uint32_t T, float* gm, float* gs, cudaStream_t st) {
+                              uint32_t n, uint32_t T, uint32_t stride, float* gm, float* gs, cudaStream_t st) {
   if (T == 0) return;
-  k_reduce_stats_peer<<<(T + 255) / 256, 256, 0, st>>>(mean, sq, flags, epoch, n, T, gm, gs);
+  k_reduce_stats_peer<<<(T + 255) / 256, 256, 0, st>>>(mean, sq, flags, epoch, n, T, stride, gm, gs);
 }
 
 // ------------------------------------------------------------ allocation
@@ -686,6 +686,12 @@ __global__ void __launch_bounds__(kAllocBins) k_alloc_coop(const float* __restri
     uint32_t* dst = reinterpret_cast<uint32_t*>(&w.hmsg->state);
     for (uint32_t k = threadIdx.x; k < sizeof(AllocState) / 4; k += blockDim.x) dst[k] = src[k];
     __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0 && st->need_host) {  // wake the host service thread (state and F are visible)
+      __threadfence_system();
+      w.hmsg->request = st->epoch;
+      __threadfence_system();
+    }
   }
 }
 

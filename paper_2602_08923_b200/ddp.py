@@ -47,7 +47,7 @@ class DynamiQHookState:
         return r
 
 
-def dynamiq_hook(state: DynamiQHookState, bucket: dist.GradBucket) -> torch.futures.Future:
+def dynamiq_hook(state: DynamiQHookState, bucket: dist.GradBucket) -> torch.futures.Future[torch.Tensor]:
     buf = bucket.buffer()
     caller = torch.cuda.current_stream()
     rnd = state.next_round()

@@ -159,6 +159,16 @@ TEST_CASE("run_round pins the reference's wire_hash (SURVEY Appendix A)") {
   dqo_run_round(ptrs.data(), d, &oc, synced.data(), nullptr, nullptr, &oo);
   CHECK(res.synced == synced);
   CHECK(res.allocation.u == oo.u);
+  // RoundResult.wire (engine.hpp:45-54, metrics.hpp:20-40) like the reference's accounting
+  CHECK(res.wire.payload_bits == oo.wire_payload_bits);
+  CHECK(res.wire.scale_bits == oo.scale_bits);
+  CHECK(res.wire.stats_bits == oo.stats_bits);
+  CHECK(res.wire.header_bits == oo.header_bits);
+  CHECK(res.wire.repr_bits == oo.repr_bits);
+  CHECK(res.wire.total_bits() == oo.stats_bits + oo.wire_payload_bits + oo.scale_bits + oo.header_bits);
+  CHECK(res.wire.bits_per_coordinate() ==
+        static_cast<double>(oo.repr_bits) / static_cast<double>(oo.compressed_coordinates));
+  CHECK(bits_per_coordinate(res.wire) == res.wire.bits_per_coordinate());
 }
 
 TEST_CASE("single worker is an exact no-op; b=2 is infeasible") {

@@ -41,6 +41,8 @@ def main():
     cases += [("ring", 1 << 16, 5.0, "peer", flat32), ("butterfly", (1 << 18) + 77, 5.0, "peer", flat32),
               ("ring", 1 << 16, 4.0, "peer", {"allocator": dq.KIND_GENERAL}),
               ("ring", (1 << 20) + 5, 4.0, "peer", {"allocator": dq.KIND_GENERAL, "correlated": False})]
+    if os.environ.get("DIST_CHECK_SMALL"):  # under compute-sanitizer: the small cases only
+        cases = [c for c in cases if c[1] <= (1 << 16) + 300]
     comms = {}
     for topo, d, b, transport, extra in cases:
         if topo == "butterfly" and world & (world - 1):
