@@ -230,7 +230,6 @@ struct dq_ctx {
   DevBuf<uint8_t> gtemp;                 // CUB scratch
   DevBuf<int> gnum;
   DevBuf<double> gbase;
-  DevBuf<const float*> xptrs;
   DevBuf<double> vn;
   DevBuf<uint8_t> msgs;   // message pool
   DevBuf<float> accs;     // per-worker chunk accumulators (butterfly)
@@ -249,8 +248,6 @@ struct dq_ctx {
   std::atomic<bool> svc_stop{false};
   uint32_t apar = 0;
   bool async_alloc = true;   // env DQ_SYNC_ALLOC=1: host-synchronous allocation (round-1 behaviour)
-  const float** h_xptrs = nullptr;  // pinned worker-pointer tables [2][64] (capture-safe H2D)
-  uint32_t xpar = 0;
   // what the last round needs to fill dq_round_info once it has completed
   struct RoundRec {
     bool valid = false, async = false;
@@ -306,7 +303,6 @@ struct dq_ctx {
     }
     if (hmsg) cudaFreeHost(hmsg);
     if (hF) cudaFreeHost(hF);
-    if (h_xptrs) cudaFreeHost(h_xptrs);
     if (h_counts) cudaFreeHost(h_counts);
     if (h_vn) cudaFreeHost(h_vn);
     if (ev0) cudaEventDestroy(ev0);
@@ -1079,16 +1075,6 @@ void finish_info(dq_ctx* ctx, dq_round_info* info) {
   account_round(info, a, rec.lo, rec.n, rec.topology);
 }
 
-// Worker-pointer table of a round -> device (parity-double-buffered, through pinned host
-// memory so the copy is stream-ordered and capturable in a CUDA graph)
-void upload_ptrs(dq_ctx* ctx, const float* const* xs, uint32_t n, cudaStream_t st) {
-  if (!ctx->h_xptrs) DQ_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_xptrs), 2 * 64 * sizeof(float*)));
-  ctx->xpar ^= 1u;
-  const float** h = ctx->h_xptrs + 64 * ctx->xpar;
-  for (uint32_t r = 0; r < n; ++r) h[r] = xs[r];
-  DQ_CUDA(cudaMemcpyAsync(ctx->xptrs.p + 64 * ctx->xpar, h, n * sizeof(float*), cudaMemcpyHostToDevice, st));
-}
-
 // ---------------------------------------------------------- simulation
 void sim_round(dq_ctx* ctx, const float* const* xs, size_t d, float* out, int flags,
                dq_round_info* info, cudaStream_t st) {
@@ -1114,10 +1100,8 @@ void sim_round(dq_ctx* ctx, const float* const* xs, size_t d, float* out, int fl
   }
   DQ_CUDA(cudaEventRecord(ctx->ev0, st));
   reserve_round(ctx, T, n);
-  ctx->xptrs.reserve(2 * 64);
-  upload_ptrs(ctx, xs, n, st);
   timed(ctx, K_STATS, 4.0 * n * d + 8.0 * n * T, st,
-        [&] { launch_stats(ctx->xptrs.p + 64 * ctx->xpar, n, d, T, ctx->mean_all.p, ctx->sq_all.p, st); });
+        [&] { launch_stats(xs, n, d, T, ctx->mean_all.p, ctx->sq_all.p, st); });
   timed(ctx, K_REDUCE, 8.0 * (n + 1) * T, st,
         [&] { launch_reduce_stats(ctx->mean_all.p, ctx->sq_all.p, n, T, ctx->gmean.p, ctx->gsq.p, st); });
   DQ_CUDA(cudaGetLastError());
@@ -1291,7 +1275,7 @@ void sim_round(dq_ctx* ctx, const float* const* xs, size_t d, float* out, int fl
   ctx->vn.reserve(2);
   if (!ctx->h_vn) DQ_CUDA(cudaMallocHost(&ctx->h_vn, 2 * sizeof(double)));
   DQ_CUDA(cudaMemsetAsync(ctx->vn.p, 0, 2 * sizeof(double), st));
-  launch_vnmse(ctx->xptrs.p + 64 * ctx->xpar, n, out, d, ctx->vn.p, st);
+  launch_vnmse(xs, n, out, d, ctx->vn.p, st);
   DQ_CUDA(cudaMemcpyAsync(ctx->h_vn, ctx->vn.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
   DQ_CUDA(cudaStreamSynchronize(st));
   harvest(ctx);
@@ -1769,9 +1753,7 @@ void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info
   }
   DQ_CUDA(cudaEventRecord(ctx->ev0, st));
   reserve_round(ctx, T, n);
-  ctx->xptrs.reserve(2 * 64);
-  upload_ptrs(ctx, &x, 1, st);
-  const float* const* dxp = ctx->xptrs.p + 64 * ctx->xpar;
+  const float* const* dxp = &x;
   // (a) local stats into this rank's row, (b) all-gather rows, fixed-order fp64 reduce (H4).
   // Peer transport: the all-gather is fused into the statistics kernel (each block stores
   // its rows into every rank's exchange area over NVLink, the last block raises the row
@@ -2341,13 +2323,8 @@ int dq_from_reference_wire(const void* h_ref, size_t len, void* h_soa, size_t so
 int dq_compute_stats(const float* d_x, size_t d, float* d_mean, float* d_sq, void* stream) {
   return guarded([&] {
     const uint32_t T = static_cast<uint32_t>((d + 255) / 256);
-    const float** dp = nullptr;
-    DQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dp), sizeof(float*), S(stream)));
-    DQ_CUDA(cudaMemcpyAsync(dp, &d_x, sizeof(float*), cudaMemcpyHostToDevice, S(stream)));
-    launch_stats(dp, 1, d, T, d_mean, d_sq, S(stream));
+    launch_stats(&d_x, 1, d, T, d_mean, d_sq, S(stream));  // the pointer travels in the kernel parameters
     DQ_CUDA(cudaGetLastError());
-    DQ_CUDA(cudaFreeAsync(dp, S(stream)));
-    DQ_CUDA(cudaStreamSynchronize(S(stream)));  // the pointer array lives on the host stack
   });
 }
 

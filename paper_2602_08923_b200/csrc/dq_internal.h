@@ -114,6 +114,12 @@ void launch_selftest(int which, uint64_t n, uint64_t seed, unsigned long long* b
 // ------------------------------------------------------------ statistics
 // per-super-group fp64 sequential sum / sum of squares of `n_workers` gradients
 // (pointer array in device memory) -> mean[w * T + j], sq[w * T + j]
+// worker gradients by value in the kernel parameters (no pointer table in memory: a round
+// enqueued far ahead of the GPU, or captured in a graph, carries its own pointers)
+struct WorkerPtrs {
+  const float* p[64];
+};
+WorkerPtrs worker_ptrs(const float* const* host_ptrs, uint32_t n);
 void launch_stats(const float* const* xs, uint32_t n_workers, uint64_t d, uint32_t T, float* mean,
                   float* sq, cudaStream_t st);
 // Statistics all-gather fused into the statistics kernel (peer transport): row `me` of

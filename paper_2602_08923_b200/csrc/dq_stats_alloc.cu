@@ -36,10 +36,10 @@ constexpr int kStatSG = 128;
 // the last block to finish (system-scope fences before the completion count) raises
 // row me's flag on every rank.  The reduction waits for all rows' flags.
 template <bool PEER>
-__global__ void __launch_bounds__(kStatSG) k_stats(const float* const* xs, uint64_t d, uint32_t T,
+__global__ void __launch_bounds__(kStatSG) k_stats(const WorkerPtrs xs, uint64_t d, uint32_t T,
                                                    float* mean, float* sq, StatsPeerArgs sp) {
   __shared__ float tile[kStatSG][33];
-  const float* __restrict__ x = xs[blockIdx.y];
+  const float* __restrict__ x = xs.p[blockIdx.y];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // PEER: a persistent grid walks the tiles, so the one system-scope fence per block
   // before the completion count is amortised over many tiles
@@ -100,11 +100,17 @@ __global__ void __launch_bounds__(kStatSG) k_stats(const float* const* xs, uint6
   }
 }
 
+WorkerPtrs worker_ptrs(const float* const* host_ptrs, uint32_t n) {
+  WorkerPtrs w{};
+  for (uint32_t r = 0; r < n && r < 64; ++r) w.p[r] = host_ptrs[r];
+  return w;
+}
+
 void launch_stats(const float* const* xs, uint32_t n_workers, uint64_t d, uint32_t T, float* mean,
                   float* sq, cudaStream_t st) {
   if (T == 0) return;
-  k_stats<false><<<dim3((T + kStatSG - 1) / kStatSG, n_workers), kStatSG, 0, st>>>(xs, d, T, mean, sq,
-                                                                                    StatsPeerArgs{});
+  k_stats<false><<<dim3((T + kStatSG - 1) / kStatSG, n_workers), kStatSG, 0, st>>>(
+      worker_ptrs(xs, n_workers), d, T, mean, sq, StatsPeerArgs{});
 }
 
 void launch_stats_peer(const float* const* xs, uint64_t d, uint32_t T, const StatsPeerArgs& sp, cudaStream_t st) {
@@ -119,7 +125,8 @@ void launch_stats_peer(const float* const* xs, uint64_t d, uint32_t T, const Sta
     return (sms > 0 ? sms : 148) * (per_sm > 0 ? per_sm : 4);
   }));
   const uint32_t ntiles = (T + kStatSG - 1) / kStatSG;
-  k_stats<true><<<dim3(ntiles < cap ? ntiles : cap, 1), kStatSG, 0, st>>>(xs, d, T, nullptr, nullptr, sp);
+  k_stats<true><<<dim3(ntiles < cap ? ntiles : cap, 1), kStatSG, 0, st>>>(worker_ptrs(xs, 1), d, T, nullptr,
+                                                                          nullptr, sp);
 }
 
 __global__ void k_reduce_stats(const float* mean, const float* sq, uint32_t n, uint32_t T,
@@ -1059,12 +1066,12 @@ void launch_general_counts(const float* F, uint32_t T, const uint64_t* pts, uint
 }
 
 // ------------------------------------------------------------------ vNMSE
-__global__ void k_vnmse(const float* const* xs, uint32_t n, const float* y, uint64_t d, double* acc) {
+__global__ void k_vnmse(const WorkerPtrs xs, uint32_t n, const float* y, uint64_t d, double* acc) {
   double err = 0.0, ref = 0.0;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < d;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     double e = 0.0;
-    for (uint32_t r = 0; r < n; ++r) e += static_cast<double>(xs[r][i]);
+    for (uint32_t r = 0; r < n; ++r) e += static_cast<double>(xs.p[r][i]);
     const double diff = static_cast<double>(y[i]) - e;
     err += diff * diff;
     ref += e * e;
@@ -1082,7 +1089,7 @@ __global__ void k_vnmse(const float* const* xs, uint32_t n, const float* y, uint
 
 void launch_vnmse(const float* const* xs, uint32_t n, const float* y, uint64_t d, double* acc2,
                   cudaStream_t st) {
-  k_vnmse<<<148 * 4, 256, 0, st>>>(xs, n, y, d, acc2);
+  k_vnmse<<<148 * 4, 256, 0, st>>>(worker_ptrs(xs, n), n, y, d, acc2);
 }
 
 }  // namespace dq
