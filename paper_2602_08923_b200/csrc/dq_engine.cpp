@@ -174,43 +174,42 @@ uint64_t fnv1a(const uint8_t* b, size_t n, uint64_t h) {
 using namespace dq;
 
 // Peer transport region of one rank (cudaMalloc'd, exported by CUDA IPC, mapped by
-// every other rank of the node): per round parity, `ninbox` inboxes (ring: hop h's
-// output lands in the right neighbour's inbox h; butterfly: stage s's message for
-// chunk c in the receiver's inbox s * n + c) and n gather slots (the sink of chunk c
-// stores its bytes into every rank's slot c), then one u32 flag per unit of each.
+// every other rank of the node): `ninbox` inboxes (ring: hop h's output lands in the right
+// neighbour's inbox h; butterfly: stage s's message for chunk c in the receiver's inbox
+// s * n + c) and n gather slots (the sink of chunk c stores its bytes into every rank's slot
+// c), then one u32 flag per unit of each, then the ring's permutation slices.  Single-
+// buffered: a rank's round k+1 writes into a peer only after its own round k completed,
+// which needed every rank's round-k sink output, hence every peer's round-k reads of its
+// region; flags carry the round's epoch (device memory, advanced once per round).
 struct PeerMem {
   uint8_t* base = nullptr;
   std::vector<uint8_t*> peer;  // rank q's region as mapped here (peer[me] == base)
   size_t cap = 0;              // bytes per chunk slot
   size_t cap_units = 0;        // flags per chunk slot
-  uint32_t n = 0, ninbox = 0, npin = 0, epoch = 0;
-  size_t slots() const { return 2ull * ninbox + 2ull * n; }
-  size_t inbox(uint32_t par, uint32_t h) const { return (static_cast<size_t>(par) * ninbox + h) * cap; }
-  size_t gather(uint32_t par, uint32_t c) const { return (2ull * ninbox + static_cast<size_t>(par) * n + c) * cap; }
+  uint32_t n = 0, ninbox = 0, npin = 0;
+  size_t slots() const { return static_cast<size_t>(ninbox) + n; }
+  size_t inbox(uint32_t h) const { return static_cast<size_t>(h) * cap; }
+  size_t gather(uint32_t c) const { return (static_cast<size_t>(ninbox) + c) * cap; }
   size_t flags() const { return slots() * cap; }
-  size_t iflag(uint32_t par, uint32_t h) const { return flags() + 4 * cap_units * inbox(par, h) / cap; }
-  size_t gflag(uint32_t par, uint32_t c) const { return flags() + 4 * cap_units * gather(par, c) / cap; }
-  // ring permutation slices: per parity npin areas of one u32 per (super-group, lane)
+  size_t iflag(uint32_t h) const { return flags() + 4 * cap_units * h; }
+  size_t gflag(uint32_t c) const { return flags() + 4 * cap_units * (static_cast<size_t>(ninbox) + c); }
+  // ring permutation slices: npin areas of one u32 per (super-group, lane)
   size_t pins() const { return (flags() + 4 * cap_units * slots() + 255) & ~static_cast<size_t>(255); }
-  size_t pin(uint32_t par, uint32_t k) const { return pins() + (static_cast<size_t>(par) * npin + k) * 128 * cap_units; }
-  size_t total() const { return pins() + 2ull * npin * 128 * cap_units; }
+  size_t pin(uint32_t k) const { return pins() + static_cast<size_t>(k) * 128 * cap_units; }
+  size_t total() const { return pins() + static_cast<size_t>(npin) * 128 * cap_units; }
 };
 
-// Statistics exchange area of one rank (peer transport): per round parity the [n][T]
-// mean and sum-of-squares rows every rank stores its row into, then n row flags.
+// Statistics exchange area of one rank (peer transport): the [n][T] mean and sum-of-squares
+// rows every rank stores its row into, then n row flags (single-buffered, as PeerMem).
 struct StatsMem {
   uint8_t* base = nullptr;
   std::vector<uint8_t*> peer;
-  uint32_t n = 0, T = 0, epoch = 0;  // T: row capacity (grow-only, headroom): rounds of any T <= it reuse the area
+  uint32_t n = 0, T = 0;  // T: row capacity (grow-only, headroom): rounds of any T <= it reuse the area
   size_t rows() const { return 4ull * n * T; }  // bytes of one [n][T] float array
-  float* mean(uint8_t* b, uint32_t par, uint32_t r) const {
-    return reinterpret_cast<float*>(b + 2ull * par * rows()) + static_cast<size_t>(r) * T;
-  }
-  float* sq(uint8_t* b, uint32_t par, uint32_t r) const {
-    return reinterpret_cast<float*>(b + (2ull * par + 1) * rows()) + static_cast<size_t>(r) * T;
-  }
-  uint32_t* flags(uint8_t* b, uint32_t par) const { return reinterpret_cast<uint32_t*>(b + 4 * rows()) + par * n; }
-  size_t total() const { return 4 * rows() + 2ull * n * sizeof(uint32_t); }
+  float* mean(uint8_t* b, uint32_t r) const { return reinterpret_cast<float*>(b) + static_cast<size_t>(r) * T; }
+  float* sq(uint8_t* b, uint32_t r) const { return reinterpret_cast<float*>(b + rows()) + static_cast<size_t>(r) * T; }
+  uint32_t* flags(uint8_t* b) const { return reinterpret_cast<uint32_t*>(b + 2 * rows()); }
+  size_t total() const { return 2 * rows() + static_cast<size_t>(n) * sizeof(uint32_t); }
 };
 
 struct dq_ctx {
@@ -284,6 +283,7 @@ struct dq_ctx {
   PeerMem pm;
   StatsMem sm;
   DevBuf<unsigned int> sdone;           // fused stats all-gather: block completion counter
+  DevBuf<uint32_t> dev_epoch;           // peer transport: the round's epoch (advanced on the device)
   DevBuf<uint8_t> ipc;                  // IPC handle exchange
   static void close_map(std::vector<uint8_t*>& peer, const uint8_t* base) {
     for (size_t q = 0; q < peer.size(); ++q)
@@ -1489,9 +1489,13 @@ bool stats_setup(dq_ctx* ctx, uint32_t T, cudaStream_t st) {
   sm.n = n;
   sm.T = std::max<uint32_t>(T + T / 4 + 64, 4096u);
   DQ_CUDA(cudaMalloc(&sm.base, sm.total()));
-  DQ_CUDA(cudaMemsetAsync(sm.base + 4 * sm.rows(), 0, sm.total() - 4 * sm.rows(), st));
+  DQ_CUDA(cudaMemsetAsync(sm.base + 2 * sm.rows(), 0, sm.total() - 2 * sm.rows(), st));
   ctx->sdone.reserve(1);
   DQ_CUDA(cudaMemsetAsync(ctx->sdone.p, 0, sizeof(unsigned int), st));
+  if (!ctx->dev_epoch.p) {  // every rank starts at 0 and advances once per round
+    ctx->dev_epoch.reserve(1);
+    DQ_CUDA(cudaMemsetAsync(ctx->dev_epoch.p, 0, sizeof(uint32_t), st));
+  }
   const bool ok = ipc_map(ctx, sm.base, sm.peer, st);
   if (old) DQ_CUDA(cudaFree(old));
   if (!ok) {
@@ -1510,7 +1514,7 @@ bool stats_setup(dq_ctx* ctx, uint32_t T, cudaStream_t st) {
 // into gather slot r of every rank - the all-gather - and one decode launch per rank
 // consumes all n gather slots as their units land.
 void peer_gather_decode(dq_ctx* ctx, const Prepared& p, const std::vector<Layout>& lays,
-                        const std::vector<char>& decoded, float* out, size_t d, uint32_t epoch, cudaStream_t st);
+                        const std::vector<char>& decoded, float* out, size_t d, cudaStream_t st);
 
 // Fused own-chunk decode in the peer sinks (launch_quant_dec) only up to this many ranks.
 // Measured at d = 2^28 per rank (profiles/r1_multi_gpu.md): N = 2 the gather decode is
@@ -1533,37 +1537,36 @@ void ring_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>& bas
   const uint32_t n = ctx->cfg.n_workers, me = static_cast<uint32_t>(ctx->rank);
   const uint32_t right = (me + 1) % n;
   PeerMem& pm = ctx->pm;
-  const uint32_t epoch = ++pm.epoch, par = epoch & 1u;
   std::vector<char> decoded(n, 0);
   for (uint32_t h = 0; h < n; ++h) {
     const uint32_t ch = (me + 2 * n - 1 - h) % n;  // sink at h = n-1
     CodecArgs a = bases[ch];
     a.slot = h;
     a.unit = peer_unit(lays[ch].nsg);
-    a.epoch = epoch;
+    a.epoch_ptr = ctx->dev_epoch.p;
     if (h > 0) {
-      a.in = pm.base + pm.inbox(par, h - 1);
-      a.in_flags = reinterpret_cast<const uint32_t*>(pm.base + pm.iflag(par, h - 1));
+      a.in = pm.base + pm.inbox(h - 1);
+      a.in_flags = reinterpret_cast<const uint32_t*>(pm.base + pm.iflag(h - 1));
     }
     if (pm.npin) {  // hop s of this chunk runs on rank me + s - h
       if (h == 0) {
         a.pc_mode = 3;
         for (uint32_t s = 1; s < n; ++s)
-          a.pin_out[s] = reinterpret_cast<uint32_t*>(pm.peer[(me + s) % n] + pm.pin(par, s - 1));
+          a.pin_out[s] = reinterpret_cast<uint32_t*>(pm.peer[(me + s) % n] + pm.pin(s - 1));
       } else {
         a.pc_mode = 4;
-        a.pin = reinterpret_cast<const uint32_t*>(pm.base + pm.pin(par, h - 1));
+        a.pin = reinterpret_cast<const uint32_t*>(pm.base + pm.pin(h - 1));
       }
     }
     if (h + 1 < n) {
-      a.outs[0] = pm.peer[right] + pm.inbox(par, h);
-      a.out_flags[0] = reinterpret_cast<uint32_t*>(pm.peer[right] + pm.iflag(par, h));
+      a.outs[0] = pm.peer[right] + pm.inbox(h);
+      a.out_flags[0] = reinterpret_cast<uint32_t*>(pm.peer[right] + pm.iflag(h));
       a.n_outs = 1;
     } else {
       for (uint32_t k = 0; k < n; ++k) {  // remote copies first, own slot last
         const uint32_t q = (me + 1 + k) % n;
-        a.outs[k] = pm.peer[q] + pm.gather(par, me);
-        a.out_flags[k] = reinterpret_cast<uint32_t*>(pm.peer[q] + pm.gflag(par, me));
+        a.outs[k] = pm.peer[q] + pm.gather(me);
+        a.out_flags[k] = reinterpret_cast<uint32_t*>(pm.peer[q] + pm.gflag(me));
       }
       a.n_outs = static_cast<int>(n);
     }
@@ -1579,16 +1582,15 @@ void ring_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>& bas
       else launch_quant_dec(a, 0, true, st);
     });
   }
-  peer_gather_decode(ctx, p, lays, decoded, out, d, epoch, st);
+  peer_gather_decode(ctx, p, lays, decoded, out, d, st);
 }
 
 // Every rank decodes the n gather slots of this round's parity into the output, unit by
 // unit as the sinks' stores land (its own slot is complete: its sink ran earlier on st),
 // except the chunks its own sink already decoded (decoded[c], launch_quant_dec).
 void peer_gather_decode(dq_ctx* ctx, const Prepared& p, const std::vector<Layout>& lays,
-                        const std::vector<char>& decoded, float* out, size_t d, uint32_t epoch, cudaStream_t st) {
+                        const std::vector<char>& decoded, float* out, size_t d, cudaStream_t st) {
   const uint32_t n = ctx->cfg.n_workers, me = static_cast<uint32_t>(ctx->rank);
-  const uint32_t par = epoch & 1u;
   PeerMem& pm = ctx->pm;
   GatherArgs g{};
   set_format(g, ctx->cfg);
@@ -1598,19 +1600,19 @@ void peer_gather_decode(dq_ctx* ctx, const Prepared& p, const std::vector<Layout
   double gbytes = 0;
   for (uint32_t c = 0; c < n; ++c) {
     if (decoded[c]) continue;
-    g.in[k] = pm.base + pm.gather(par, c);
+    g.in[k] = pm.base + pm.gather(c);
     g.lo[k] = p.lo[c];
     g.hi[k] = p.lo[c + 1];
     g.n8[k] = lays[c].n8;
     g.n4[k] = lays[c].n4;
-    g.flags[k] = c == me ? nullptr : reinterpret_cast<const uint32_t*>(pm.base + pm.gflag(par, c));
+    g.flags[k] = c == me ? nullptr : reinterpret_cast<const uint32_t*>(pm.base + pm.gflag(c));
     g.unit[k] = peer_unit(lays[c].nsg);
     max_nsg = std::max(max_nsg, lays[c].nsg);
     gbytes += 1032.0 * lays[c].nsg + lays[c].bytes();
     ++k;
   }
   if (!k) return;
-  g.epoch = epoch;
+  g.epoch_ptr = ctx->dev_epoch.p;
   g.perm = ctx->perm.p;
   g.gmean = ctx->pmean.p;
   g.out = out;
@@ -1641,7 +1643,6 @@ void butterfly_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>
   uint32_t stages = 0;
   while ((1u << stages) < n) ++stages;
   PeerMem& pm = ctx->pm;
-  const uint32_t epoch = ++pm.epoch, par = epoch & 1u;
   ctx->accs.reserve(static_cast<size_t>(n) * max_nsg * 256);
   auto acc_ptr = [&](uint32_t ch) { return ctx->accs.p + static_cast<size_t>(ch) * max_nsg * 256; };
   std::vector<int> held(n, -1);
@@ -1649,7 +1650,7 @@ void butterfly_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>
   auto prep = [&](uint32_t ch) {
     CodecArgs a = bases[ch];
     a.unit = peer_unit(lays[ch].nsg);
-    a.epoch = epoch;
+    a.epoch_ptr = ctx->dev_epoch.p;
     return a;
   };
   auto operand = [&](uint32_t ch, CodecArgs& a) {
@@ -1658,8 +1659,8 @@ void butterfly_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>
     return 1;
   };
   auto inbox_in = [&](CodecArgs& a, uint32_t k) {
-    a.in = pm.base + pm.inbox(par, k);
-    a.in_flags = reinterpret_cast<const uint32_t*>(pm.base + pm.iflag(par, k));
+    a.in = pm.base + pm.inbox(k);
+    a.in_flags = reinterpret_cast<const uint32_t*>(pm.base + pm.iflag(k));
   };
   for (uint32_t s = 0; s < stages; ++s) {
     for (uint32_t ch = 0; ch < n; ++ch)
@@ -1672,8 +1673,8 @@ void butterfly_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>
         const bool dar = held[ch] >= 0;
         if (dar) inbox_in(a, static_cast<uint32_t>(held[ch]));
         const uint32_t k = s * n + ch;
-        a.outs[0] = pm.peer[ev.rcv] + pm.inbox(par, k);
-        a.out_flags[0] = reinterpret_cast<uint32_t*>(pm.peer[ev.rcv] + pm.iflag(par, k));
+        a.outs[0] = pm.peer[ev.rcv] + pm.inbox(k);
+        a.out_flags[0] = reinterpret_cast<uint32_t*>(pm.peer[ev.rcv] + pm.iflag(k));
         a.n_outs = 1;
         timed(ctx, dar ? K_DAR : K_LEAF, quant_bytes(lays[ch], dar), st, [&] { launch_quant_peer(a, src, dar, st); });
         held[ch] = -1;
@@ -1698,8 +1699,8 @@ void butterfly_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>
           a.slot = pl.sink_slot;
           for (uint32_t j = 0; j < n; ++j) {
             const uint32_t q = (me + 1 + j) % n;
-            a.outs[j] = pm.peer[q] + pm.gather(par, ch);
-            a.out_flags[j] = reinterpret_cast<uint32_t*>(pm.peer[q] + pm.gflag(par, ch));
+            a.outs[j] = pm.peer[q] + pm.gather(ch);
+            a.out_flags[j] = reinterpret_cast<uint32_t*>(pm.peer[q] + pm.gflag(ch));
           }
           a.n_outs = static_cast<int>(n);
           if (n <= kFuseDecodeMaxRanks) a.dec_out = out;  // and decoded into this rank's output
@@ -1717,7 +1718,7 @@ void butterfly_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>
       }
     }
   }
-  peer_gather_decode(ctx, p, lays, decoded, out, d, epoch, st);
+  peer_gather_decode(ctx, p, lays, decoded, out, d, st);
 }
 
 // NCCL reports errors of enqueued work (a dead peer, a network failure) asynchronously
@@ -1761,20 +1762,19 @@ void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info
   // previous round before any store of this round into its regions.
   if (ctx->transport == DQ_TRANSPORT_PEER && n <= static_cast<uint32_t>(kMaxPeers) && stats_setup(ctx, T, st)) {
     StatsMem& sm = ctx->sm;
-    const uint32_t ep = ++sm.epoch, par = ep & 1u;
     StatsPeerArgs sp{};
     for (uint32_t q = 0; q < n; ++q) {
-      sp.mean[q] = sm.mean(sm.peer[q], par, me);
-      sp.sq[q] = sm.sq(sm.peer[q], par, me);
-      sp.flag[q] = sm.flags(sm.peer[q], par) + me;
+      sp.mean[q] = sm.mean(sm.peer[q], me);
+      sp.sq[q] = sm.sq(sm.peer[q], me);
+      sp.flag[q] = sm.flags(sm.peer[q]) + me;
     }
     sp.done = ctx->sdone.p;
     sp.n = n;
-    sp.epoch = ep;
+    sp.epoch = ctx->dev_epoch.p;  // advanced by the statistics kernel: this round's epoch
     timed(ctx, K_STATS, 4.0 * d + 8.0 * T * n, st, [&] { launch_stats_peer(dxp, d, T, sp, st); });
     timed(ctx, K_REDUCE, 8.0 * (n + 1) * T, st, [&] {
-      launch_reduce_stats_peer(sm.mean(sm.base, par, 0), sm.sq(sm.base, par, 0), sm.flags(sm.base, par), ep, n, T, sm.T,
-                               ctx->gmean.p, ctx->gsq.p, st);
+      launch_reduce_stats_peer(sm.mean(sm.base, 0), sm.sq(sm.base, 0), sm.flags(sm.base), ctx->dev_epoch.p, n, T,
+                               sm.T, ctx->gmean.p, ctx->gsq.p, st);
     });
   } else {
     float* my_mean = ctx->mean_all.p + static_cast<size_t>(me) * T;

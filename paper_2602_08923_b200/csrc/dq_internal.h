@@ -34,12 +34,15 @@ struct CodecArgs {
   // peer transport (k_quant_peer): the chunk is produced/consumed in flag units of
   // `unit` consecutive super-groups; a unit of `in` may be read once in_flags[unit]
   // == epoch, and every finished unit is stored to all n_outs destinations (peer
-  // memory over NVLink) before its out_flags[o][unit] is set to epoch.
+  // memory over NVLink) before its out_flags[o][unit] is set to epoch.  The round's epoch
+  // lives in device memory (*epoch_ptr, advanced by the round's statistics kernel), so a
+  // round captured in a CUDA graph gets a fresh epoch on every replay.
   const uint32_t* in_flags;
   uint8_t* outs[kMaxPeers];
   uint32_t* out_flags[kMaxPeers];
   int n_outs;
-  uint32_t unit, epoch;
+  uint32_t unit;
+  const uint32_t* epoch_ptr;
   // permutation slices (pc_mode 3 / 4, correlated, n <= 8): the chunk's leaf stores slot
   // s's pi of every entry into pin_out[s] (null = none): the rank running hop s (ring,
   // peer transport) or the simulated round's slice buffer; hop s reads a.pin.
@@ -68,10 +71,10 @@ struct GatherArgs {
   float n_workers_f;
   int uniform_books;
   uint32_t gs = 16, ss = 2, gshift = 1;  // scale format of every chunk (see Layout)
-  // peer transport: chunk c's unit k may be decoded once flags[c][k] == epoch (null: ready)
+  // peer transport: chunk c's unit k may be decoded once flags[c][k] == *epoch_ptr (null: ready)
   const uint32_t* flags[64];
   uint32_t unit[64];
-  uint32_t epoch;
+  const uint32_t* epoch_ptr;
 };
 void launch_gather_decode(const GatherArgs& g, uint32_t n_chunks, uint32_t max_nsg, cudaStream_t st);
 
@@ -124,17 +127,20 @@ void launch_stats(const float* const* xs, uint32_t n_workers, uint64_t d, uint32
                   float* sq, cudaStream_t st);
 // Statistics all-gather fused into the statistics kernel (peer transport): row `me` of
 // every rank's area (mean[r], sq[r] = peer pointers), completion flags flag[r] (row me
-// on rank r) set to epoch by the last block; done = local block-completion counter.
+// on rank r) set to the new epoch by the last block, which also stores it to *epoch (the
+// round's epoch counter in device memory, read by the round's later kernels); done =
+// local block-completion counter.
 struct StatsPeerArgs {
   float* mean[kMaxPeers];
   float* sq[kMaxPeers];
   uint32_t* flag[kMaxPeers];
   unsigned int* done;
-  uint32_t n, epoch;
+  uint32_t n;
+  uint32_t* epoch;
 };
 void launch_stats_peer(const float* const* xs, uint64_t d, uint32_t T, const StatsPeerArgs& sp, cudaStream_t st);
-// reduction of the fused all-gather's rows after waiting for all n row flags == epoch
-void launch_reduce_stats_peer(const float* mean, const float* sq, const uint32_t* flags, uint32_t epoch,
+// reduction of the fused all-gather's rows after waiting for all n row flags == *epoch
+void launch_reduce_stats_peer(const float* mean, const float* sq, const uint32_t* flags, const uint32_t* epoch,
                               uint32_t n, uint32_t T, uint32_t stride, float* gm, float* gs, cudaStream_t st);
 // rank-ordered fp64 reduction of [n][T] stats -> global [T]
 void launch_reduce_stats(const float* mean, const float* sq, uint32_t n, uint32_t T, float* gmean,

@@ -93,9 +93,11 @@ __global__ void __launch_bounds__(kStatSG) k_stats(const WorkerPtrs xs, uint64_t
     __syncthreads();
     if (last && threadIdx.x == 0) {
       *sp.done = 0;  // reset for the next round (stream-ordered before its stats kernel)
+      const uint32_t epoch = *sp.epoch + 1;  // this round's epoch, read by its later kernels
+      *sp.epoch = epoch;
       __threadfence_system();
       for (uint32_t r = 0; r < sp.n; ++r)
-        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(sp.flag[r]), "r"(sp.epoch) : "memory");
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(sp.flag[r]), "r"(epoch) : "memory");
     }
   }
 }
@@ -150,9 +152,11 @@ void launch_reduce_stats(const float* mean, const float* sq, uint32_t n, uint32_
 
 // The rank-ordered reduction over the fused all-gather's rows: each block first waits
 // (thread 0, acquire at system scope, g_spin_ns timeout -> trap) for every row's flag.
-__global__ void k_reduce_stats_peer(const float* mean, const float* sq, const uint32_t* flags, uint32_t epoch,
-                                    uint32_t n, uint32_t T, uint32_t stride, float* gm, float* gs) {
+__global__ void k_reduce_stats_peer(const float* mean, const float* sq, const uint32_t* flags,
+                                    const uint32_t* epoch_ptr, uint32_t n, uint32_t T, uint32_t stride, float* gm,
+                                    float* gs) {
   if (threadIdx.x == 0) {
+    const uint32_t epoch = *epoch_ptr;
     for (uint32_t r = 0; r < n; ++r) {
       uint32_t v;
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + r) : "memory");
@@ -178,7 +182,7 @@ __global__ void k_reduce_stats_peer(const float* mean, const float* sq, const ui
   gs[j] = static_cast<float>(b);
 }
 
-void launch_reduce_stats_peer(const float* mean, const float* sq, const uint32_t* flags, uint32_t epoch,
+void launch_reduce_stats_peer(const float* mean, const float* sq, const uint32_t* flags, const uint32_t* epoch,
                               uint32_t n, uint32_t T, uint32_t stride, float* gm, float* gs, cudaStream_t st) {
   if (T == 0) return;
   k_reduce_stats_peer<<<(T + 255) / 256, 256, 0, st>>>(mean, sq, flags, epoch, n, T, stride, gm, gs);

@@ -60,3 +60,20 @@ def test_distributed_allreduce_three_ranks():
     res = json.loads(lines[-1])
     assert res["ok"], json.dumps(res, indent=1)
     assert res["world"] == 3
+
+
+def test_distributed_round_in_cuda_graph():
+    """dq_allreduce captured in a CUDA graph (device-side epochs and allocation): replays on
+    new inputs equal the simulated round and agree across ranks."""
+    torch = pytest.importorskip("torch")
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    n = min(n, 8)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", "--master-port=29537", os.path.join(ROOT, "tools", "dist_graph.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert lines, r.stdout[-3000:] + r.stderr[-3000:]
+    res = json.loads(lines[-1])
+    assert res["ok"], json.dumps(res, indent=1)
