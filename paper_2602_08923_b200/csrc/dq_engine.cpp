@@ -247,6 +247,7 @@ struct dq_ctx {
   std::atomic<bool> svc_stop{false};
   uint32_t apar = 0;
   bool async_alloc = true;   // env DQ_SYNC_ALLOC=1: host-synchronous allocation (round-1 behaviour)
+  bool no_small_alloc = false;  // env DQ_NO_SMALL_ALLOC=1: the cooperative search at every T
   // what the last round needs to fill dq_round_info once it has completed
   struct RoundRec {
     bool valid = false, async = false;
@@ -876,6 +877,10 @@ AllocResult allocate_fast_async(dq_ctx* ctx, const dq_config& c, const float* dF
   DQ_CUDA(cudaHostGetDevicePointer(&dF_host, ctx->hF, 0));
   w.hmsg = static_cast<HostMsg*>(dm);
   w.hF = static_cast<float*>(dF_host);
+  if (!ctx->no_small_alloc && launch_alloc_small(dF, T, kAlpha, budget, S, w, dW, dP, st)) {
+    DQ_CUDA(cudaGetLastError());
+    return r;
+  }
   DQ_CUDA(launch_alloc_search(dF, T, kAlpha, static_cast<uint64_t>(W), budget, S, w, st));
   launch_alloc_assign(dF, T, 0.f, 0.f, true, w, dW, dP, st);
   DQ_CUDA(cudaGetLastError());
@@ -2059,6 +2064,8 @@ int dq_ctx_create(const dq_config* cfg, int device, dq_ctx** out) {
       if (std::strcmp(t, "nccl") == 0) c->transport = DQ_TRANSPORT_NCCL;
     if (const char* t = std::getenv("DQ_SYNC_ALLOC"))
       if (std::strcmp(t, "1") == 0) c->async_alloc = false;
+    if (const char* t = std::getenv("DQ_NO_SMALL_ALLOC"))
+      if (std::strcmp(t, "1") == 0) c->no_small_alloc = true;
     *out = c;
   });
 }

@@ -220,6 +220,9 @@ cudaError_t launch_alloc_search(const float* F, uint32_t T, double alpha, uint64
                                 uint32_t S, AllocWork w, cudaStream_t st);
 // test hook: make every asynchronous search hand its decision to the host (need_host)
 void set_force_host_alloc(int on);
+// asynchronous rounds with T <= 4096: search + assignment in one CTA (false: not applicable)
+bool launch_alloc_small(const float* F, uint32_t T, double alpha, double budget, uint32_t S, AllocWork w,
+                        uint8_t* widths, uint32_t* perm, cudaStream_t st);
 // Slow exact path helpers (rare): neighbour flip of `key` (dir -1: largest key below,
 // +1: smallest key above) -> rec; float-threshold counts -> counts[0] = #F>=t48,
 // counts[1] = #F>=t24.  Both asynchronous on st.

@@ -708,6 +708,290 @@ __global__ void __launch_bounds__(kAllocBins) k_alloc_coop(const float* __restri
 
 void set_force_host_alloc(int on) { cudaMemcpyToSymbol(g_force_host_alloc, &on, sizeof on); }
 
+// ---------------------------------------------- small T: search + assignment in one block
+// The latency path of small all-reduces (T <= 4096 super-groups, d <= 1M entries): the
+// reference's allocate_fast restated literally in one CTA - every flip 4 - a log2 F_j and
+// 8 - a log2 F_j (device libm) radix-sorted in shared memory (CUB), de-duplicated, the
+// plateau samples between them bisected exactly as allocation.cpp:228-255 does with the
+// float-threshold payload of each probe, every probe's thresholds certified (as in
+// alloc_candidates) - then widths, the stable 8/4/2 partition and the permuted means.  One
+// launch instead of the cooperative search's passes and grid syncs plus three assignment
+// kernels.  Uncertified probes hand the round to the host exactly like the search does.
+constexpr int kSmallThreads = 512;
+__device__ __forceinline__ double key_double(uint64_t k) {  // inverse of dkey
+  const uint64_t b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double(static_cast<long long>(b));
+}
+__device__ __forceinline__ bool stable_float(double d) {
+  const float lo = __double2float_rn(__dmul_rd(d, 1.0 - 0x1p-40)), hi = __double2float_rn(__dmul_ru(d, 1.0 + 0x1p-40));
+  return __float_as_uint(lo) == __float_as_uint(hi);
+}
+__device__ __forceinline__ unsigned long long small_block_sum(unsigned long long v, unsigned long long* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  unsigned long long t = 0;
+  for (int k = 0; k < kSmallThreads / 32; ++k) t += red[k];
+  return t;
+}
+
+template <int IPT>
+__global__ void __launch_bounds__(kSmallThreads) k_alloc_small(const float* __restrict__ F, uint32_t T, double alpha,
+                                                               double budget, uint32_t S, AllocWork w,
+                                                               uint8_t* widths, uint32_t* perm) {
+  constexpr int N = kSmallThreads * IPT;  // >= 2T flips
+  using Sort = cub::BlockRadixSort<uint64_t, kSmallThreads, IPT, uint32_t>;
+  extern __shared__ __align__(16) uint8_t smem[];
+  auto& sort_tmp = *reinterpret_cast<typename Sort::TempStorage*>(smem);
+  uint64_t* K = reinterpret_cast<uint64_t*>(smem);           // sorted keys   [N] (after the sort)
+  uint32_t* V = reinterpret_cast<uint32_t*>(K + N);          // sorted values [N]
+  uint64_t* UK = reinterpret_cast<uint64_t*>(V + N);         // unique flips  [N]
+  uint32_t* UV = reinterpret_cast<uint32_t*>(UK + N);        // their super-group | type << 31
+  __shared__ unsigned long long red[kSmallThreads / 32];
+  __shared__ uint32_t m_sh;
+  __shared__ float thr_sh[2];
+  __shared__ int ok_sh, lo_sh, hi_sh, cert_sh;
+  AllocState* st = w.state;
+  const int t = threadIdx.x;
+  // flips (blocked arrangement: item i of thread t is flip t * IPT + i = super-group >> 1, type & 1)
+  uint64_t key[IPT];
+  uint32_t val[IPT];
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const uint32_t idx = static_cast<uint32_t>(t * IPT + i), j = idx >> 1, type = idx & 1;
+    key[i] = ~0ull;
+    val[i] = j | type << 31;
+    if (j < T) {
+      const float f = F[j];
+      if (f > 0.0f) key[i] = dkey(__dsub_rn(type ? 8.0 : 4.0, __dmul_rn(alpha, log2(static_cast<double>(f)))));
+    }
+  }
+  Sort(sort_tmp).Sort(key, val);
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    K[t * IPT + i] = key[i];
+    V[t * IPT + i] = val[i];
+  }
+  __syncthreads();
+  // unique flips (std::unique on the sorted doubles), compacted in order
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int idx = t * IPT + i;
+    cnt += key[i] != ~0ull && (idx == 0 || K[idx - 1] != key[i]);
+  }
+  unsigned long long incl = cnt;
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long u = __shfl_up_sync(0xffffffffu, incl, o);
+    if ((t & 31) >= o) incl += u;
+  }
+  if ((t & 31) == 31) red[t >> 5] = incl;
+  __syncthreads();
+  unsigned long long off = 0, all = 0;
+  for (int k = 0; k < kSmallThreads / 32; ++k) {
+    if (k < (t >> 5)) off += red[k];
+    all += red[k];
+  }
+  uint32_t pos = static_cast<uint32_t>(off + incl - cnt);
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int idx = t * IPT + i;
+    if (key[i] != ~0ull && (idx == 0 || K[idx - 1] != key[i])) {
+      UK[pos] = key[i];
+      UV[pos] = val[i];
+      ++pos;
+    }
+  }
+  if (t == 0) {
+    m_sh = static_cast<uint32_t>(all);
+    cert_sh = 1;
+  }
+  __syncthreads();
+  const uint32_t m = m_sh;
+  const uint32_t ns = m ? m + 1 : 1;  // samples (fast_sample_points)
+  auto sample = [&](uint32_t i) {
+    double u;
+    if (m == 0) u = 0.0;
+    else if (i == 0) u = __dsub_rn(key_double(UK[0]), 1.0);
+    else if (i == m) u = __dadd_rn(key_double(UK[m - 1]), 1.0);
+    else u = __dmul_rn(0.5, __dadd_rn(key_double(UK[i - 1]), key_double(UK[i])));
+    return u < -1e6 ? -1e6 : (u > 1e6 ? 1e6 : u);
+  };
+  // payload(u) <= budget with the float thresholds (allocation.cpp:173-189,237), certified
+  auto fits = [&](uint32_t i) {
+    if (t == 0) {
+      const double u = sample(i);
+      const double d24 = exp2(__ddiv_rn(__dsub_rn(4.0, u), alpha)), d48 = exp2(__ddiv_rn(__dsub_rn(8.0, u), alpha));
+      thr_sh[0] = static_cast<float>(d24);
+      thr_sh[1] = static_cast<float>(d48);
+      if (!stable_float(d24) || !stable_float(d48)) cert_sh = 0;
+    }
+    __syncthreads();
+    const float t24 = thr_sh[0], t48 = thr_sh[1];
+    unsigned long long wsum = 0;
+    for (uint32_t j = t; j < T; j += kSmallThreads) {
+      const float f = F[j];
+      wsum += f >= t48 ? 8 : (f >= t24 ? 4 : 2);
+    }
+    const unsigned long long tot = small_block_sum(wsum, red);
+    return static_cast<double>(tot * S) <= budget;
+  };
+  if (t == 0) {
+    lo_sh = 0;
+    hi_sh = static_cast<int>(ns - 1);
+  }
+  __syncthreads();
+  bool feasible = fits(0);
+  if (feasible) {
+    if (fits(ns - 1)) {
+      if (t == 0) lo_sh = static_cast<int>(ns - 1);
+      __syncthreads();
+    } else {
+      for (;;) {
+        const int lo = lo_sh, hi = hi_sh;
+        if (lo + 1 >= hi) break;
+        const int mid = (lo + hi) / 2;
+        const bool ok = fits(static_cast<uint32_t>(mid));
+        if (t == 0) {
+          if (ok) lo_sh = mid;
+          else hi_sh = mid;
+        }
+        __syncthreads();
+      }
+    }
+  }
+  const uint32_t lo = static_cast<uint32_t>(lo_sh);
+  // final thresholds (certified) + the state the host reads (u via host_u_of, mailbox)
+  if (t == 0) {
+    const double u = sample(lo);
+    const double d24 = exp2(__ddiv_rn(__dsub_rn(4.0, u), alpha)), d48 = exp2(__ddiv_rn(__dsub_rn(8.0, u), alpha));
+    const uint32_t epoch = st->epoch + 1;
+    *st = AllocState{};
+    st->epoch = epoch;
+    auto rec = [&](uint32_t i) {
+      FlipRec r{};
+      r.key = UK[i];
+      r.fbits = __float_as_uint(F[UV[i] & 0x7fffffffu]);
+      r.type = UV[i] >> 31;
+      r.present = 1;
+      return r;
+    };
+    if (m == 0) {
+      st->status = 3;
+    } else if (lo == m) {
+      st->status = 2;
+      st->slot[1] = rec(m - 1);
+    } else {
+      st->status = 1;
+      st->slot[2] = rec(lo);
+      if (lo > 0) st->slot[1] = rec(lo - 1);
+    }
+    st->choice = 1;
+    st->u = u;
+    st->t24 = static_cast<float>(d24);
+    st->t48 = static_cast<float>(d48);
+    st->certified = cert_sh && stable_float(d24) && stable_float(d48) ? 1u : 0u;
+    st->need_host = (!st->certified || !feasible || g_force_host_alloc) ? 1u : 0u;
+    st->T = T;
+    st->S = S;
+    st->budget = budget;
+    st->alpha = alpha;
+    ok_sh = static_cast<int>(st->need_host);
+  }
+  __syncthreads();
+  if (ok_sh) {  // hand the round to the host: export F, mirror, request, wait for the answer
+    for (uint32_t j = t; j < T; j += kSmallThreads) w.hF[j] = F[j];
+  }
+  __syncthreads();
+  {
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(st);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(&w.hmsg->state);
+    for (uint32_t k = t; k < sizeof(AllocState) / 4; k += kSmallThreads) dst[k] = src[k];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (t == 0 && ok_sh) {
+    w.hmsg->request = st->epoch;
+    __threadfence_system();
+    const uint64_t t0 = dq_globaltimer();
+    for (;;) {
+      uint32_t v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(&w.hmsg->resolved) : "memory");
+      if (v == st->epoch) break;
+      __nanosleep(1000);
+      if (dq_globaltimer() - t0 > g_spin_ns) __trap();
+    }
+    st->t24 = *reinterpret_cast<volatile float*>(&w.hmsg->t24);
+    st->t48 = *reinterpret_cast<volatile float*>(&w.hmsg->t48);
+  }
+  __syncthreads();
+  const float t24 = st->t24, t48 = st->t48;
+  // widths + stable partition 8 | 4 | 2 (build_permutation, allocation.cpp:302-310): thread t
+  // owns the contiguous super-groups [t * per, (t + 1) * per)
+  const uint32_t per = (T + kSmallThreads - 1) / kSmallThreads;
+  const uint32_t j0 = t * per, j1 = j0 + per < T ? j0 + per : T;
+  unsigned long long packed = 0;  // 21-bit class counts
+  for (uint32_t j = j0; j < j1; ++j) {
+    const float fj = F[j];
+    const int c = fj >= t48 ? 0 : (fj >= t24 ? 1 : 2);
+    widths[j] = static_cast<uint8_t>(c == 0 ? 8 : (c == 1 ? 4 : 2));
+    packed += 1ull << (21 * c);
+  }
+  unsigned long long sc = packed;
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long u = __shfl_up_sync(0xffffffffu, sc, o);
+    if ((t & 31) >= o) sc += u;
+  }
+  __syncthreads();
+  if ((t & 31) == 31) red[t >> 5] = sc;
+  __syncthreads();
+  unsigned long long base = 0, tot = 0;
+  for (int k = 0; k < kSmallThreads / 32; ++k) {
+    if (k < (t >> 5)) base += red[k];
+    tot += red[k];
+  }
+  const unsigned long long excl = base + sc - packed;
+  const uint32_t n8 = static_cast<uint32_t>(tot & 0x1fffff), n4 = static_cast<uint32_t>((tot >> 21) & 0x1fffff);
+  uint32_t p[3] = {static_cast<uint32_t>(excl & 0x1fffff), n8 + static_cast<uint32_t>((excl >> 21) & 0x1fffff),
+                   n8 + n4 + static_cast<uint32_t>((excl >> 42) & 0x1fffff)};
+  for (uint32_t j = j0; j < j1; ++j) {
+    const float fj = F[j];
+    const int c = fj >= t48 ? 0 : (fj >= t24 ? 1 : 2);
+    const uint32_t at = p[c]++;
+    perm[at] = j;
+    if (w.pmean) w.pmean[at] = w.gmean[j];
+  }
+  if (t == 0) {
+    w.counts[0] = n8;
+    w.counts[1] = n4;
+    w.counts[2] = T - n8 - n4;
+    w.hmsg->counts[0] = n8;
+    w.hmsg->counts[1] = n4;
+    w.hmsg->counts[2] = T - n8 - n4;
+    __threadfence_system();
+  }
+}
+
+bool launch_alloc_small(const float* F, uint32_t T, double alpha, double budget, uint32_t S, AllocWork w,
+                        uint8_t* widths, uint32_t* perm, cudaStream_t st) {
+  if (!w.hmsg || T == 0 || T > 4096) return false;
+  auto go = [&](auto ipt) {
+    constexpr int IPT = decltype(ipt)::value;
+    constexpr size_t N = static_cast<size_t>(kSmallThreads) * IPT;
+    using Sort = cub::BlockRadixSort<uint64_t, kSmallThreads, IPT, uint32_t>;
+    const size_t bytes = std::max(sizeof(typename Sort::TempStorage), N * 12) + N * 12;
+    cudaFuncSetAttribute(k_alloc_small<IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+    k_alloc_small<IPT><<<1, kSmallThreads, bytes, st>>>(F, T, alpha, budget, S, w, widths, perm);
+  };
+  if (2 * T <= kSmallThreads * 4) go(std::integral_constant<int, 4>{});
+  else if (2 * T <= kSmallThreads * 8) go(std::integral_constant<int, 8>{});
+  else go(std::integral_constant<int, 16>{});
+  return true;
+}
+
 cudaError_t launch_alloc_search(const float* F, uint32_t T, double alpha, uint64_t wmax, double budget,
                                 uint32_t S, AllocWork w, cudaStream_t st) {
   static int cache[kMaxDevices] = {};

@@ -47,7 +47,10 @@ def _check(dq, got, want):
 
 
 @pytest.mark.parametrize("n,b,topo,d", [(4, 4.0, "ring", 1 << 16), (8, 3.0, "butterfly", (1 << 15) + 77),
-                                        (3, 5.0, "ring", 1 << 14), (2, 6.0, "ring", 3000)])
+                                        (3, 5.0, "ring", 1 << 14), (2, 6.0, "ring", 3000),
+                                        # T = 4096 (largest one-CTA allocation) and 4097 (cooperative search)
+                                        (4, 4.0, "ring", 1 << 20), (2, 3.0, "ring", (1 << 20) + 256),
+                                        (4, 4.0, "ring", 1 << 22)])
 def test_async_round_matches_oracle(dq, port, n, b, topo, d):
     ws = _workers(port, n, d, seed=11 + n)
     want = port.run_round(ws, port.round_cfg(n, b, topo, seed=1))
@@ -55,7 +58,8 @@ def test_async_round_matches_oracle(dq, port, n, b, topo, d):
     _check(dq, got, want)
 
 
-@pytest.mark.parametrize("n,b,d", [(4, 4.0, 1 << 16), (4, 5.0, (1 << 14) + 9), (8, 4.0, 1 << 15)])
+@pytest.mark.parametrize("n,b,d", [(4, 4.0, 1 << 16), (4, 5.0, (1 << 14) + 9), (8, 4.0, 1 << 15),
+                                    (4, 4.0, (1 << 20) + 256)])
 def test_host_finished_allocation(dq, port, n, b, d):
     """need_host forced on every round: the side-stream host function answers, the
     assignment kernel waits for it; results unchanged."""
