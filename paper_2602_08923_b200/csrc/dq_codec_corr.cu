@@ -7,14 +7,12 @@ namespace dq {
 namespace {
 template <int NS>
 void launch_ns(const CodecArgs& a, int src, bool dar, cudaStream_t st) {
-  const uint32_t per_warp = per_warp_sgs(a.L.nsg);
-  const dim3 grid(persistent_grid((a.L.nsg + per_warp - 1) / per_warp, 64));
   if (src == 0) {
-    if (dar) k_quant<NS, true, 0, true><<<grid, kThreads, 0, st>>>(a);
-    else k_quant<NS, true, 0, false><<<grid, kThreads, 0, st>>>(a);
+    if (dar) launch_hop(k_quant<NS, true, 0, true>, a.L.nsg, a, st);
+    else launch_hop(k_quant<NS, true, 0, false>, a.L.nsg, a, st);
   } else {
-    if (dar) k_quant<NS, true, 1, true><<<grid, kThreads, 0, st>>>(a);
-    else k_quant<NS, true, 1, false><<<grid, kThreads, 0, st>>>(a);
+    if (dar) launch_hop(k_quant<NS, true, 1, true>, a.L.nsg, a, st);
+    else launch_hop(k_quant<NS, true, 1, false>, a.L.nsg, a, st);
   }
 }
 }  // namespace

@@ -39,9 +39,7 @@ void launch_peer_dec_corr(const CodecArgs& a, int src, cudaStream_t st) {
 template <int NS>
 bool launch_pc_dec(const CodecArgs& a, cudaStream_t st, bool launch) {
   if (!launch) return true;
-  const uint32_t per_warp = per_warp_sgs(a.L.nsg);
-  const dim3 grid(persistent_grid((a.L.nsg + per_warp - 1) / per_warp, 64));
-  k_quant<NS, true, 0, true, false, 4, true><<<grid, kThreads, 0, st>>>(a);
+  launch_hop(k_quant<NS, true, 0, true, false, 4, true>, a.L.nsg, a, st);
   return true;
 }
 }  // namespace
@@ -56,10 +54,8 @@ bool launch_quant_dec(const CodecArgs& a, int src, bool peer, cudaStream_t st, b
   }
   if (!a.correlated) {  // independent rounding: no permutation
     if (!launch) return true;
-    const uint32_t per_warp = per_warp_sgs(a.L.nsg);
-    const dim3 grid(persistent_grid((a.L.nsg + per_warp - 1) / per_warp, 64));
-    if (src == 0) k_quant<1, false, 0, true, false, 0, true><<<grid, kThreads, 0, st>>>(a);
-    else k_quant<1, false, 1, true, false, 0, true><<<grid, kThreads, 0, st>>>(a);
+    if (src == 0) launch_hop(k_quant<1, false, 0, true, false, 0, true>, a.L.nsg, a, st);
+    else launch_hop(k_quant<1, false, 1, true, false, 0, true>, a.L.nsg, a, st);
     return true;
   }
   if (a.pc_mode != 4 || src != 0) return false;  // correlated: the slice-reading sink only

@@ -7,13 +7,12 @@ namespace {
 template <bool CORR>
 void launch_gen(const CodecArgs& a, int src, bool dar, cudaStream_t st) {
   constexpr int NS = CORR ? 0 : 1;
-  const dim3 grid(persistent_grid(a.L.nsg, 64));
   if (src == 0) {
-    if (dar) k_quant<NS, CORR, 0, true, true><<<grid, kThreads, 0, st>>>(a);
-    else k_quant<NS, CORR, 0, false, true><<<grid, kThreads, 0, st>>>(a);
+    if (dar) launch_hop(k_quant<NS, CORR, 0, true, true>, a.L.nsg, a, st);
+    else launch_hop(k_quant<NS, CORR, 0, false, true>, a.L.nsg, a, st);
   } else {
-    if (dar) k_quant<NS, CORR, 1, true, true><<<grid, kThreads, 0, st>>>(a);
-    else k_quant<NS, CORR, 1, false, true><<<grid, kThreads, 0, st>>>(a);
+    if (dar) launch_hop(k_quant<NS, CORR, 1, true, true>, a.L.nsg, a, st);
+    else launch_hop(k_quant<NS, CORR, 1, false, true>, a.L.nsg, a, st);
   }
 }
 }  // namespace

@@ -8,15 +8,13 @@ namespace dq {
 namespace {
 template <int NS>
 bool launch_pc_ns(const CodecArgs& a, bool dar, cudaStream_t st) {
-  const uint32_t per_warp = per_warp_sgs(a.L.nsg);
-  const dim3 grid(persistent_grid((a.L.nsg + per_warp - 1) / per_warp, 64));
   if (a.pc_mode == 3 && !dar) {
-    k_quant<NS, true, 0, false, false, 3><<<grid, kThreads, 0, st>>>(a);
+    launch_hop(k_quant<NS, true, 0, false, false, 3>, a.L.nsg, a, st);
     return true;
   }
   if (a.pc_mode == 4) {
-    if (dar) k_quant<NS, true, 0, true, false, 4><<<grid, kThreads, 0, st>>>(a);
-    else k_quant<NS, true, 0, false, false, 4><<<grid, kThreads, 0, st>>>(a);
+    if (dar) launch_hop(k_quant<NS, true, 0, true, false, 4>, a.L.nsg, a, st);
+    else launch_hop(k_quant<NS, true, 0, false, false, 4>, a.L.nsg, a, st);
     return true;
   }
   return false;
