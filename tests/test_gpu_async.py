@@ -4,8 +4,9 @@ synchronisation inside a round.
 * bit-identical to the oracle's run_round (proj/src/engine.cpp:269-418): synced gradient,
   widths, permutation, u, payload and wire accounting - without the wire-hash mode, which
   forces the host-synchronous path;
-* the rare rounds the device cannot certify, forced: the host function finishes the
-  allocation from the exported F (allocation.cpp:195-260) and releases the assignment;
+* the rare rounds the device cannot certify, forced: the context's host service thread
+  finishes the allocation from the exported F (allocation.cpp:195-260) and releases the
+  assignment;
 * metrics=False returns at once; Context.wait() fills the allocation fields later;
 * a whole round captured in a CUDA graph and replayed on new inputs equals direct rounds.
 """
@@ -61,8 +62,9 @@ def test_async_round_matches_oracle(dq, port, n, b, topo, d):
 @pytest.mark.parametrize("n,b,d", [(4, 4.0, 1 << 16), (4, 5.0, (1 << 14) + 9), (8, 4.0, 1 << 15),
                                     (4, 4.0, (1 << 20) + 256)])
 def test_host_finished_allocation(dq, port, n, b, d):
-    """need_host forced on every round: the side-stream host function answers, the
-    assignment kernel waits for it; results unchanged."""
+    """need_host forced on every round: the host service thread answers, the assignment
+    waits for it; results unchanged (T <= 4096: the one-CTA allocation; larger: the
+    cooperative search)."""
     from paper_2602_08923_b200._lib import check, lib
     ws = _workers(port, n, d, seed=23 + n)
     want = port.run_round(ws, port.round_cfg(n, b, "ring", seed=1))
