@@ -234,6 +234,9 @@ struct dq_ctx {
   DevBuf<float> accs;     // per-worker chunk accumulators (butterfly)
   DevBuf<uint32_t> pcache; // simulated round: the chunk's permutation slices (slots 1..n-1)
   DevBuf<float> stage;    // host-round staging of inputs / output
+  std::vector<cudaStream_t> cstreams;  // simulated rounds: concurrent chunk chains
+  std::vector<cudaEvent_t> cjoin;
+  cudaEvent_t cfork = nullptr;
   dq_round_info last_info{};  // the last round's host-known info (dq_round_wait)
   AllocState* h_state = nullptr;
   uint32_t* h_counts = nullptr;
@@ -298,6 +301,9 @@ struct dq_ctx {
     if (pm.base) cudaFree(pm.base);
     if (sm.base) cudaFree(sm.base);
     if (h_state) cudaFreeHost(h_state);
+    for (cudaStream_t s2 : cstreams) cudaStreamDestroy(s2);
+    for (cudaEvent_t e2 : cjoin) cudaEventDestroy(e2);
+    if (cfork) cudaEventDestroy(cfork);
     if (svc.joinable()) {
       svc_stop = true;
       svc.join();
@@ -976,6 +982,8 @@ struct Prepared {
   size_t max_chunk_bytes;
 };
 
+constexpr uint32_t kChunkStreams = 8;  // worker streams of a simulated round's chunk chains
+
 // Rounds that allocate asynchronously: the fast allocator without the instrumentation or
 // wire-hash modes (both read per-chunk sizes on the host); DQ_SYNC_ALLOC=1 turns it off.
 bool async_alloc_ok(const dq_ctx* ctx, bool collect_wire) {
@@ -1114,16 +1122,36 @@ void sim_round(dq_ctx* ctx, const float* const* xs, size_t d, float* out, int fl
   Prepared p = prepare(ctx, T, st, async);
   if (!async) fill_info_alloc(info, p);
 
-  // message pool: per-worker pending slots + scratch, reused per chunk; plus one gather
-  // (sink output) buffer per chunk, decoded together at the end of the round
+  // The chunks' event chains are independent: asynchronous rounds run chunk ch on worker
+  // stream ch % kChunkStreams (forked after the allocation, joined before the gather decode),
+  // so one chunk's kernels fill the others' partial last waves; each chunk then owns its
+  // message slots, slices and accumulators.  The wire-hash and profiling modes keep one stream.
+  const bool multi = async && n >= 2;
+  const uint32_t nstreams = multi ? std::min<uint32_t>(n, kChunkStreams) : 1;
+  if (multi) {
+    while (ctx->cstreams.size() < nstreams) {
+      cudaStream_t s2;
+      DQ_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+      ctx->cstreams.push_back(s2);
+      cudaEvent_t e2;
+      DQ_CUDA(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
+      ctx->cjoin.push_back(e2);
+    }
+    if (!ctx->cfork) DQ_CUDA(cudaEventCreateWithFlags(&ctx->cfork, cudaEventDisableTiming));
+    DQ_CUDA(cudaEventRecord(ctx->cfork, st));
+    for (uint32_t k = 0; k < nstreams; ++k) DQ_CUDA(cudaStreamWaitEvent(ctx->cstreams[k], ctx->cfork, 0));
+  }
+  // message pool: per-worker pending slots + scratch (per chunk when the chunks run
+  // concurrently, else reused); plus one gather (sink output) buffer per chunk
   const size_t mb = p.max_chunk_bytes;
-  ctx->msgs.reserve((n + 2 + n) * mb);
+  const uint32_t scratch_sets = multi ? n : 1;
+  ctx->msgs.reserve((scratch_sets * (n + 2) + n) * mb);
   std::vector<int> gslots(n, -1);
   std::vector<char> decoded(n, 0);  // chunk decoded into `out` by its fused sink
   uint32_t max_nsg = 0;
   for (uint32_t i = 0; i < n; ++i) max_nsg = std::max(max_nsg, p.lo[i + 1] - p.lo[i]);
   const bool need_acc = c.topology == DQ_BUTTERFLY;
-  if (need_acc) ctx->accs.reserve(static_cast<size_t>(n) * max_nsg * 256);
+  if (need_acc) ctx->accs.reserve(static_cast<size_t>(scratch_sets) * n * max_nsg * 256);
   std::vector<uint8_t> host_soa, host_ref;
   uint64_t H = 0xcbf29ce484222325ULL;
   // Permutation slices: every simulated hop of a chunk draws from the same per-entry
@@ -1133,10 +1161,12 @@ void sim_round(dq_ctx* ctx, const float* const* xs, size_t d, float* out, int fl
   // hop s reads - the same slices the distributed ring ships to the rank running hop s.
   const bool use_pc = c.correlated && n >= 2 && n <= 8 && p.a.gs == 16 && p.a.ss == 2 && p.a.gshift == 1;
   const size_t slice_words = static_cast<size_t>(max_nsg) * 32;  // u32 per (super-group, lane)
-  if (use_pc) ctx->pcache.reserve((n - 1) * slice_words);
-  auto slice = [&](uint32_t s) { return ctx->pcache.p + (s - 1) * slice_words; };
+  if (use_pc) ctx->pcache.reserve(scratch_sets * (n - 1) * slice_words);
 
   for (uint32_t ch = 0; ch < n; ++ch) {
+    const cudaStream_t cst = multi ? ctx->cstreams[ch % nstreams] : st;  // this chunk's stream
+    const size_t set = multi ? ch : 0;                                    // its scratch set
+    auto slice = [&](uint32_t s) { return ctx->pcache.p + (set * (n - 1) + s - 1) * slice_words; };
     const Plan plan = make_plan(n, ch, c.topology);
     const Layout L = chunk_layout(p.a, p.lo[ch], p.lo[ch + 1]);
     CodecArgs base = base_args(c, ch);
@@ -1152,9 +1182,11 @@ void sim_round(dq_ctx* ctx, const float* const* xs, size_t d, float* out, int fl
     for (size_t e = 0; e < plan.red.size(); ++e) last_in[plan.red[e].rcv] = static_cast<int>(e);
     std::vector<int> free_slots;
     for (int k = static_cast<int>(n) + 1; k >= 0; --k) free_slots.push_back(k);
-    const int gather_dst = static_cast<int>(n + 2 + ch);  // this chunk's sink output lives here
-    auto slot_ptr = [&](int k) { return ctx->msgs.p + static_cast<size_t>(k) * mb; };
-    auto acc_ptr = [&](uint32_t w) { return ctx->accs.p + static_cast<size_t>(w) * max_nsg * 256; };
+    const int gather_dst = static_cast<int>(scratch_sets * (n + 2) + ch);  // this chunk's sink output lives here
+    auto slot_ptr = [&](int k) {
+      return ctx->msgs.p + (k < static_cast<int>(n + 2) ? set * (n + 2) + k : static_cast<size_t>(k)) * mb;
+    };
+    auto acc_ptr = [&](uint32_t w) { return ctx->accs.p + (set * n + w) * max_nsg * 256; };
     uint64_t hsh = 0xcbf29ce484222325ULL;
     auto hash_msg = [&](const uint8_t* dmsg, int times_fresh_first) {
       if (!collect_wire) return;
@@ -1192,7 +1224,7 @@ void sim_round(dq_ctx* ctx, const float* const* xs, size_t d, float* out, int fl
         else
           a.pin = slice(ev.slot);
       }
-      timed(ctx, dar ? K_DAR : K_LEAF, quant_bytes(L, dar), st, [&] { launch_quant(a, src, dar, st); });
+      timed(ctx, dar ? K_DAR : K_LEAF, quant_bytes(L, dar), cst, [&] { launch_quant(a, src, dar, cst); });
       if (dar) {
         free_slots.push_back(pend_slot[ev.snd]);
         pend_slot[ev.snd] = -1;
@@ -1215,10 +1247,10 @@ void sim_round(dq_ctx* ctx, const float* const* xs, size_t d, float* out, int fl
           g.pin = slice(plan.sink_slot);
         }
         g.dec_out = out;  // fused decode of the chunk into the output where a variant exists
-        decoded[ch] = launch_quant_dec(g, gsrc, false, st, false);
-        timed(ctx, K_DAR, quant_bytes(L, true) + (decoded[ch] ? 1032.0 * L.nsg : 0.0), st, [&] {
-          if (!decoded[ch]) launch_quant(g, gsrc, true, st);
-          else launch_quant_dec(g, gsrc, false, st);
+        decoded[ch] = launch_quant_dec(g, gsrc, false, cst, false);
+        timed(ctx, K_DAR, quant_bytes(L, true) + (decoded[ch] ? 1032.0 * L.nsg : 0.0), cst, [&] {
+          if (!decoded[ch]) launch_quant(g, gsrc, true, cst);
+          else launch_quant_dec(g, gsrc, false, cst);
         });
         free_slots.push_back(os);
         gather_slot = gs;
@@ -1227,7 +1259,7 @@ void sim_round(dq_ctx* ctx, const float* const* xs, size_t d, float* out, int fl
         g.in = slot_ptr(os);
         const int gsrc = operand(r, g);
         g.acc_out = acc_ptr(r);
-        timed(ctx, K_DA, 2048.0 * L.nsg + L.bytes(), st, [&] { launch_da(g, gsrc, st); });
+        timed(ctx, K_DA, 2048.0 * L.nsg + L.bytes(), cst, [&] { launch_da(g, gsrc, cst); });
         has_acc[r] = 1;
         free_slots.push_back(os);
       }
@@ -1243,6 +1275,12 @@ void sim_round(dq_ctx* ctx, const float* const* xs, size_t d, float* out, int fl
     H ^= hsh + 0x9e3779b97f4a7c15ULL + (H << 6) + (H >> 2);
   }
   if (collect_wire) info->wire_hash = H;
+  if (multi) {  // join the chunk streams
+    for (uint32_t k = 0; k < nstreams; ++k) {
+      DQ_CUDA(cudaEventRecord(ctx->cjoin[k], ctx->cstreams[k]));
+      DQ_CUDA(cudaStreamWaitEvent(st, ctx->cjoin[k], 0));
+    }
+  }
   {  // the chunks whose sink had no fused decode
     GatherArgs g{};
     set_format(g, ctx->cfg);
