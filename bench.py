@@ -463,7 +463,7 @@ def bench_dist(args):
 def bench_reference(args):
     """--impl reference: the reference's CPU run_round (oracle/_ref) on the host cores, rank 0
     only, on the SAME inputs as our arm (make_inputs).  Every step is the full workload when
-    the whole --steps/--warmup run fits in about four minutes (the warm-up round measures
+    the whole --steps/--warmup run fits in about five and a half minutes (the warm-up round measures
     it), else the first entries of every worker - stated in config and cpu_baseline."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -485,8 +485,8 @@ def bench_reference(args):
     t0 = time.perf_counter()
     res = ora.run_round([np.ascontiguousarray(w[:dsamp]) for w in hw], cfg)  # first warm-up round
     t1 = time.perf_counter() - t0
-    if t1 * (total - 1) > 240.0:  # keep the run to a few minutes: a per-step prefix sample
-        dsamp = max(1 << 16, int(dsamp * 240.0 / (t1 * max(total - 1, 1))) // 256 * 256)
+    if t1 * (total - 1) > 330.0:  # keep the run to a few minutes: a per-step prefix sample
+        dsamp = max(1 << 16, int(dsamp * 330.0 / (t1 * max(total - 1, 1))) // 256 * 256)
     ws = [np.ascontiguousarray(w[:dsamp]) for w in hw]
     for _ in range(max(0, args.warmup) - 1):
         ora.run_round(ws, cfg)

@@ -223,9 +223,19 @@ int dq_profile_read(dq_ctx* ctx, dq_kernel_profile* out, int cap, int* count, in
  * decode's code * sg_scale / 255 fast path with div.rn for every code and every
  * bf16 scale.  *mismatches = count. */
 int dq_selftest(int which, uint64_t n, uint64_t seed, uint64_t* mismatches);
-/* Test hook: make every asynchronous allocation hand its decision to the host
- * function (the path of rounds whose thresholds the device cannot certify). */
+/* Test hook: on = 1 makes every asynchronous allocation hand its decision to the
+ * host service thread (the path of rounds the device cannot decide); on = 2
+ * makes every cooperative search consult the host for its candidates' glibc
+ * thresholds (the path of ambiguous float thresholds); 0 = normal. */
 int dq_debug_force_host_alloc(int on);
+/* Diagnostics.  *finished: rounds of this context whose allocation the host
+ * finished (asynchronous rounds the device could not decide, plus the
+ * synchronous path's exact walks) - normally 0, each costs a host sort of the
+ * flips in the round's critical path.  *consulted (may be NULL): asynchronous
+ * rounds that asked the host only for the candidates' glibc thresholds (a float
+ * threshold within rounding of an F_j) - a few microseconds of host math and
+ * one mapped-memory round trip. */
+int dq_ctx_host_allocations(const dq_ctx* ctx, uint64_t* finished, uint64_t* consulted);
 
 /* Multi-GPU: one process per GPU.  Rank 0 creates the id, the caller ships the
  * 128 bytes to every rank (e.g. torch.distributed), every rank joins. */

@@ -120,6 +120,7 @@ SIGNATURES = {
     "dq_round_wait": (C.c_int, [_V, _P(RoundInfo)]),
     "dq_codec_format_set": (C.c_int, [C.c_uint32, C.c_int, _P(C.c_uint32), _P(C.c_int)]),
     "dq_debug_force_host_alloc": (C.c_int, [C.c_int]),
+    "dq_ctx_host_allocations": (C.c_int, [_V, _P(C.c_uint64), _P(C.c_uint64)]),
     "dq_comm_set_transport": (C.c_int, [_V, C.c_int]),
     "dq_comm_get_transport": (C.c_int, [_V, _P(C.c_int)]),
 }

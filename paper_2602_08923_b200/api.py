@@ -381,6 +381,13 @@ class Context:
         check(lib().dq_round_wait(self.h, C.byref(info)))
         return _info_dict(info)
 
+    def host_allocations(self) -> dict:
+        """Diagnostics: rounds whose bit allocation the host finished ("finished", rare) and
+        rounds that only asked the host for the candidates' glibc thresholds ("consulted")."""
+        f, c = C.c_uint64(), C.c_uint64()
+        check(lib().dq_ctx_host_allocations(self.h, C.byref(f), C.byref(c)))
+        return {"finished": f.value, "consulted": c.value}
+
     def close(self) -> None:
         if getattr(self, "h", None):
             lib().dq_ctx_destroy(self.h)

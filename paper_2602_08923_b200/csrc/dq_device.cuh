@@ -9,6 +9,7 @@
 // compiled with --fmad=false -prec-div=true -ftz=false as a second guard.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 namespace dq {
@@ -22,6 +23,24 @@ constexpr uint64_t kGolden = 0x9e3779b97f4a7c15ULL;
 constexpr uint64_t kSeedSalt = 0x6a09e667f3bcc909ULL;
 
 enum Purpose : uint32_t { kEntryQuant = 1, kScaleQuant = 2, kPermutation = 3 };
+
+// Device-side bounds and invariant checks of the debug build (-DDQ_DEBUG_CHECKS=1, the
+// `debug` variant of tools/build_debug.sh): the stand-in for compute-sanitizer, which this
+// GPU pool does not run.  A failed check prints its condition and traps the kernel.
+#if defined(DQ_DEBUG_CHECKS) && DQ_DEBUG_CHECKS
+#define DQ_CHECK(c)                                                                             \
+  do {                                                                                          \
+    if (!(c)) {                                                                                 \
+      printf("DQ_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #c,        \
+             blockIdx.x, threadIdx.x);                                                          \
+      __trap();                                                                                 \
+    }                                                                                           \
+  } while (0)
+#else
+#define DQ_CHECK(c) \
+  do {              \
+  } while (0)
+#endif
 
 // Spin-wait budget of every kernel that waits on another GPU or on the host (peer flags,
 // the statistics exchange, a host allocation answer): a wait longer than this traps the

@@ -260,6 +260,8 @@ struct dq_ctx {
   } rec;
   double* h_vn = nullptr;
   uint32_t last_T = 0;
+  std::atomic<uint64_t> host_allocs{0};    // asynchronous rounds finished by alloc_service
+  std::atomic<uint64_t> host_consults{0};  // threshold consults answered by alloc_service
   uint64_t alloc_redos = 0;  // rounds where the device thresholds differed from glibc's
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   // round-boundary events of the last asynchronously finished round (measured at the next sync)
@@ -643,7 +645,13 @@ AllocResult allocate_fast(dq_ctx* ctx, const dq_config& c, const float* dF, uint
     if (!s.cand_present[c]) continue;
     float a, b;
     thr(cand[c].u(), &a, &b);
-    mismatch |= a != s.cand_t24[c] || b != s.cand_t48[c];
+    // a threshold the device left ambiguous (two adjacent floats, no F_j equal to the lower)
+    // gives the same widths with either float
+    auto same = [&](float h, float dv, float amb) {
+      if (h == dv) return true;
+      return s.namb == 0 && amb > 0.0f && std::min(h, dv) == amb && std::nextafter(amb, INFINITY) == std::max(h, dv);
+    };
+    mismatch |= !same(a, s.cand_t24[c], s.amb[c][0]) || !same(b, s.cand_t48[c], s.amb[c][1]);
   }
   double u;
   float t24, t48;
@@ -732,14 +740,14 @@ AllocResult allocate_fast(dq_ctx* ctx, const dq_config& c, const float* dF, uint
 
 // u of the search's chosen candidate, re-derived with the host libm exactly as
 // fast_sample_points does (allocation.cpp:201-224) from the flips the search identified.
-double host_u_of(const AllocState& s) {
+// glibc u of candidate sample c (0..2 = L-1, L, L+1) from the device's flip records
+double host_cand_u(const AllocState& s, int c) {
   auto hflip = [](const FlipRec& q) {
     float f;
     std::memcpy(&f, &q.fbits, 4);
     return (q.type ? 8.0 : 4.0) - kAlpha * std::log2(static_cast<double>(f));
   };
   auto clampu = [](double v) { return v < -1e6 ? -1e6 : (v > 1e6 ? 1e6 : v); };
-  const int c = s.choice >= 0 ? s.choice : 1;
   const FlipRec* l = nullptr;
   const FlipRec* r = nullptr;
   if (s.status == 2) {
@@ -755,6 +763,7 @@ double host_u_of(const AllocState& s) {
   if (l) return clampu(hflip(*l) + 1.0);
   return 0.0;
 }
+double host_u_of(const AllocState& s) { return host_cand_u(s, s.choice >= 0 ? s.choice : 1); }
 
 // allocate_fast on the host (allocation.cpp:195-260, the same sorted samples and the same
 // bisection): the rare asynchronous rounds whose thresholds the device could not certify.
@@ -810,6 +819,23 @@ bool host_allocate_fast(const float* F, uint32_t T, uint32_t S, double budget, d
 // release the assignment kernel, which waits for `resolved` to reach the round's epoch.
 void host_alloc_resolve(HostMsg* m) {
   const AllocState& s = m->state;
+  static const bool verbose = std::getenv("DQ_DEBUG_ALLOC") != nullptr;
+  if (verbose) {
+    std::fprintf(stderr, "dynamiq_b200: host finish: T=%u certified=%u choice=%d status=%u passes=%u\n", s.T,
+                 s.certified, s.choice, s.status, s.passes);
+    for (int c = 0; c < 3; ++c) {
+      if (!s.cand_present[c]) continue;
+      const double uu = s.cand_u[c];
+      const double d24 = std::exp2((4.0 - uu) / kAlpha), d48 = std::exp2((8.0 - uu) / kAlpha);
+      std::fprintf(stderr, "  cand %d: u=%.17g t24=%a (host %a, d %a) t48=%a (host %a, d %a)\n", c, uu,
+                   s.cand_t24[c], static_cast<float>(d24), d24, s.cand_t48[c], static_cast<float>(d48), d48);
+    }
+    for (int k = 0; k < 4; ++k) {
+      float f;
+      std::memcpy(&f, &s.slot[k].fbits, 4);
+      std::fprintf(stderr, "  slot %d: present=%u type=%u F=%a\n", k, s.slot[k].present, s.slot[k].type, f);
+    }
+  }
   double u = 0.0;
   float a = INFINITY, b = INFINITY;  // infeasible: all width 2 (the round is reported as failed)
   const bool ok = host_allocate_fast(m->hF, s.T, s.S, s.budget, &u, &a, &b);
@@ -820,6 +846,20 @@ void host_alloc_resolve(HostMsg* m) {
   __atomic_store_n(const_cast<uint32_t*>(&m->resolved), s.epoch, __ATOMIC_RELEASE);
 }
 
+// Threshold consult (alloc_consult): the glibc u and float thresholds of each present
+// candidate - a few log2 / exp2 calls, the device recounts with them.
+void host_thr_resolve(HostMsg* m, uint32_t tag) {
+  const AllocState& s = m->state;
+  for (int c = 0; c < 3; ++c) {
+    if (!s.cand_present[c]) continue;
+    const double u = host_cand_u(s, c);
+    m->thr_u[c] = u;
+    m->thr_t24[c] = static_cast<float>(std::exp2((4.0 - u) / kAlpha));
+    m->thr_t48[c] = static_cast<float>(std::exp2((8.0 - u) / kAlpha));
+  }
+  __atomic_store_n(const_cast<uint32_t*>(&m->thr_resolved), tag, __ATOMIC_RELEASE);
+}
+
 // Per-context host service thread: polls both mailboxes for a request newer than its
 // answer (no CUDA calls, no per-round callbacks: the common round never involves the host).
 void alloc_service(dq_ctx* ctx) {
@@ -827,9 +867,16 @@ void alloc_service(dq_ctx* ctx) {
     bool busy = false;
     for (int p = 0; p < 2; ++p) {
       HostMsg* m = ctx->hmsg + p;
+      const uint32_t treq = __atomic_load_n(const_cast<uint32_t*>(&m->thr_request), __ATOMIC_ACQUIRE);
+      if (treq != 0 && treq != m->thr_resolved) {
+        host_thr_resolve(m, treq);
+        ctx->host_consults.fetch_add(1, std::memory_order_relaxed);
+        busy = true;
+      }
       const uint32_t req = __atomic_load_n(const_cast<uint32_t*>(&m->request), __ATOMIC_ACQUIRE);
       if (req != 0 && req != m->resolved && req == m->state.epoch) {
         host_alloc_resolve(m);
+        ctx->host_allocs.fetch_add(1, std::memory_order_relaxed);
         busy = true;
       }
     }
@@ -2541,6 +2588,14 @@ int dq_round_wait(dq_ctx* ctx, dq_round_info* info) {
     *info = ctx->last_info;
     if (ctx->rec.async) finish_info(ctx, info);
     info->ms_total = ctx->last_round_ms;
+  });
+}
+
+int dq_ctx_host_allocations(const dq_ctx* ctx, uint64_t* finished, uint64_t* consulted) {
+  return guarded([&] {
+    if (!ctx || !finished) invalid("null argument");
+    *finished = ctx->host_allocs.load(std::memory_order_relaxed) + ctx->alloc_redos;
+    if (consulted) *consulted = ctx->host_consults.load(std::memory_order_relaxed);
   });
 }
 

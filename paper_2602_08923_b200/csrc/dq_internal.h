@@ -173,6 +173,12 @@ struct AllocState {
   double cand_u[3];
   float cand_t24[3], cand_t48[3];
   unsigned long long cand_n8[3], cand_n48[3];
+  // a threshold whose float rounding is not stable can only be one of two adjacent floats
+  // a < b; the widths differ between them only for an F_j equal to a: amb[c][0/1] = a for
+  // the uncertified t24 / t48 of candidate c (else -1), namb = how many F_j equal one
+  float amb[3][2];
+  unsigned long long namb;
+  uint32_t consulted, pad1_;  // the candidates' exact thresholds came from the host (HostMsg::thr_*)
   int32_t choice;          // chosen candidate (0..2); -1 ambiguous (host walk); -2 infeasible
   // chosen u and thresholds (read by the assignment kernels)
   double u;
@@ -199,6 +205,12 @@ struct HostMsg {
   int32_t host_status;        // 0 ok, 3 infeasible budget, 5 internal error (reported at the next sync)
   double u;                   // host answer: u, t24, t48
   float t24, t48;
+  // threshold consult (asynchronous rounds whose candidate thresholds are ambiguous and
+  // some F_j equals the lower float): the search mirrors its state, raises thr_request;
+  // the service thread answers each present candidate's glibc u and float thresholds
+  volatile uint32_t thr_request, thr_resolved;
+  double thr_u[3];
+  float thr_t24[3], thr_t48[3];
 };
 constexpr int kAllocBins = 1024;
 constexpr int kAllocMaxPasses = 8;

@@ -559,11 +559,20 @@ __device__ void alloc_candidates(AllocState* s, double alpha) {
   // while glibc's double (log2 and exp2 within ~0.5 ulp, CUDA's within 1-2 ulp, five
   // rounded double operations between them on |log2 F| <= 150) differs from the device
   // double by far less than 2^-43 relative
-  auto stable = [](double d) {
+  // stable: float(d) is certain; otherwise the two possible floats lo < hi are adjacent and
+  // the widths (F_j >= t) differ between them only for F_j == lo: certified unless some F_j
+  // equals lo (counted by alloc_count, checked by alloc_decide)
+  auto stable = [](double d, float* amb) {
     const float lo = __double2float_rn(__dmul_rd(d, 1.0 - 0x1p-40)), hi = __double2float_rn(__dmul_ru(d, 1.0 + 0x1p-40));
-    return __float_as_uint(lo) == __float_as_uint(hi);
+    if (__float_as_uint(lo) == __float_as_uint(hi)) {
+      *amb = -1.0f;
+      return true;
+    }
+    *amb = lo;
+    return nextafterf(lo, INFINITY) == hi && lo > 0.0f;  // else (overflow / underflow edges): uncertified
   };
   uint32_t cert = 1;
+  s->namb = 0;
   for (int c = 0; c < 3; ++c) {
     double u = s->cand_u[c];
     u = u < -1e6 ? -1e6 : (u > 1e6 ? 1e6 : u);
@@ -571,20 +580,62 @@ __device__ void alloc_candidates(AllocState* s, double alpha) {
     const double d24 = exp2(__ddiv_rn(__dsub_rn(4.0, u), alpha)), d48 = exp2(__ddiv_rn(__dsub_rn(8.0, u), alpha));
     s->cand_t24[c] = static_cast<float>(d24);
     s->cand_t48[c] = static_cast<float>(d48);
-    if (s->cand_present[c]) cert &= stable(d24) && stable(d48) ? 1u : 0u;
+    const bool st24 = stable(d24, &s->amb[c][0]), st48 = stable(d48, &s->amb[c][1]);
+    if (s->cand_present[c]) cert &= (st24 || s->amb[c][0] > 0.0f) && (st48 || s->amb[c][1] > 0.0f) ? 1u : 0u;
+    else s->amb[c][0] = s->amb[c][1] = -1.0f;
     s->cand_n8[c] = 0;
     s->cand_n48[c] = 0;
   }
   s->certified = cert;
+  s->consulted = 0;
+}
+
+// Ambiguous thresholds with an F_j equal to the lower float: ask the host service thread
+// for the candidates' glibc u and thresholds (microseconds on the host, instead of handing
+// it the whole allocation), then recount.  Block 0 only; the caller grid-syncs.
+__device__ void alloc_consult(AllocState* s, HostMsg* m) {
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(s);
+  uint32_t* dst = reinterpret_cast<uint32_t*>(&m->state);
+  for (uint32_t k = threadIdx.x; k < sizeof(AllocState) / 4; k += blockDim.x) dst[k] = src[k];
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t tag = s->epoch + 1;
+    m->thr_request = tag;
+    __threadfence_system();
+    const uint64_t t0 = dq_globaltimer();
+    for (;;) {
+      uint32_t v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(&m->thr_resolved) : "memory");
+      if (v == tag) break;
+      __nanosleep(500);
+      if (dq_globaltimer() - t0 > g_spin_ns) __trap();
+    }
+    for (int c = 0; c < 3; ++c) {
+      if (s->cand_present[c]) {
+        s->cand_u[c] = *reinterpret_cast<volatile double*>(&m->thr_u[c]);
+        s->cand_t24[c] = *reinterpret_cast<volatile float*>(&m->thr_t24[c]);
+        s->cand_t48[c] = *reinterpret_cast<volatile float*>(&m->thr_t48[c]);
+      }
+      s->amb[c][0] = s->amb[c][1] = -1.0f;
+      s->cand_n8[c] = 0;
+      s->cand_n48[c] = 0;
+    }
+    s->consulted = 1;
+  }
 }
 
 __device__ void alloc_count(const float* __restrict__ F, uint32_t T, AllocState* s) {
-  float t24[3], t48[3];
+  float t24[3], t48[3], amb[6];
+  bool any_amb = false;
   for (int c = 0; c < 3; ++c) {
     t24[c] = s->cand_t24[c];
     t48[c] = s->cand_t48[c];
+    amb[2 * c] = s->amb[c][0];
+    amb[2 * c + 1] = s->amb[c][1];
+    any_amb |= amb[2 * c] > 0.0f || amb[2 * c + 1] > 0.0f;
   }
-  unsigned long long n8[3] = {0, 0, 0}, n48[3] = {0, 0, 0};
+  unsigned long long n8[3] = {0, 0, 0}, n48[3] = {0, 0, 0}, namb = 0;
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < T; j += gridDim.x * blockDim.x) {
     const float f = F[j];
 #pragma unroll
@@ -592,6 +643,14 @@ __device__ void alloc_count(const float* __restrict__ F, uint32_t T, AllocState*
       n8[c] += f >= t48[c];
       n48[c] += f >= t24[c];
     }
+    if (any_amb) {
+#pragma unroll
+      for (int k = 0; k < 6; ++k) namb += f == amb[k];
+    }
+  }
+  if (__syncthreads_or(any_amb)) {
+    namb = block_reduce<kRedAdd>(namb);
+    if (threadIdx.x == 0 && namb) atomicAdd(&s->namb, namb);
   }
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
@@ -605,7 +664,7 @@ __device__ void alloc_count(const float* __restrict__ F, uint32_t T, AllocState*
     }
 }
 
-__device__ int g_force_host_alloc;  // test hook (set_force_host_alloc)
+__device__ int g_force_host_alloc;  // test hook (set_force_host_alloc): 1 finish on the host, 2 consult
 
 // the reference's choice: the largest sample whose float-threshold payload fits
 __device__ void alloc_decide(AllocState* s, double budget, uint32_t S, uint32_t T) {
@@ -623,7 +682,8 @@ __device__ void alloc_decide(AllocState* s, double budget, uint32_t S, uint32_t 
   s->u = s->cand_u[c];
   s->t24 = s->cand_t24[c];
   s->t48 = s->cand_t48[c];
-  s->need_host = (!s->certified || ch < 0 || g_force_host_alloc) ? 1u : 0u;
+  if (s->namb && !s->consulted) s->certified = 0;
+  s->need_host = (!s->certified || ch < 0 || g_force_host_alloc == 1) ? 1u : 0u;
 }
 
 // The whole search in one cooperative launch: prep -> up to kAllocMaxPasses x
@@ -678,6 +738,12 @@ __global__ void __launch_bounds__(kAllocBins) k_alloc_coop(const float* __restri
   grid.sync();
   alloc_count(F, T, st);
   grid.sync();
+  if (w.hmsg && (st->namb || g_force_host_alloc == 2) && st->certified) {  // uniform: namb is not written again this round
+    if (blockIdx.x == 0) alloc_consult(st, w.hmsg);
+    grid.sync();
+    alloc_count(F, T, st);
+    grid.sync();
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     alloc_decide(st, budget, S, T);
     st->T = T;
@@ -722,9 +788,12 @@ __device__ __forceinline__ double key_double(uint64_t k) {  // inverse of dkey
   const uint64_t b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
   return __longlong_as_double(static_cast<long long>(b));
 }
-__device__ __forceinline__ bool stable_float(double d) {
+// float(d) certain: -1 (never equals an F_j >= 0); two adjacent candidates lo < hi: lo (the
+// probe stays certified if no F_j equals it, see alloc_candidates); else NaN (uncertified)
+__device__ __forceinline__ float ambiguous_float(double d) {
   const float lo = __double2float_rn(__dmul_rd(d, 1.0 - 0x1p-40)), hi = __double2float_rn(__dmul_ru(d, 1.0 + 0x1p-40));
-  return __float_as_uint(lo) == __float_as_uint(hi);
+  if (__float_as_uint(lo) == __float_as_uint(hi)) return -1.0f;
+  return nextafterf(lo, INFINITY) == hi && lo > 0.0f ? lo : __int_as_float(0x7fc00000);
 }
 __device__ __forceinline__ unsigned long long small_block_sum(unsigned long long v, unsigned long long* red) {
 #pragma unroll
@@ -751,7 +820,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_alloc_small(const float* __re
   uint32_t* UV = reinterpret_cast<uint32_t*>(UK + N);        // their super-group | type << 31
   __shared__ unsigned long long red[kSmallThreads / 32];
   __shared__ uint32_t m_sh;
-  __shared__ float thr_sh[2];
+  __shared__ float thr_sh[4];
   __shared__ int ok_sh, lo_sh, hi_sh, cert_sh;
   AllocState* st = w.state;
   const int t = threadIdx.x;
@@ -827,17 +896,21 @@ __global__ void __launch_bounds__(kSmallThreads) k_alloc_small(const float* __re
       const double d24 = exp2(__ddiv_rn(__dsub_rn(4.0, u), alpha)), d48 = exp2(__ddiv_rn(__dsub_rn(8.0, u), alpha));
       thr_sh[0] = static_cast<float>(d24);
       thr_sh[1] = static_cast<float>(d48);
-      if (!stable_float(d24) || !stable_float(d48)) cert_sh = 0;
+      thr_sh[2] = ambiguous_float(d24);
+      thr_sh[3] = ambiguous_float(d48);
+      if (thr_sh[2] != thr_sh[2] || thr_sh[3] != thr_sh[3]) cert_sh = 0;
     }
     __syncthreads();
-    const float t24 = thr_sh[0], t48 = thr_sh[1];
-    unsigned long long wsum = 0;
+    const float t24 = thr_sh[0], t48 = thr_sh[1], a24 = thr_sh[2], a48 = thr_sh[3];
+    unsigned long long wsum = 0;  // payload units (< 2^32) + 2^32 x (F_j equal to an ambiguous float)
     for (uint32_t j = t; j < T; j += kSmallThreads) {
       const float f = F[j];
       wsum += f >= t48 ? 8 : (f >= t24 ? 4 : 2);
+      wsum += static_cast<unsigned long long>(f == a24 || f == a48) << 32;
     }
     const unsigned long long tot = small_block_sum(wsum, red);
-    return static_cast<double>(tot * S) <= budget;
+    if (t == 0 && (tot >> 32)) cert_sh = 0;
+    return static_cast<double>((tot & 0xffffffffull) * S) <= budget;
   };
   if (t == 0) {
     lo_sh = 0;
@@ -893,8 +966,8 @@ __global__ void __launch_bounds__(kSmallThreads) k_alloc_small(const float* __re
     st->u = u;
     st->t24 = static_cast<float>(d24);
     st->t48 = static_cast<float>(d48);
-    st->certified = cert_sh && stable_float(d24) && stable_float(d48) ? 1u : 0u;
-    st->need_host = (!st->certified || !feasible || g_force_host_alloc) ? 1u : 0u;
+    st->certified = cert_sh ? 1u : 0u;  // every probe (the final one included) certified
+    st->need_host = (!st->certified || !feasible || g_force_host_alloc == 1) ? 1u : 0u;
     st->T = T;
     st->S = S;
     st->budget = budget;

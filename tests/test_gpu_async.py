@@ -117,3 +117,55 @@ def test_round_captured_in_cuda_graph(dq, port):
         assert np.array_equal(out.cpu().numpy().view(np.uint32), want["synced"].view(np.uint32)), seed
     del g
     ctx.close()
+
+
+@pytest.mark.parametrize("n,b,d", [(4, 4.0, 1 << 16), (2, 3.0, (1 << 20) + 256), (8, 4.0, 1 << 15)])
+def test_threshold_consult(dq, port, n, b, d):
+    """Forced threshold consult (the path of a float threshold within rounding of an F_j):
+    the host service thread answers the candidates' glibc u and thresholds, the device
+    recounts and decides - results unchanged, no host-finished allocation."""
+    from paper_2602_08923_b200._lib import check, lib
+    ws = _workers(port, n, d, seed=31 + n)
+    want = port.run_round(ws, port.round_cfg(n, b, "ring", seed=1))
+    cfg = _cfg(dq, n, b)
+    ctx = dq.Context(cfg)
+    check(lib().dq_debug_force_host_alloc(2))
+    try:
+        got = dq.run_round([torch.from_numpy(w).cuda() for w in ws], cfg, ctx=ctx, with_allocation=True)
+    finally:
+        check(lib().dq_debug_force_host_alloc(0))
+    _check(dq, got, want)
+    h = ctx.host_allocations()
+    assert h["finished"] == 0 and h["consulted"] >= 1, h
+    ctx.close()
+
+
+@pytest.mark.parametrize("n,d", [(2, 1 << 26), (2, 1 << 28), (4, 1 << 26)])
+def test_large_rounds_decided_on_device(dq, n, d):
+    """Bench-sized heavy-tailed gradients (dense F: adjacent-float F_j around the plateau
+    are common) - every asynchronous round decided on the device (at most a threshold
+    consult), bit-identical to the host-synchronous allocation path."""
+    import os
+    import bench
+    cfg = _cfg(dq, n, 4.0)
+    xs = bench.synth(torch, d, n, 4.0, seed=7)
+    ctx = dq.Context(cfg)
+    os.environ["DQ_SYNC_ALLOC"] = "1"
+    try:
+        ref_ctx = dq.Context(cfg)
+    finally:
+        del os.environ["DQ_SYNC_ALLOC"]
+    for rnd in range(3):
+        cfg.seed = dq.SharedSeed(1, rnd)
+        ctx.set_config(cfg)
+        ref_ctx.set_config(cfg)
+        a = dq.run_round(xs, cfg, ctx=ctx, metrics=False).synced
+        info = ctx.wait()
+        r = dq.run_round(xs, cfg, ctx=ref_ctx, with_allocation=True)
+        assert torch.equal(a.view(torch.int32), r.synced.view(torch.int32)), rnd
+        assert info["u"] == r.u and info["payload_bits"] == r.payload_bits
+    h = ctx.host_allocations()
+    assert h["finished"] == 0, h
+    print("host consults", h)
+    ctx.close()
+    ref_ctx.close()

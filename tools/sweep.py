@@ -39,7 +39,7 @@ def timed(fn, steps, st):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--sizes", default="18:30")
+    ap.add_argument("--sizes", default="18:30", help="lo:hi[:step] exponents of d")
     ap.add_argument("--budgets", default="4")
     ap.add_argument("--topology", default="ring")
     ap.add_argument("--steps", type=int, default=10)
@@ -50,7 +50,8 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    lo, hi = (int(x) for x in args.sizes.split(":"))
+    parts = [int(x) for x in args.sizes.split(":")]
+    lo, hi, step = parts[0], parts[1], parts[2] if len(parts) > 2 else 1
     st = torch.cuda.current_stream()
     for topo in args.topology.split(","):
         if topo == "butterfly" and world & (world - 1):
@@ -59,7 +60,7 @@ def main():
             cfg = dq.PipelineConfig(n_workers=world, budget_bits=b, seed=dq.SharedSeed(1, 0),
                                     topology=dq.BUTTERFLY if topo == "butterfly" else dq.RING)
             comm = dq.Communicator(cfg, rank, world, transport=args.transport)
-            for e in range(lo, hi + 1):
+            for e in range(lo, hi + 1, step):
                 d = 1 << e
                 g = torch.Generator(device="cuda").manual_seed(1)
                 T = (d + 255) // 256
