@@ -119,7 +119,7 @@ def test_round_captured_in_cuda_graph(dq, port):
     ctx.close()
 
 
-@pytest.mark.parametrize("n,b,d", [(4, 4.0, 1 << 16), (2, 3.0, (1 << 20) + 256), (8, 4.0, 1 << 15)])
+@pytest.mark.parametrize("n,b,d", [(4, 4.0, 1 << 21), (2, 3.0, (1 << 20) + 256), (8, 4.0, (1 << 20) + 4096 * 3)])
 def test_threshold_consult(dq, port, n, b, d):
     """Forced threshold consult (the path of a float threshold within rounding of an F_j):
     the host service thread answers the candidates' glibc u and thresholds, the device
