@@ -774,16 +774,8 @@ __global__ void __launch_bounds__(kAllocBins) k_alloc_coop(const float* __restri
 
 void set_force_host_alloc(int on) { cudaMemcpyToSymbol(g_force_host_alloc, &on, sizeof on); }
 
-// ---------------------------------------------- small T: search + assignment in one block
-// The latency path of small all-reduces (T <= 4096 super-groups, d <= 1M entries): the
-// reference's allocate_fast restated literally in one CTA - every flip 4 - a log2 F_j and
-// 8 - a log2 F_j (device libm) radix-sorted in shared memory (CUB), de-duplicated, the
-// plateau samples between them bisected exactly as allocation.cpp:228-255 does with the
-// float-threshold payload of each probe, every probe's thresholds certified (as in
-// alloc_candidates) - then widths, the stable 8/4/2 partition and the permuted means.  One
-// launch instead of the cooperative search's passes and grid syncs plus three assignment
-// kernels.  Uncertified probes hand the round to the host exactly like the search does.
 constexpr int kSmallThreads = 512;
+constexpr int kSmallWarps = kSmallThreads / 32;
 __device__ __forceinline__ double key_double(uint64_t k) {  // inverse of dkey
   const uint64_t b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
   return __longlong_as_double(static_cast<long long>(b));
@@ -795,90 +787,214 @@ __device__ __forceinline__ float ambiguous_float(double d) {
   if (__float_as_uint(lo) == __float_as_uint(hi)) return -1.0f;
   return nextafterf(lo, INFINITY) == hi && lo > 0.0f ? lo : __int_as_float(0x7fc00000);
 }
-__device__ __forceinline__ unsigned long long small_block_sum(unsigned long long v, unsigned long long* red) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  unsigned long long t = 0;
-  for (int k = 0; k < kSmallThreads / 32; ++k) t += red[k];
-  return t;
+
+// Shared memory of the one-CTA allocation (N = kSmallThreads * IPT >= T super-groups):
+//   Fs[N]   F in original order (the assignment reads it here)
+//   SF[N]   the positive F sorted descending (the probes count F_j >= t by binary search)
+//   L[N]    alpha log2 F of the super-groups sorted by F descending (flip order), J[N] their index
+//   UK[2N]  the merged flips as order-preserving keys, then the unique flips; UV[2N] = j | type << 31
+// The CUB sort's temporary storage aliases UK (written only after the sort; the region is
+// widened when the sort needs more).
+template <int IPT>
+struct SmallSmem {
+  static constexpr int N = kSmallThreads * IPT;
+  using Sort = cub::BlockRadixSort<uint32_t, kSmallThreads, IPT, uint32_t>;
+  static constexpr size_t kSortB = sizeof(typename Sort::TempStorage);
+  static constexpr size_t kF = 0, kSF = kF + 4ull * N, kL = kSF + 4ull * N, kJ = kL + 8ull * N, kUK = kJ + 4ull * N;
+  static constexpr size_t kUV = kUK + ((16ull * N > kSortB ? 16ull * N : kSortB) + 15) / 16 * 16;
+  static constexpr size_t bytes = kUV + 8ull * N;
+};
+
+// #{F_j >= t} from the positive F sorted descending (SF[0, np)) and the count of F_j >= 0
+__device__ __forceinline__ uint32_t small_count_ge(const float* SF, uint32_t np, uint32_t nonneg, float t) {
+  if (!(t > 0.0f)) return nonneg;  // t = 0: every F_j >= 0 (t is never negative or NaN)
+  uint32_t lo = 0, hi = np;        // first p with SF[p] < t
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (SF[mid] < t) hi = mid;
+    else lo = mid + 1;
+  }
+  return lo;
+}
+// Probe of the bisection (allocation.cpp:237: payload with the float thresholds of sample u
+// <= budget): bit 0 fits, bit 1 certified (thresholds stable, or ambiguous with no F_j
+// equal to the lower float).  payload = S (2 T + 2 #{F >= t24} + 4 #{F >= t48}), t48 >= t24.
+__device__ __forceinline__ uint32_t small_probe(double u, const float* SF, uint32_t np, uint32_t nonneg, uint32_t T,
+                                                double alpha, double budget, uint32_t S) {
+  const double d24 = exp2(__ddiv_rn(__dsub_rn(4.0, u), alpha)), d48 = exp2(__ddiv_rn(__dsub_rn(8.0, u), alpha));
+  const float t24 = static_cast<float>(d24), t48 = static_cast<float>(d48);
+  const float a24 = ambiguous_float(d24), a48 = ambiguous_float(d48);
+  const unsigned long long units = 2ull * T + 2ull * small_count_ge(SF, np, nonneg, t24) +
+                                   4ull * small_count_ge(SF, np, nonneg, t48);
+  // some F_j == a (a > 0): the first p with SF[p] < a is past an element equal to a
+  auto hit = [&](float a) {
+    if (!(a > 0.0f)) return false;
+    const uint32_t c = small_count_ge(SF, np, nonneg, a);
+    return c > 0 && SF[c - 1] == a;
+  };
+  const bool cert = !(a24 != a24) && !(a48 != a48) && !hit(a24) && !hit(a48);
+  const bool fits = static_cast<double>(units * S) <= budget;
+  return (fits ? 1u : 0u) | (cert ? 2u : 0u);
 }
 
+// ---------------------------------------------- small T: search + assignment in one block
+// The latency path of small all-reduces (T <= 4096 super-groups, d <= 1M entries): the
+// reference's allocate_fast (allocation.cpp:195-260) restated literally in one CTA.
+// * Flip order without a 64-bit sort: both flip families 4 - a log2 F_j and 8 - a log2 F_j
+//   are decreasing in F_j, so one stable radix sort of the T float bit patterns (CUB,
+//   descending F) orders both; a merge-path merge of the two families (ties broken by
+//   super-group then family, the stable order of the flat sort) gives the sorted flips,
+//   de-duplicated like std::unique on the doubles.
+// * The bisection (allocation.cpp:237-255) evaluated 3-4 levels at a time: every warp
+//   evaluates one node of the next levels of the bisection tree from the current (lo, hi)
+//   (speculative probes, one warp each, F staged in shared memory), then thread 0 follows
+//   the path the sequential bisection takes - same probes, same result, and the
+//   certification counts only the probes on that path.
+// * widths, the stable 8/4/2 partition and the permuted means, as build_permutation.
+// One launch instead of the cooperative search's passes and grid syncs plus three
+// assignment kernels.  Uncertified probes hand the round to the host (need_host).
 template <int IPT>
 __global__ void __launch_bounds__(kSmallThreads) k_alloc_small(const float* __restrict__ F, uint32_t T, double alpha,
                                                                double budget, uint32_t S, AllocWork w,
                                                                uint8_t* widths, uint32_t* perm) {
-  constexpr int N = kSmallThreads * IPT;  // >= 2T flips
-  using Sort = cub::BlockRadixSort<uint64_t, kSmallThreads, IPT, uint32_t>;
+  using SM = SmallSmem<IPT>;
+  constexpr int N = SM::N;
   extern __shared__ __align__(16) uint8_t smem[];
-  auto& sort_tmp = *reinterpret_cast<typename Sort::TempStorage*>(smem);
-  uint64_t* K = reinterpret_cast<uint64_t*>(smem);           // sorted keys   [N] (after the sort)
-  uint32_t* V = reinterpret_cast<uint32_t*>(K + N);          // sorted values [N]
-  uint64_t* UK = reinterpret_cast<uint64_t*>(V + N);         // unique flips  [N]
-  uint32_t* UV = reinterpret_cast<uint32_t*>(UK + N);        // their super-group | type << 31
-  __shared__ unsigned long long red[kSmallThreads / 32];
-  __shared__ uint32_t m_sh;
-  __shared__ float thr_sh[4];
-  __shared__ int ok_sh, lo_sh, hi_sh, cert_sh;
+  float* Fs = reinterpret_cast<float*>(smem + SM::kF);
+  float* SF = reinterpret_cast<float*>(smem + SM::kSF);
+  double* L = reinterpret_cast<double*>(smem + SM::kL);
+  uint32_t* J = reinterpret_cast<uint32_t*>(smem + SM::kJ);
+  uint64_t* UK = reinterpret_cast<uint64_t*>(smem + SM::kUK);
+  uint32_t* UV = reinterpret_cast<uint32_t*>(smem + SM::kUV);
+  auto& sort_tmp = *reinterpret_cast<typename SM::Sort::TempStorage*>(smem + SM::kUK);
+  __shared__ unsigned long long red[kSmallWarps];
+  __shared__ uint32_t node_res[kSmallWarps];
+  __shared__ uint32_t m_sh, npos_sh, nonneg_sh;
+  __shared__ int ok_sh, lo_sh, hi_sh, cert_sh, feas_sh, done_sh;
   AllocState* st = w.state;
-  const int t = threadIdx.x;
-  // flips (blocked arrangement: item i of thread t is flip t * IPT + i = super-group >> 1, type & 1)
-  uint64_t key[IPT];
-  uint32_t val[IPT];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+#if defined(DQ_SMALL_PHASES)
+  uint64_t ph[8];
+  int nph = 0;
+#define DQ_PHASE() do { __syncthreads(); if (t == 0) ph[nph++] = dq_globaltimer(); } while (0)
+#else
+#define DQ_PHASE() do { } while (0)
+#endif
+  DQ_PHASE();
+  // stage F; sort keys ~bits (ascending = F descending) of the positive F_j, stable in j
+  uint32_t key[IPT], val[IPT];
+  uint32_t npos = 0, nonneg = 0;
 #pragma unroll
   for (int i = 0; i < IPT; ++i) {
-    const uint32_t idx = static_cast<uint32_t>(t * IPT + i), j = idx >> 1, type = idx & 1;
-    key[i] = ~0ull;
-    val[i] = j | type << 31;
-    if (j < T) {
-      const float f = F[j];
-      if (f > 0.0f) key[i] = dkey(__dsub_rn(type ? 8.0 : 4.0, __dmul_rn(alpha, log2(static_cast<double>(f)))));
-    }
+    const uint32_t j = static_cast<uint32_t>(t * IPT + i);
+    const float f = j < T ? F[j] : -1.0f;
+    if (j < T) Fs[j] = f;
+    const bool pos = f > 0.0f;
+    key[i] = pos ? ~__float_as_uint(f) : 0xffffffffu;
+    val[i] = j;
+    npos += pos;
+    nonneg += f >= 0.0f;
   }
-  Sort(sort_tmp).Sort(key, val);
+  {
+    unsigned long long c = static_cast<unsigned long long>(npos) | static_cast<unsigned long long>(nonneg) << 32;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) red[warp] = c;
+  }
   __syncthreads();
-#pragma unroll
-  for (int i = 0; i < IPT; ++i) {
-    K[t * IPT + i] = key[i];
-    V[t * IPT + i] = val[i];
-  }
-  __syncthreads();
-  // unique flips (std::unique on the sorted doubles), compacted in order
-  uint32_t cnt = 0;
-#pragma unroll
-  for (int i = 0; i < IPT; ++i) {
-    const int idx = t * IPT + i;
-    cnt += key[i] != ~0ull && (idx == 0 || K[idx - 1] != key[i]);
-  }
-  unsigned long long incl = cnt;
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned long long u = __shfl_up_sync(0xffffffffu, incl, o);
-    if ((t & 31) >= o) incl += u;
-  }
-  if ((t & 31) == 31) red[t >> 5] = incl;
-  __syncthreads();
-  unsigned long long off = 0, all = 0;
-  for (int k = 0; k < kSmallThreads / 32; ++k) {
-    if (k < (t >> 5)) off += red[k];
-    all += red[k];
-  }
-  uint32_t pos = static_cast<uint32_t>(off + incl - cnt);
-#pragma unroll
-  for (int i = 0; i < IPT; ++i) {
-    const int idx = t * IPT + i;
-    if (key[i] != ~0ull && (idx == 0 || K[idx - 1] != key[i])) {
-      UK[pos] = key[i];
-      UV[pos] = val[i];
-      ++pos;
-    }
-  }
   if (t == 0) {
-    m_sh = static_cast<uint32_t>(all);
-    cert_sh = 1;
+    unsigned long long c = 0;
+    for (int k = 0; k < kSmallWarps; ++k) c += red[k];
+    npos_sh = static_cast<uint32_t>(c);
+    nonneg_sh = static_cast<uint32_t>(c >> 32);
+  }
+  DQ_PHASE();
+  typename SM::Sort(sort_tmp).SortBlockedToStriped(key, val);  // item i of thread t: position t + 512 i
+  __syncthreads();
+  DQ_PHASE();
+  const uint32_t np = npos_sh, nonneg_all = nonneg_sh;  // sorted positions [0, np): the positive F_j
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const uint32_t p = static_cast<uint32_t>(t + kSmallThreads * i);
+    if (p < np) {
+      const float f = __uint_as_float(~key[i]);
+      SF[p] = f;
+      L[p] = __dmul_rn(alpha, log2(static_cast<double>(f)));
+      J[p] = val[i];
+    }
   }
   __syncthreads();
+  // merge A_p = 4 - L[p] (family 0) and B_q = 8 - L[q] (family 1), both ascending in p, by
+  // ranks: A_p lands at p + #{B before A_p}, B_q at q + #{A before B_q} (one binary search
+  // each; position-striped so the shared-memory reads of a warp are consecutive)
+  const uint32_t M = 2 * np;
+  auto a_val = [&](uint32_t p) { return __dsub_rn(4.0, L[p]); };
+  auto b_val = [&](uint32_t q) { return __dsub_rn(8.0, L[q]); };
+  // A_p before B_q in the flat stable order (value, then super-group, family 0 first)
+  auto a_first = [&](uint32_t p, uint32_t q) {
+    const double x = a_val(p), y = b_val(q);
+    return x < y || (x == y && J[p] <= J[q]);
+  };
+  for (uint32_t p = t; p < np; p += kSmallThreads) {
+    uint32_t lo = 0, hi = np;  // first q with A_p before B_q
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (a_first(p, mid)) hi = mid;
+      else lo = mid + 1;
+    }
+    UK[p + lo] = dkey(a_val(p));
+    UV[p + lo] = J[p];
+    lo = 0;
+    hi = np;  // first p' with B_p not after A_p'
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (a_first(mid, p)) lo = mid + 1;
+      else hi = mid;
+    }
+    UK[p + lo] = dkey(b_val(p));
+    UV[p + lo] = J[p] | 0x80000000u;
+  }
+  __syncthreads();
+  // std::unique on the merged flips, compacted in place: warp w owns a segment of `seg`
+  // positions, lane l its positions seg w + 32 k + l (held in registers across the barrier)
+  {
+    constexpr int K = 2 * IPT;  // seg / 32 <= 2 N / (16 * 32)
+    const uint32_t seg = ((M + kSmallWarps - 1) / kSmallWarps + 31) / 32 * 32;
+    const uint32_t s0 = warp * seg;
+    uint64_t k_[K];
+    uint32_t v_[K], keep[K];
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const uint32_t r = s0 + 32u * i + lane;
+      const bool in = r < M && 32u * i < seg;
+      k_[i] = in ? UK[r] : 0;
+      v_[i] = in ? UV[r] : 0;
+      const bool kp = in && (r == 0 || k_[i] != UK[r - 1]);
+      keep[i] = __ballot_sync(0xffffffffu, kp);
+      cnt += __popc(keep[i]);
+    }
+    if (lane == 0) red[warp] = cnt;
+    __syncthreads();  // every segment is in registers before the compaction overwrites UK
+    uint32_t off = 0, all = 0;
+    for (int k = 0; k < kSmallWarps; ++k) {
+      if (k < warp) off += static_cast<uint32_t>(red[k]);
+      all += static_cast<uint32_t>(red[k]);
+    }
+    const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      if (keep[i] & (1u << lane)) {
+        const uint32_t pos = off + __popc(keep[i] & lt);
+        UK[pos] = k_[i];
+        UV[pos] = v_[i];
+      }
+      off += __popc(keep[i]);
+    }
+    if (t == 0) m_sh = all;
+  }
+  __syncthreads();
+  DQ_PHASE();
   const uint32_t m = m_sh;
   const uint32_t ns = m ? m + 1 : 1;  // samples (fast_sample_points)
   auto sample = [&](uint32_t i) {
@@ -889,54 +1005,99 @@ __global__ void __launch_bounds__(kSmallThreads) k_alloc_small(const float* __re
     else u = __dmul_rn(0.5, __dadd_rn(key_double(UK[i - 1]), key_double(UK[i])));
     return u < -1e6 ? -1e6 : (u > 1e6 ? 1e6 : u);
   };
-  // payload(u) <= budget with the float thresholds (allocation.cpp:173-189,237), certified
-  auto fits = [&](uint32_t i) {
-    if (t == 0) {
-      const double u = sample(i);
-      const double d24 = exp2(__ddiv_rn(__dsub_rn(4.0, u), alpha)), d48 = exp2(__ddiv_rn(__dsub_rn(8.0, u), alpha));
-      thr_sh[0] = static_cast<float>(d24);
-      thr_sh[1] = static_cast<float>(d48);
-      thr_sh[2] = ambiguous_float(d24);
-      thr_sh[3] = ambiguous_float(d48);
-      if (thr_sh[2] != thr_sh[2] || thr_sh[3] != thr_sh[3]) cert_sh = 0;
+  // Bisection tree node k (breadth-first, k = 0 the next probe) below the interval
+  // (lo, hi): descend by the bits of k + 1 (1 = the probe fitted: lo = mid).  Returns the
+  // node's probe index, or -1 where the sequential loop would already have stopped.
+  auto node_mid = [](int lo, int hi, int k) {
+    int level = 31 - __clz(k + 1);
+    for (int l = level - 1; l >= 0; --l) {
+      if (lo + 1 >= hi) return -1;
+      const int mid = (lo + hi) / 2;
+      if (((k + 1) >> l) & 1) lo = mid;
+      else hi = mid;
     }
-    __syncthreads();
-    const float t24 = thr_sh[0], t48 = thr_sh[1], a24 = thr_sh[2], a48 = thr_sh[3];
-    unsigned long long wsum = 0;  // payload units (< 2^32) + 2^32 x (F_j equal to an ambiguous float)
-    for (uint32_t j = t; j < T; j += kSmallThreads) {
-      const float f = F[j];
-      wsum += f >= t48 ? 8 : (f >= t24 ? 4 : 2);
-      wsum += static_cast<unsigned long long>(f == a24 || f == a48) << 32;
-    }
-    const unsigned long long tot = small_block_sum(wsum, red);
-    if (t == 0 && (tot >> 32)) cert_sh = 0;
-    return static_cast<double>((tot & 0xffffffffull) * S) <= budget;
+    return lo + 1 >= hi ? -1 : (lo + hi) / 2;
   };
-  if (t == 0) {
-    lo_sh = 0;
-    hi_sh = static_cast<int>(ns - 1);
+  // round 0: fits(0), fits(ns - 1) and the first 3 tree levels below (0, ns - 1)
+  {
+    int probe = -1;
+    if (warp == 0) probe = 0;
+    else if (warp == 1) probe = ns > 1 ? static_cast<int>(ns - 1) : -1;
+    else if (warp < 9) probe = node_mid(0, static_cast<int>(ns - 1), warp - 2);
+    if (probe >= 0) {
+      if (lane == 0)
+        node_res[warp] = small_probe(sample(static_cast<uint32_t>(probe)), SF, np, nonneg_all, T, alpha, budget, S) | 4u;
+    } else if (lane == 0) {
+      node_res[warp] = 0;
+    }
   }
   __syncthreads();
-  bool feasible = fits(0);
-  if (feasible) {
-    if (fits(ns - 1)) {
-      if (t == 0) lo_sh = static_cast<int>(ns - 1);
-      __syncthreads();
+  if (t == 0) {
+    int lo = 0, hi = static_cast<int>(ns - 1), cert = 1, done = 0;
+    const uint32_t r0 = node_res[0];
+    cert &= (r0 >> 1) & 1;
+    const int feasible = r0 & 1;
+    if (!feasible) {
+      done = 1;
+    } else if (ns == 1) {
+      done = 1;  // the single sample fits (lo = 0)
     } else {
-      for (;;) {
-        const int lo = lo_sh, hi = hi_sh;
-        if (lo + 1 >= hi) break;
-        const int mid = (lo + hi) / 2;
-        const bool ok = fits(static_cast<uint32_t>(mid));
-        if (t == 0) {
-          if (ok) lo_sh = mid;
-          else hi_sh = mid;
+      const uint32_t r1 = node_res[1];
+      cert &= (r1 >> 1) & 1;
+      if (r1 & 1) {
+        lo = hi;
+        done = 1;
+      } else {
+        int k = 0;
+        for (int l = 0; l < 3; ++l) {
+          if (lo + 1 >= hi) break;
+          const uint32_t r = node_res[2 + k];
+          cert &= (r >> 1) & 1;
+          const int mid = (lo + hi) / 2;
+          if (r & 1) lo = mid;
+          else hi = mid;
+          k = 2 * k + 1 + static_cast<int>(r & 1);
         }
-        __syncthreads();
+        done = lo + 1 >= hi;
       }
     }
+    lo_sh = lo;
+    hi_sh = hi;
+    cert_sh = cert;
+    feas_sh = feasible;
+    done_sh = done;
   }
+  __syncthreads();
+  // later rounds: 4 tree levels (15 nodes) per round
+  while (!done_sh) {
+    const int lo0 = lo_sh, hi0 = hi_sh;
+    if (warp < 15) {
+      const int probe = node_mid(lo0, hi0, warp);
+      if (probe >= 0 && lane == 0)
+        node_res[warp] = small_probe(sample(static_cast<uint32_t>(probe)), SF, np, nonneg_all, T, alpha, budget, S) | 4u;
+    }
+    __syncthreads();
+    if (t == 0) {
+      int lo = lo0, hi = hi0, cert = cert_sh, k = 0;
+      for (int l = 0; l < 4; ++l) {
+        if (lo + 1 >= hi) break;
+        const uint32_t r = node_res[k];
+        cert &= (r >> 1) & 1;
+        const int mid = (lo + hi) / 2;
+        if (r & 1) lo = mid;
+        else hi = mid;
+        k = 2 * k + 1 + static_cast<int>(r & 1);
+      }
+      lo_sh = lo;
+      hi_sh = hi;
+      cert_sh = cert;
+      done_sh = lo + 1 >= hi;
+    }
+    __syncthreads();
+  }
+  DQ_PHASE();
   const uint32_t lo = static_cast<uint32_t>(lo_sh);
+  const bool feasible = feas_sh != 0;
   // final thresholds (certified) + the state the host reads (u via host_u_of, mailbox)
   if (t == 0) {
     const double u = sample(lo);
@@ -947,7 +1108,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_alloc_small(const float* __re
     auto rec = [&](uint32_t i) {
       FlipRec r{};
       r.key = UK[i];
-      r.fbits = __float_as_uint(F[UV[i] & 0x7fffffffu]);
+      r.fbits = __float_as_uint(Fs[UV[i] & 0x7fffffffu]);
       r.type = UV[i] >> 31;
       r.present = 1;
       return r;
@@ -966,7 +1127,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_alloc_small(const float* __re
     st->u = u;
     st->t24 = static_cast<float>(d24);
     st->t48 = static_cast<float>(d48);
-    st->certified = cert_sh ? 1u : 0u;  // every probe (the final one included) certified
+    st->certified = cert_sh ? 1u : 0u;  // every probe on the bisection's path certified
     st->need_host = (!st->certified || !feasible || g_force_host_alloc == 1) ? 1u : 0u;
     st->T = T;
     st->S = S;
@@ -975,67 +1136,80 @@ __global__ void __launch_bounds__(kSmallThreads) k_alloc_small(const float* __re
     ok_sh = static_cast<int>(st->need_host);
   }
   __syncthreads();
-  if (ok_sh) {  // hand the round to the host: export F, mirror, request, wait for the answer
-    for (uint32_t j = t; j < T; j += kSmallThreads) w.hF[j] = F[j];
+  const bool need_host = ok_sh != 0;
+  if (need_host) {  // hand the round to the host: export F, mirror, request, wait for the answer
+    for (uint32_t j = t; j < T; j += kSmallThreads) w.hF[j] = Fs[j];
   }
-  __syncthreads();
   {
     const uint32_t* src = reinterpret_cast<const uint32_t*>(st);
     uint32_t* dst = reinterpret_cast<uint32_t*>(&w.hmsg->state);
     for (uint32_t k = t; k < sizeof(AllocState) / 4; k += kSmallThreads) dst[k] = src[k];
   }
-  __threadfence_system();
-  __syncthreads();
-  if (t == 0 && ok_sh) {
-    w.hmsg->request = st->epoch;
+  if (need_host) {  // (the common round's mirror is read after the round completes: no fence)
     __threadfence_system();
-    const uint64_t t0 = dq_globaltimer();
-    for (;;) {
-      uint32_t v;
-      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(&w.hmsg->resolved) : "memory");
-      if (v == st->epoch) break;
-      __nanosleep(1000);
-      if (dq_globaltimer() - t0 > g_spin_ns) __trap();
+    __syncthreads();
+    if (t == 0) {
+      w.hmsg->request = st->epoch;
+      __threadfence_system();
+      const uint64_t t0 = dq_globaltimer();
+      for (;;) {
+        uint32_t v;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(&w.hmsg->resolved) : "memory");
+        if (v == st->epoch) break;
+        __nanosleep(1000);
+        if (dq_globaltimer() - t0 > g_spin_ns) __trap();
+      }
+      st->t24 = *reinterpret_cast<volatile float*>(&w.hmsg->t24);
+      st->t48 = *reinterpret_cast<volatile float*>(&w.hmsg->t48);
     }
-    st->t24 = *reinterpret_cast<volatile float*>(&w.hmsg->t24);
-    st->t48 = *reinterpret_cast<volatile float*>(&w.hmsg->t48);
   }
   __syncthreads();
+  DQ_PHASE();
   const float t24 = st->t24, t48 = st->t48;
-  // widths + stable partition 8 | 4 | 2 (build_permutation, allocation.cpp:302-310): thread t
-  // owns the contiguous super-groups [t * per, (t + 1) * per)
-  const uint32_t per = (T + kSmallThreads - 1) / kSmallThreads;
-  const uint32_t j0 = t * per, j1 = j0 + per < T ? j0 + per : T;
-  unsigned long long packed = 0;  // 21-bit class counts
-  for (uint32_t j = j0; j < j1; ++j) {
-    const float fj = F[j];
-    const int c = fj >= t48 ? 0 : (fj >= t24 ? 1 : 2);
-    widths[j] = static_cast<uint8_t>(c == 0 ? 8 : (c == 1 ? 4 : 2));
-    packed += 1ull << (21 * c);
-  }
-  unsigned long long sc = packed;
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned long long u = __shfl_up_sync(0xffffffffu, sc, o);
-    if ((t & 31) >= o) sc += u;
+  // widths + stable partition 8 | 4 | 2 (build_permutation, allocation.cpp:302-310):
+  // super-group j = 512 k + t (position-striped), class ballots per (k, warp), then each
+  // element's place = class base + the class count of every (k', warp') before it + its
+  // rank in the ballot
+  __shared__ uint32_t ccnt[IPT][kSmallWarps];
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t bal[IPT][3];
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    const uint32_t j = static_cast<uint32_t>(k * kSmallThreads + t);
+    int c = 3;
+    if (j < T) {
+      const float fj = Fs[j];
+      c = fj >= t48 ? 0 : (fj >= t24 ? 1 : 2);
+      widths[j] = static_cast<uint8_t>(c == 0 ? 8 : (c == 1 ? 4 : 2));
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) bal[k][q] = __ballot_sync(0xffffffffu, c == q);
+    if (lane == 0) ccnt[k][warp] = __popc(bal[k][0]) | __popc(bal[k][1]) << 8 | __popc(bal[k][2]) << 16;
   }
   __syncthreads();
-  if ((t & 31) == 31) red[t >> 5] = sc;
-  __syncthreads();
-  unsigned long long base = 0, tot = 0;
-  for (int k = 0; k < kSmallThreads / 32; ++k) {
-    if (k < (t >> 5)) base += red[k];
-    tot += red[k];
+  unsigned long long acc = 0, pre[IPT];  // 16-bit class counts (T <= 4096)
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    pre[k] = 0;
+    for (int v = 0; v < kSmallWarps; ++v) {
+      if (v == warp) pre[k] = acc;
+      const uint32_t e = ccnt[k][v];
+      acc += (e & 0xffu) | static_cast<unsigned long long>((e >> 8) & 0xffu) << 16 |
+             static_cast<unsigned long long>((e >> 16) & 0xffu) << 32;
+    }
   }
-  const unsigned long long excl = base + sc - packed;
-  const uint32_t n8 = static_cast<uint32_t>(tot & 0x1fffff), n4 = static_cast<uint32_t>((tot >> 21) & 0x1fffff);
-  uint32_t p[3] = {static_cast<uint32_t>(excl & 0x1fffff), n8 + static_cast<uint32_t>((excl >> 21) & 0x1fffff),
-                   n8 + n4 + static_cast<uint32_t>((excl >> 42) & 0x1fffff)};
-  for (uint32_t j = j0; j < j1; ++j) {
-    const float fj = F[j];
-    const int c = fj >= t48 ? 0 : (fj >= t24 ? 1 : 2);
-    const uint32_t at = p[c]++;
-    perm[at] = j;
-    if (w.pmean) w.pmean[at] = w.gmean[j];
+  const uint32_t n8 = static_cast<uint32_t>(acc & 0xffffu), n4 = static_cast<uint32_t>((acc >> 16) & 0xffffu);
+  const uint32_t cbase[3] = {0, n8, n8 + n4};
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    const uint32_t j = static_cast<uint32_t>(k * kSmallThreads + t);
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+      if (bal[k][q] & (1u << lane)) {
+        const uint32_t at = cbase[q] + static_cast<uint32_t>((pre[k] >> (16 * q)) & 0xffffu) + __popc(bal[k][q] & lt);
+        perm[at] = j;
+        if (w.pmean) w.pmean[at] = w.gmean[j];
+      }
   }
   if (t == 0) {
     w.counts[0] = n8;
@@ -1044,8 +1218,14 @@ __global__ void __launch_bounds__(kSmallThreads) k_alloc_small(const float* __re
     w.hmsg->counts[0] = n8;
     w.hmsg->counts[1] = n4;
     w.hmsg->counts[2] = T - n8 - n4;
-    __threadfence_system();
   }
+  DQ_PHASE();
+#if defined(DQ_SMALL_PHASES)
+  if (t == 0)
+    printf("k_alloc_small T=%u m=%u phases(ns): stage %llu sort %llu merge+unique %llu bisect %llu mirror %llu assign %llu\n",
+           T, m, ph[1] - ph[0], ph[2] - ph[1], ph[3] - ph[2], ph[4] - ph[3], ph[5] - ph[4], ph[6] - ph[5]);
+#endif
+#undef DQ_PHASE
 }
 
 bool launch_alloc_small(const float* F, uint32_t T, double alpha, double budget, uint32_t S, AllocWork w,
@@ -1053,15 +1233,20 @@ bool launch_alloc_small(const float* F, uint32_t T, double alpha, double budget,
   if (!w.hmsg || T == 0 || T > 4096) return false;
   auto go = [&](auto ipt) {
     constexpr int IPT = decltype(ipt)::value;
-    constexpr size_t N = static_cast<size_t>(kSmallThreads) * IPT;
-    using Sort = cub::BlockRadixSort<uint64_t, kSmallThreads, IPT, uint32_t>;
-    const size_t bytes = std::max(sizeof(typename Sort::TempStorage), N * 12) + N * 12;
-    cudaFuncSetAttribute(k_alloc_small<IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+    constexpr size_t bytes = SmallSmem<IPT>::bytes;
+    static bool attr[kMaxDevices] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!attr[dev]) {
+      cudaFuncSetAttribute(k_alloc_small<IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+      attr[dev] = true;
+    }
     k_alloc_small<IPT><<<1, kSmallThreads, bytes, st>>>(F, T, alpha, budget, S, w, widths, perm);
   };
-  if (2 * T <= kSmallThreads * 4) go(std::integral_constant<int, 4>{});
-  else if (2 * T <= kSmallThreads * 8) go(std::integral_constant<int, 8>{});
-  else go(std::integral_constant<int, 16>{});
+  if (T <= kSmallThreads) go(std::integral_constant<int, 1>{});
+  else if (T <= kSmallThreads * 2) go(std::integral_constant<int, 2>{});
+  else if (T <= kSmallThreads * 4) go(std::integral_constant<int, 4>{});
+  else go(std::integral_constant<int, 8>{});
   return true;
 }
 
