@@ -97,6 +97,9 @@ typedef struct dq_round_info {
 typedef struct dq_ctx dq_ctx;
 
 int dq_version(void);
+/* Build flags of the loaded library: bit 0 = device-side invariant checks
+ * (DQ_CHECK, -DDQ_DEBUG_CHECKS=1), bit 1 = phase timing (-DDQ_SMALL_PHASES=1). */
+int dq_build_flags(void);
 const char* dq_last_error(void);
 void dq_config_default(dq_config* cfg);
 

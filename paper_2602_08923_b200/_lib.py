@@ -80,6 +80,7 @@ _P, _V, _u8p, _u32p = C.POINTER, C.c_void_p, C.POINTER(C.c_uint8), C.POINTER(C.c
 _fp = C.POINTER(C.c_float)
 SIGNATURES = {
     "dq_version": (C.c_int, []),
+    "dq_build_flags": (C.c_int, []),
     "dq_last_error": (C.c_char_p, []),
     "dq_config_default": (None, [_P(Config)]),
     "dq_ctx_create": (C.c_int, [_P(Config), C.c_int, _P(_V)]),

@@ -2116,6 +2116,16 @@ void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info
 extern "C" {
 
 int dq_version(void) { return DQ_VERSION; }
+int dq_build_flags(void) {
+  int f = 0;
+#if defined(DQ_DEBUG_CHECKS) && DQ_DEBUG_CHECKS
+  f |= 1;
+#endif
+#if defined(DQ_SMALL_PHASES)
+  f |= 2;
+#endif
+  return f;
+}
 const char* dq_last_error(void) { return g_err.c_str(); }
 
 void dq_config_default(dq_config* c) {  // engine.hpp:22-43 defaults

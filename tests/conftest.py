@@ -22,6 +22,18 @@ def pytest_configure(config):
         subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], check=False)
 
 
+def pytest_terminal_summary(terminalreporter):
+    """Which native library the run loaded (DQ_LIB_VARIANT selects a build variant)."""
+    mod = sys.modules.get("paper_2602_08923_b200._lib")
+    if mod is None or getattr(mod, "_lib", None) is None:
+        return
+    try:
+        flags = mod.lib().dq_build_flags()
+        terminalreporter.write_line(f"dynamiq_b200 library: {mod.LIB_PATH} (build flags {flags:#x}; bit 0: device checks)")
+    except Exception:
+        pass
+
+
 @pytest.fixture(scope="session")
 def port():
     from oracle.oracle import Oracle
