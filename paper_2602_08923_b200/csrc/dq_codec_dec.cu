@@ -14,12 +14,12 @@ void launch_peer_dec(const CodecArgs& a, int src, cudaStream_t st) {
   const dim3 grid(persistent_grid(units, 64));
   if constexpr (CORR && NS >= 2) {
     if (a.pc_mode == 4 && src == 0) {  // ring sink reading its permutation slice
-      k_quant_peer<NS, true, 0, true, true, 4><<<grid, kThreads, 0, st>>>(a);
+      launch_pdl(k_quant_peer<NS, true, 0, true, true, 4>, dim3(grid), dim3(kThreads), 0, st, a);
       return;
     }
   }
-  if (src == 0) k_quant_peer<NS, CORR, 0, true, true><<<grid, kThreads, 0, st>>>(a);
-  else k_quant_peer<NS, CORR, 1, true, true><<<grid, kThreads, 0, st>>>(a);
+  if (src == 0) launch_pdl(k_quant_peer<NS, CORR, 0, true, true>, dim3(grid), dim3(kThreads), 0, st, a);
+  else launch_pdl(k_quant_peer<NS, CORR, 1, true, true>, dim3(grid), dim3(kThreads), 0, st, a);
 }
 
 void launch_peer_dec_corr(const CodecArgs& a, int src, cudaStream_t st) {

@@ -10,20 +10,20 @@ void launch_peer_ns(const CodecArgs& a, int src, bool dar, cudaStream_t st) {
   const dim3 grid(persistent_grid(units, 64));  // one unit per warp (not persistent: see per_warp_sgs)
   if constexpr (CORR && NS >= 2) {  // ring permutation slices (leaf writes, later hops read)
     if (a.pc_mode == 3 && src == 0 && !dar) {
-      k_quant_peer<NS, true, 0, false, false, 3><<<grid, kThreads, 0, st>>>(a);
+      launch_pdl(k_quant_peer<NS, true, 0, false, false, 3>, dim3(grid), dim3(kThreads), 0, st, a);
       return;
     }
     if (a.pc_mode == 4 && src == 0 && dar) {
-      k_quant_peer<NS, true, 0, true, false, 4><<<grid, kThreads, 0, st>>>(a);
+      launch_pdl(k_quant_peer<NS, true, 0, true, false, 4>, dim3(grid), dim3(kThreads), 0, st, a);
       return;
     }
   }
   if (src == 0) {
-    if (dar) k_quant_peer<NS, CORR, 0, true><<<grid, kThreads, 0, st>>>(a);
-    else k_quant_peer<NS, CORR, 0, false><<<grid, kThreads, 0, st>>>(a);
+    if (dar) launch_pdl(k_quant_peer<NS, CORR, 0, true>, dim3(grid), dim3(kThreads), 0, st, a);
+    else launch_pdl(k_quant_peer<NS, CORR, 0, false>, dim3(grid), dim3(kThreads), 0, st, a);
   } else {
-    if (dar) k_quant_peer<NS, CORR, 1, true><<<grid, kThreads, 0, st>>>(a);
-    else k_quant_peer<NS, CORR, 1, false><<<grid, kThreads, 0, st>>>(a);
+    if (dar) launch_pdl(k_quant_peer<NS, CORR, 1, true>, dim3(grid), dim3(kThreads), 0, st, a);
+    else launch_pdl(k_quant_peer<NS, CORR, 1, false>, dim3(grid), dim3(kThreads), 0, st, a);
   }
 }
 template <bool CORR>
@@ -46,8 +46,8 @@ void launch_da_peer(const CodecArgs& a, int src, cudaStream_t st) {
   if (a.L.nsg == 0) return;
   const uint32_t units = (a.L.nsg + a.unit - 1) / a.unit;
   const dim3 grid(persistent_grid(units, 64));
-  if (src == 0) k_da_peer<0><<<grid, kThreads, 0, st>>>(a);
-  else k_da_peer<1><<<grid, kThreads, 0, st>>>(a);
+  if (src == 0) launch_pdl(k_da_peer<0>, dim3(grid), dim3(kThreads), 0, st, a);
+  else launch_pdl(k_da_peer<1>, dim3(grid), dim3(kThreads), 0, st, a);
 }
 
 void launch_quant_peer(const CodecArgs& a, int src, bool dar, cudaStream_t st) {

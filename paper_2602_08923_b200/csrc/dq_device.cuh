@@ -10,6 +10,7 @@
 #pragma once
 #include <cstdint>
 #include <cstdio>
+#include <utility>
 #include <cuda_runtime.h>
 
 namespace dq {
@@ -47,6 +48,31 @@ enum Purpose : uint32_t { kEntryQuant = 1, kScaleQuant = 2, kPermutation = 3 };
 // kernel instead of hanging the GPU.  Per device; set from DQ_WAIT_TIMEOUT_S (default
 // 600 s, the scale of PyTorch's NCCL timeout) when the device is first used.
 extern __device__ uint64_t g_spin_ns;
+
+// Programmatic dependent launch (PDL) along a round's kernel chain: each kernel is launched
+// with programmatic stream serialization (launch_pdl), so its CTAs are scheduled and run
+// their independent prologue (shared-memory tables) while the predecessor drains;
+// pdl_wait() (griddepcontrol.wait) blocks until the predecessor grid has completed and its
+// memory is visible - before any read of the predecessor's outputs and any store the
+// predecessor could still observe - and pdl_trigger() then lets the successor launch.
+// Kernels launched without the attribute see both as no-ops.  Env DQ_PDL=0 turns it off.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+bool pdl_enabled();
+template <class... P, class... A>
+inline void launch_pdl(void (*kernel)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...);
+}
 __device__ __forceinline__ uint64_t dq_globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

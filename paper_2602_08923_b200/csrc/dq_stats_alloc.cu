@@ -39,6 +39,8 @@ template <bool PEER>
 __global__ void __launch_bounds__(kStatSG) k_stats(const WorkerPtrs xs, uint64_t d, uint32_t T,
                                                    float* mean, float* sq, StatsPeerArgs sp) {
   __shared__ float tile[kStatSG][33];
+  pdl_wait();
+  pdl_trigger();
   const float* __restrict__ x = xs.p[blockIdx.y];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // PEER: a persistent grid walks the tiles, so the one system-scope fence per block
@@ -111,8 +113,8 @@ WorkerPtrs worker_ptrs(const float* const* host_ptrs, uint32_t n) {
 void launch_stats(const float* const* xs, uint32_t n_workers, uint64_t d, uint32_t T, float* mean,
                   float* sq, cudaStream_t st) {
   if (T == 0) return;
-  k_stats<false><<<dim3((T + kStatSG - 1) / kStatSG, n_workers), kStatSG, 0, st>>>(
-      worker_ptrs(xs, n_workers), d, T, mean, sq, StatsPeerArgs{});
+  launch_pdl(k_stats<false>, dim3((T + kStatSG - 1) / kStatSG, n_workers), dim3(kStatSG), 0, st,
+             worker_ptrs(xs, n_workers), d, T, mean, sq, StatsPeerArgs{});
 }
 
 void launch_stats_peer(const float* const* xs, uint64_t d, uint32_t T, const StatsPeerArgs& sp, cudaStream_t st) {
@@ -127,12 +129,14 @@ void launch_stats_peer(const float* const* xs, uint64_t d, uint32_t T, const Sta
     return (sms > 0 ? sms : 148) * (per_sm > 0 ? per_sm : 4);
   }));
   const uint32_t ntiles = (T + kStatSG - 1) / kStatSG;
-  k_stats<true><<<dim3(ntiles < cap ? ntiles : cap, 1), kStatSG, 0, st>>>(worker_ptrs(xs, 1), d, T, nullptr,
-                                                                          nullptr, sp);
+  launch_pdl(k_stats<true>, dim3(ntiles < cap ? ntiles : cap, 1), dim3(kStatSG), 0, st, worker_ptrs(xs, 1), d, T,
+             static_cast<float*>(nullptr), static_cast<float*>(nullptr), sp);
 }
 
 __global__ void k_reduce_stats(const float* mean, const float* sq, uint32_t n, uint32_t T,
                                float* gm, float* gs) {
+  pdl_wait();
+  pdl_trigger();
   const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= T) return;
   double a = 0.0, b = 0.0;
@@ -147,7 +151,7 @@ __global__ void k_reduce_stats(const float* mean, const float* sq, uint32_t n, u
 void launch_reduce_stats(const float* mean, const float* sq, uint32_t n, uint32_t T, float* gm,
                          float* gs, cudaStream_t st) {
   if (T == 0) return;
-  k_reduce_stats<<<(T + 255) / 256, 256, 0, st>>>(mean, sq, n, T, gm, gs);
+  launch_pdl(k_reduce_stats, dim3((T + 255) / 256), dim3(256), 0, st, mean, sq, n, T, gm, gs);
 }
 
 // The rank-ordered reduction over the fused all-gather's rows: each block first waits
@@ -155,6 +159,8 @@ void launch_reduce_stats(const float* mean, const float* sq, uint32_t n, uint32_
 __global__ void k_reduce_stats_peer(const float* mean, const float* sq, const uint32_t* flags,
                                     const uint32_t* epoch_ptr, uint32_t n, uint32_t T, uint32_t stride, float* gm,
                                     float* gs) {
+  pdl_wait();
+  pdl_trigger();
   if (threadIdx.x == 0) {
     const uint32_t epoch = *epoch_ptr;
     for (uint32_t r = 0; r < n; ++r) {
@@ -185,7 +191,7 @@ __global__ void k_reduce_stats_peer(const float* mean, const float* sq, const ui
 void launch_reduce_stats_peer(const float* mean, const float* sq, const uint32_t* flags, const uint32_t* epoch,
                               uint32_t n, uint32_t T, uint32_t stride, float* gm, float* gs, cudaStream_t st) {
   if (T == 0) return;
-  k_reduce_stats_peer<<<(T + 255) / 256, 256, 0, st>>>(mean, sq, flags, epoch, n, T, stride, gm, gs);
+  launch_pdl(k_reduce_stats_peer, dim3((T + 255) / 256), dim3(256), 0, st, mean, sq, flags, epoch, n, T, stride, gm, gs);
 }
 
 // ------------------------------------------------------------ allocation
@@ -873,6 +879,8 @@ __global__ void __launch_bounds__(kSmallThreads) k_alloc_small(const float* __re
   __shared__ int ok_sh, lo_sh, hi_sh, cert_sh, feas_sh, done_sh;
   AllocState* st = w.state;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  pdl_wait();
+  pdl_trigger();
 #if defined(DQ_SMALL_PHASES)
   uint64_t ph[8];
   int nph = 0;
@@ -1241,7 +1249,7 @@ bool launch_alloc_small(const float* F, uint32_t T, double alpha, double budget,
       cudaFuncSetAttribute(k_alloc_small<IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
       attr[dev] = true;
     }
-    k_alloc_small<IPT><<<1, kSmallThreads, bytes, st>>>(F, T, alpha, budget, S, w, widths, perm);
+    launch_pdl(k_alloc_small<IPT>, dim3(1), dim3(kSmallThreads), bytes, st, F, T, alpha, budget, S, w, widths, perm);
   };
   if (T <= kSmallThreads) go(std::integral_constant<int, 1>{});
   else if (T <= kSmallThreads * 2) go(std::integral_constant<int, 2>{});
