@@ -234,6 +234,8 @@ struct dq_ctx {
   DevBuf<float> accs;     // per-worker chunk accumulators (butterfly)
   DevBuf<uint32_t> pcache; // simulated round: the chunk's permutation slices (slots 1..n-1)
   DevBuf<float> stage;    // host-round staging of inputs / output
+  cudaStream_t gstream = nullptr;      // small peer rounds: the gather decode, launched early
+  cudaEvent_t gfork = nullptr, gjoin = nullptr;
   std::vector<cudaStream_t> cstreams;  // simulated rounds: concurrent chunk chains
   std::vector<cudaEvent_t> cjoin;
   cudaEvent_t cfork = nullptr;
@@ -251,6 +253,7 @@ struct dq_ctx {
   uint32_t apar = 0;
   bool async_alloc = true;   // env DQ_SYNC_ALLOC=1: host-synchronous allocation (round-1 behaviour)
   bool no_small_alloc = false;  // env DQ_NO_SMALL_ALLOC=1: the cooperative search at every T
+  StatsReduce pending_red;      // small rounds: the statistics reduction handed to k_alloc_small
   // what the last round needs to fill dq_round_info once it has completed
   struct RoundRec {
     bool valid = false, async = false;
@@ -306,6 +309,9 @@ struct dq_ctx {
     for (cudaStream_t s2 : cstreams) cudaStreamDestroy(s2);
     for (cudaEvent_t e2 : cjoin) cudaEventDestroy(e2);
     if (cfork) cudaEventDestroy(cfork);
+    if (gstream) cudaStreamDestroy(gstream);
+    if (gfork) cudaEventDestroy(gfork);
+    if (gjoin) cudaEventDestroy(gjoin);
     if (svc.joinable()) {
       svc_stop = true;
       svc.join();
@@ -908,6 +914,8 @@ void ensure_mailbox(dq_ctx* ctx, uint32_t T) {
 // (ctx->counts) for the kernels and are mirrored to the mailbox for dq_round_info.
 AllocResult allocate_fast_async(dq_ctx* ctx, const dq_config& c, const float* dF, uint32_t T, uint8_t* dW,
                                 uint32_t* dP, cudaStream_t st) {
+  const StatsReduce red = ctx->pending_red;  // the round's statistics reduction, not yet launched
+  ctx->pending_red = StatsReduce{};
   AllocResult r;
   r.async = true;
   const uint32_t S = c.super_group_size;
@@ -930,9 +938,16 @@ AllocResult allocate_fast_async(dq_ctx* ctx, const dq_config& c, const float* dF
   DQ_CUDA(cudaHostGetDevicePointer(&dF_host, ctx->hF, 0));
   w.hmsg = static_cast<HostMsg*>(dm);
   w.hF = static_cast<float*>(dF_host);
+  w.red = red;
   if (!ctx->no_small_alloc && launch_alloc_small(dF, T, kAlpha, budget, S, w, dW, dP, st)) {
     DQ_CUDA(cudaGetLastError());
     return r;
+  }
+  if (red.mean) {  // (not reached: the caller folds the reduction only into small rounds)
+    if (red.flags)
+      launch_reduce_stats_peer(red.mean, red.sq, red.flags, red.epoch_ptr, red.n, T, red.stride, red.gm, red.gs, st);
+    else
+      launch_reduce_stats(red.mean, red.sq, red.n, T, red.gm, red.gs, st);
   }
   DQ_CUDA(launch_alloc_search(dF, T, kAlpha, static_cast<uint64_t>(W), budget, S, w, st));
   launch_alloc_assign(dF, T, 0.f, 0.f, true, w, dW, dP, st);
@@ -1036,6 +1051,11 @@ constexpr uint32_t kChunkStreams = 8;  // worker streams of a simulated round's 
 bool async_alloc_ok(const dq_ctx* ctx, bool collect_wire) {
   const dq_config& c = ctx->cfg;
   return ctx->async_alloc && !ctx->profile && !collect_wire && c.variable_width && c.allocator == DQ_ALLOC_FAST;
+}
+// asynchronous rounds small enough for the one-CTA allocation, which then also performs the
+// statistics reduction (one kernel less on the latency path of small all-reduces)
+bool small_alloc_round(const dq_ctx* ctx, uint32_t T, bool async) {
+  return async && !ctx->no_small_alloc && T > 0 && T <= kSmallAllocMaxT;
 }
 
 // stats (already reduced into ctx->gsq / gmean) -> allocation -> chunk plan.  Async: the
@@ -1160,12 +1180,18 @@ void sim_round(dq_ctx* ctx, const float* const* xs, size_t d, float* out, int fl
   }
   DQ_CUDA(cudaEventRecord(ctx->ev0, st));
   reserve_round(ctx, T, n);
+  ctx->pending_red = StatsReduce{};
   timed(ctx, K_STATS, 4.0 * n * d + 8.0 * n * T, st,
         [&] { launch_stats(xs, n, d, T, ctx->mean_all.p, ctx->sq_all.p, st); });
-  timed(ctx, K_REDUCE, 8.0 * (n + 1) * T, st,
-        [&] { launch_reduce_stats(ctx->mean_all.p, ctx->sq_all.p, n, T, ctx->gmean.p, ctx->gsq.p, st); });
-  DQ_CUDA(cudaGetLastError());
   const bool async = async_alloc_ok(ctx, collect_wire);
+  if (small_alloc_round(ctx, T, async)) {
+    StatsReduce& rd = ctx->pending_red;
+    rd = StatsReduce{ctx->mean_all.p, ctx->sq_all.p, nullptr, nullptr, n, T, ctx->gmean.p, ctx->gsq.p};
+  } else {
+    timed(ctx, K_REDUCE, 8.0 * (n + 1) * T, st,
+          [&] { launch_reduce_stats(ctx->mean_all.p, ctx->sq_all.p, n, T, ctx->gmean.p, ctx->gsq.p, st); });
+  }
+  DQ_CUDA(cudaGetLastError());
   Prepared p = prepare(ctx, T, st, async);
   if (!async) fill_info_alloc(info, p);
 
@@ -1604,7 +1630,36 @@ bool stats_setup(dq_ctx* ctx, uint32_t T, cudaStream_t st) {
 // into gather slot r of every rank - the all-gather - and one decode launch per rank
 // consumes all n gather slots as their units land.
 void peer_gather_decode(dq_ctx* ctx, const Prepared& p, const std::vector<Layout>& lays,
-                        const std::vector<char>& decoded, float* out, size_t d, cudaStream_t st);
+                        const std::vector<char>& decoded, float* out, size_t d, cudaStream_t st,
+                        bool early = false);
+
+// Small rounds (every chunk <= kSmallChunkSGs super-groups): the gather decode is launched
+// on a side stream right after the allocation, before the hop kernels, and consumes every
+// gather slot (its own too) unit by unit as the sinks' stores land - its launch, prologue
+// and most of its work leave the latency path.  Its grid is capped far below the GPU's
+// resident capacity (kEarlyDecodeCtas), so its waiting CTAs never keep a hop kernel's CTAs
+// from being scheduled.  The stream joins back before the round's end event.
+constexpr uint32_t kEarlyDecodeCtas = 64;
+bool early_gather(const std::vector<Layout>& lays) {
+  for (const Layout& L : lays)
+    if (L.nsg > kSmallChunkSGs) return false;
+  return true;
+}
+void early_gather_begin(dq_ctx* ctx, const Prepared& p, const std::vector<Layout>& lays, float* out, size_t d,
+                        cudaStream_t st) {
+  if (!ctx->gstream) {
+    int lo = 0, hi = 0;
+    DQ_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    DQ_CUDA(cudaStreamCreateWithPriority(&ctx->gstream, cudaStreamNonBlocking, hi));
+    DQ_CUDA(cudaEventCreateWithFlags(&ctx->gfork, cudaEventDisableTiming));
+    DQ_CUDA(cudaEventCreateWithFlags(&ctx->gjoin, cudaEventDisableTiming));
+  }
+  DQ_CUDA(cudaEventRecord(ctx->gfork, st));
+  DQ_CUDA(cudaStreamWaitEvent(ctx->gstream, ctx->gfork, 0));
+  peer_gather_decode(ctx, p, lays, std::vector<char>(lays.size(), 0), out, d, ctx->gstream, true);
+  DQ_CUDA(cudaEventRecord(ctx->gjoin, ctx->gstream));
+}
+void early_gather_end(dq_ctx* ctx, cudaStream_t st) { DQ_CUDA(cudaStreamWaitEvent(st, ctx->gjoin, 0)); }
 
 // Fused own-chunk decode in the peer sinks (launch_quant_dec) only up to this many ranks.
 // Measured at d = 2^28 per rank (profiles/r1_multi_gpu.md): N = 2 the gather decode is
@@ -1628,6 +1683,8 @@ void ring_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>& bas
   const uint32_t right = (me + 1) % n;
   PeerMem& pm = ctx->pm;
   std::vector<char> decoded(n, 0);
+  const bool early = early_gather(lays);
+  if (early) early_gather_begin(ctx, p, lays, out, d, st);
   for (uint32_t h = 0; h < n; ++h) {
     const uint32_t ch = (me + 2 * n - 1 - h) % n;  // sink at h = n-1
     CodecArgs a = bases[ch];
@@ -1661,7 +1718,7 @@ void ring_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>& bas
       a.n_outs = static_cast<int>(n);
     }
     const bool dar = h > 0;
-    if (h + 1 == n && n <= kFuseDecodeMaxRanks) {  // the sink also decodes its record into the output
+    if (h + 1 == n && n <= kFuseDecodeMaxRanks && !early) {  // the sink also decodes its record into the output
       a.dec_out = out;
       decoded[ch] = launch_quant_dec(a, 0, true, st, false);
     }
@@ -1672,14 +1729,15 @@ void ring_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>& bas
       else launch_quant_dec(a, 0, true, st);
     });
   }
-  peer_gather_decode(ctx, p, lays, decoded, out, d, st);
+  if (early) early_gather_end(ctx, st);
+  else peer_gather_decode(ctx, p, lays, decoded, out, d, st);
 }
 
 // Every rank decodes the n gather slots of this round's parity into the output, unit by
 // unit as the sinks' stores land (its own slot is complete: its sink ran earlier on st),
 // except the chunks its own sink already decoded (decoded[c], launch_quant_dec).
 void peer_gather_decode(dq_ctx* ctx, const Prepared& p, const std::vector<Layout>& lays,
-                        const std::vector<char>& decoded, float* out, size_t d, cudaStream_t st) {
+                        const std::vector<char>& decoded, float* out, size_t d, cudaStream_t st, bool early) {
   const uint32_t n = ctx->cfg.n_workers, me = static_cast<uint32_t>(ctx->rank);
   PeerMem& pm = ctx->pm;
   GatherArgs g{};
@@ -1695,7 +1753,9 @@ void peer_gather_decode(dq_ctx* ctx, const Prepared& p, const std::vector<Layout
     g.hi[k] = p.lo[c + 1];
     g.n8[k] = lays[c].n8;
     g.n4[k] = lays[c].n4;
-    g.flags[k] = c == me ? nullptr : reinterpret_cast<const uint32_t*>(pm.base + pm.gflag(c));
+    // the own slot is complete when the decode follows the own sink on st; an early decode
+    // waits for its flags like for the remote slots
+    g.flags[k] = c == me && !early ? nullptr : reinterpret_cast<const uint32_t*>(pm.base + pm.gflag(c));
     g.unit[k] = peer_unit(lays[c].nsg);
     max_nsg = std::max(max_nsg, lays[c].nsg);
     gbytes += 1032.0 * lays[c].nsg + lays[c].bytes();
@@ -1709,7 +1769,7 @@ void peer_gather_decode(dq_ctx* ctx, const Prepared& p, const std::vector<Layout
   g.d = d;
   g.n_workers_f = static_cast<float>(n);
   g.uniform_books = ctx->cfg.non_uniform ? 0 : 1;
-  timed(ctx, K_DECODE, gbytes, st, [&] { launch_gather_decode(g, k, max_nsg, st); });
+  timed(ctx, K_DECODE, gbytes, st, [&] { launch_gather_decode(g, k, max_nsg, st, early ? kEarlyDecodeCtas : 0); });
 }
 
 // halving stage of a butterfly reduce event (topology.cpp:46-54): partner bit n >> (stage + 1)
@@ -1737,6 +1797,8 @@ void butterfly_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>
   auto acc_ptr = [&](uint32_t ch) { return ctx->accs.p + static_cast<size_t>(ch) * max_nsg * 256; };
   std::vector<int> held(n, -1);
   std::vector<char> has_acc(n, 0), decoded(n, 0);
+  const bool early = early_gather(lays);
+  if (early) early_gather_begin(ctx, p, lays, out, d, st);
   auto prep = [&](uint32_t ch) {
     CodecArgs a = bases[ch];
     a.unit = peer_unit(lays[ch].nsg);
@@ -1793,7 +1855,7 @@ void butterfly_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>
             a.out_flags[j] = reinterpret_cast<uint32_t*>(pm.peer[q] + pm.gflag(ch));
           }
           a.n_outs = static_cast<int>(n);
-          if (n <= kFuseDecodeMaxRanks) a.dec_out = out;  // and decoded into this rank's output
+          if (n <= kFuseDecodeMaxRanks && !early) a.dec_out = out;  // and decoded into this rank's output
           decoded[ch] = launch_quant_dec(a, src, true, st, false);
           const double ob = decoded[ch] ? 1032.0 * lays[ch].nsg : 0.0;
           timed(ctx, K_DAR, quant_bytes(lays[ch], true) + ob, st, [&] {
@@ -1808,7 +1870,8 @@ void butterfly_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>
       }
     }
   }
-  peer_gather_decode(ctx, p, lays, decoded, out, d, st);
+  if (early) early_gather_end(ctx, st);
+  else peer_gather_decode(ctx, p, lays, decoded, out, d, st);
 }
 
 // NCCL reports errors of enqueued work (a dead peer, a network failure) asynchronously
@@ -1844,7 +1907,13 @@ void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info
   }
   DQ_CUDA(cudaEventRecord(ctx->ev0, st));
   reserve_round(ctx, T, n);
+  ctx->pending_red = StatsReduce{};
   const float* const* dxp = &x;
+  // peer transport (default scale format): the round allocates asynchronously; the NCCL
+  // transport and the ablation formats size their messages on the host (synchronous)
+  const bool peer_pre = ctx->transport == DQ_TRANSPORT_PEER && n <= static_cast<uint32_t>(kMaxPeers) &&
+                        c.group_size == 16 && c.hierarchical_scales;
+  const bool fuse_red = small_alloc_round(ctx, T, peer_pre && async_alloc_ok(ctx, false));
   // (a) local stats into this rank's row, (b) all-gather rows, fixed-order fp64 reduce (H4).
   // Peer transport: the all-gather is fused into the statistics kernel (each block stores
   // its rows into every rank's exchange area over NVLink, the last block raises the row
@@ -1862,10 +1931,15 @@ void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info
     sp.n = n;
     sp.epoch = ctx->dev_epoch.p;  // advanced by the statistics kernel: this round's epoch
     timed(ctx, K_STATS, 4.0 * d + 8.0 * T * n, st, [&] { launch_stats_peer(dxp, d, T, sp, st); });
-    timed(ctx, K_REDUCE, 8.0 * (n + 1) * T, st, [&] {
-      launch_reduce_stats_peer(sm.mean(sm.base, 0), sm.sq(sm.base, 0), sm.flags(sm.base), ctx->dev_epoch.p, n, T,
-                               sm.T, ctx->gmean.p, ctx->gsq.p, st);
-    });
+    if (fuse_red) {
+      ctx->pending_red = StatsReduce{sm.mean(sm.base, 0), sm.sq(sm.base, 0), sm.flags(sm.base), ctx->dev_epoch.p, n,
+                                     sm.T, ctx->gmean.p, ctx->gsq.p};
+    } else {
+      timed(ctx, K_REDUCE, 8.0 * (n + 1) * T, st, [&] {
+        launch_reduce_stats_peer(sm.mean(sm.base, 0), sm.sq(sm.base, 0), sm.flags(sm.base), ctx->dev_epoch.p, n, T,
+                                 sm.T, ctx->gmean.p, ctx->gsq.p, st);
+      });
+    }
   } else {
     float* my_mean = ctx->mean_all.p + static_cast<size_t>(me) * T;
     float* my_sq = ctx->sq_all.p + static_cast<size_t>(me) * T;
@@ -1876,14 +1950,13 @@ void dist_round(dq_ctx* ctx, const float* x, size_t d, float* out, dq_round_info
       DQ_NCCL(ncclAllGather(my_sq, ctx->sq_all.p, T, ncclFloat, ctx->comm, st));
       DQ_NCCL(ncclGroupEnd());
     });
-    timed(ctx, K_REDUCE, 8.0 * (n + 1) * T, st,
-          [&] { launch_reduce_stats(ctx->mean_all.p, ctx->sq_all.p, n, T, ctx->gmean.p, ctx->gsq.p, st); });
+    if (fuse_red)
+      ctx->pending_red = StatsReduce{ctx->mean_all.p, ctx->sq_all.p, nullptr, nullptr, n, T, ctx->gmean.p, ctx->gsq.p};
+    else
+      timed(ctx, K_REDUCE, 8.0 * (n + 1) * T, st,
+            [&] { launch_reduce_stats(ctx->mean_all.p, ctx->sq_all.p, n, T, ctx->gmean.p, ctx->gsq.p, st); });
   }
   DQ_CUDA(cudaGetLastError());
-  // peer transport (default scale format): the round allocates asynchronously; the NCCL
-  // transport and the ablation formats size their messages on the host (synchronous)
-  const bool peer_pre = ctx->transport == DQ_TRANSPORT_PEER && n <= static_cast<uint32_t>(kMaxPeers) &&
-                        c.group_size == 16 && c.hierarchical_scales;
   Prepared p = prepare(ctx, T, st, peer_pre && async_alloc_ok(ctx, false));
   if (!p.a.async) fill_info_alloc(info, p);
 

@@ -76,7 +76,9 @@ struct GatherArgs {
   uint32_t unit[64];
   const uint32_t* epoch_ptr;
 };
-void launch_gather_decode(const GatherArgs& g, uint32_t n_chunks, uint32_t max_nsg, cudaStream_t st);
+// max_ctas > 0 caps the grid (CTAs over all chunks; the kernel walks super-groups grid-strided)
+void launch_gather_decode(const GatherArgs& g, uint32_t n_chunks, uint32_t max_nsg, cudaStream_t st,
+                          uint32_t max_ctas = 0);
 
 void launch_quant(const CodecArgs& a, int src, bool dar, cudaStream_t st);
 // reference wire format on the device (dq_wire.cu): SoA chunk -> header + records, and
@@ -214,6 +216,18 @@ struct HostMsg {
 };
 constexpr int kAllocBins = 1024;
 constexpr int kAllocMaxPasses = 8;
+// The rank-ordered statistics reduction (k_reduce_stats / k_reduce_stats_peer) folded into
+// the one-CTA allocation of small rounds: rows [n][stride] of per-rank means and squares,
+// optional per-row flags (peer exchange, compared with *epoch_ptr), outputs gm / gs (= F).
+struct StatsReduce {
+  const float* mean = nullptr;
+  const float* sq = nullptr;
+  const uint32_t* flags = nullptr;
+  const uint32_t* epoch_ptr = nullptr;
+  uint32_t n = 0, stride = 0;
+  float* gm = nullptr;
+  float* gs = nullptr;
+};
 struct AllocWork {           // device scratch owned by the context
   double* level;             // alpha * log2(F_j) per super-group (NaN when F_j <= 0)
   AllocState* state;
@@ -224,6 +238,7 @@ struct AllocWork {           // device scratch owned by the context
   float* pmean;              // pmean[k] = gmean[perm[k]]
   HostMsg* hmsg;             // asynchronous rounds: mapped host mailbox (null: synchronous rounds)
   float* hF;                 // asynchronous rounds: mapped host copy of F (need_host rounds only)
+  StatsReduce red;           // k_alloc_small: reduce the statistics first (red.mean != null)
 };
 uint32_t alloc_blocks(uint32_t T);
 // Search for the crossing flip and the plateau midpoint u, fully on device: one
@@ -235,6 +250,10 @@ void set_force_host_alloc(int on);
 // asynchronous rounds with T <= 4096: search + assignment in one CTA (false: not applicable)
 bool launch_alloc_small(const float* F, uint32_t T, double alpha, double budget, uint32_t S, AllocWork w,
                         uint8_t* widths, uint32_t* perm, cudaStream_t st);
+constexpr uint32_t kSmallAllocMaxT = 4096;  // launch_alloc_small applies to T <= this
+// chunks of at most this many super-groups run one super-group per warp and peer unit (and
+// their peer rounds launch the gather decode early, dq_engine.cpp early_gather)
+constexpr uint32_t kSmallChunkSGs = 148u * 8 * 2;
 // Slow exact path helpers (rare): neighbour flip of `key` (dir -1: largest key below,
 // +1: smallest key above) -> rec; float-threshold counts -> counts[0] = #F>=t48,
 // counts[1] = #F>=t24.  Both asynchronous on st.

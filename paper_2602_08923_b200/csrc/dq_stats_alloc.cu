@@ -889,13 +889,48 @@ __global__ void __launch_bounds__(kSmallThreads) k_alloc_small(const float* __re
 #define DQ_PHASE() do { } while (0)
 #endif
   DQ_PHASE();
+  // the statistics reduction folded in (small rounds): wait for every rank's rows (peer
+  // exchange), then F_j = the rank-ordered fp64 sum exactly as k_reduce_stats[_peer]
+  const StatsReduce& rd = w.red;
+  if (rd.mean) {
+    if (rd.flags && t == 0) {
+      const uint32_t epoch = *rd.epoch_ptr;
+      for (uint32_t r = 0; r < rd.n; ++r) {
+        uint32_t v;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(rd.flags + r) : "memory");
+        if (v == epoch) continue;
+        const uint64_t t0 = dq_globaltimer();
+        for (;;) {
+          __nanosleep(64);
+          asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(rd.flags + r) : "memory");
+          if (v == epoch) break;
+          if (dq_globaltimer() - t0 > g_spin_ns) __trap();
+        }
+      }
+    }
+    __syncthreads();
+  }
   // stage F; sort keys ~bits (ascending = F descending) of the positive F_j, stable in j
   uint32_t key[IPT], val[IPT];
   uint32_t npos = 0, nonneg = 0;
 #pragma unroll
   for (int i = 0; i < IPT; ++i) {
     const uint32_t j = static_cast<uint32_t>(t * IPT + i);
-    const float f = j < T ? F[j] : -1.0f;
+    float f = -1.0f;
+    if (j < T) {
+      if (rd.mean) {
+        double a = 0.0, b = 0.0;
+        for (uint32_t r = 0; r < rd.n; ++r) {
+          a = __dadd_rn(a, static_cast<double>(__ldcg(rd.mean + static_cast<uint64_t>(r) * rd.stride + j)));
+          b = __dadd_rn(b, static_cast<double>(__ldcg(rd.sq + static_cast<uint64_t>(r) * rd.stride + j)));
+        }
+        rd.gm[j] = static_cast<float>(__ddiv_rn(a, static_cast<double>(rd.n)));
+        f = static_cast<float>(b);
+        rd.gs[j] = f;
+      } else {
+        f = F[j];
+      }
+    }
     if (j < T) Fs[j] = f;
     const bool pos = f > 0.0f;
     key[i] = pos ? ~__float_as_uint(f) : 0xffffffffu;
@@ -1238,7 +1273,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_alloc_small(const float* __re
 
 bool launch_alloc_small(const float* F, uint32_t T, double alpha, double budget, uint32_t S, AllocWork w,
                         uint8_t* widths, uint32_t* perm, cudaStream_t st) {
-  if (!w.hmsg || T == 0 || T > 4096) return false;
+  if (!w.hmsg || T == 0 || T > kSmallAllocMaxT) return false;
   auto go = [&](auto ipt) {
     constexpr int IPT = decltype(ipt)::value;
     constexpr size_t bytes = SmallSmem<IPT>::bytes;
