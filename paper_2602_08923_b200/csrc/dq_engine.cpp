@@ -234,8 +234,6 @@ struct dq_ctx {
   DevBuf<float> accs;     // per-worker chunk accumulators (butterfly)
   DevBuf<uint32_t> pcache; // simulated round: the chunk's permutation slices (slots 1..n-1)
   DevBuf<float> stage;    // host-round staging of inputs / output
-  cudaStream_t gstream = nullptr;      // small peer rounds: the gather decode, launched early
-  cudaEvent_t gfork = nullptr, gjoin = nullptr;
   std::vector<cudaStream_t> cstreams;  // simulated rounds: concurrent chunk chains
   std::vector<cudaEvent_t> cjoin;
   cudaEvent_t cfork = nullptr;
@@ -309,9 +307,6 @@ struct dq_ctx {
     for (cudaStream_t s2 : cstreams) cudaStreamDestroy(s2);
     for (cudaEvent_t e2 : cjoin) cudaEventDestroy(e2);
     if (cfork) cudaEventDestroy(cfork);
-    if (gstream) cudaStreamDestroy(gstream);
-    if (gfork) cudaEventDestroy(gfork);
-    if (gjoin) cudaEventDestroy(gjoin);
     if (svc.joinable()) {
       svc_stop = true;
       svc.join();
@@ -1630,36 +1625,8 @@ bool stats_setup(dq_ctx* ctx, uint32_t T, cudaStream_t st) {
 // into gather slot r of every rank - the all-gather - and one decode launch per rank
 // consumes all n gather slots as their units land.
 void peer_gather_decode(dq_ctx* ctx, const Prepared& p, const std::vector<Layout>& lays,
-                        const std::vector<char>& decoded, float* out, size_t d, cudaStream_t st,
-                        bool early = false);
+                        const std::vector<char>& decoded, float* out, size_t d, cudaStream_t st);
 
-// Small rounds (every chunk <= kSmallChunkSGs super-groups): the gather decode is launched
-// on a side stream right after the allocation, before the hop kernels, and consumes every
-// gather slot (its own too) unit by unit as the sinks' stores land - its launch, prologue
-// and most of its work leave the latency path.  Its grid is capped far below the GPU's
-// resident capacity (kEarlyDecodeCtas), so its waiting CTAs never keep a hop kernel's CTAs
-// from being scheduled.  The stream joins back before the round's end event.
-constexpr uint32_t kEarlyDecodeCtas = 64;
-bool early_gather(const std::vector<Layout>& lays) {
-  for (const Layout& L : lays)
-    if (L.nsg > kSmallChunkSGs) return false;
-  return true;
-}
-void early_gather_begin(dq_ctx* ctx, const Prepared& p, const std::vector<Layout>& lays, float* out, size_t d,
-                        cudaStream_t st) {
-  if (!ctx->gstream) {
-    int lo = 0, hi = 0;
-    DQ_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    DQ_CUDA(cudaStreamCreateWithPriority(&ctx->gstream, cudaStreamNonBlocking, hi));
-    DQ_CUDA(cudaEventCreateWithFlags(&ctx->gfork, cudaEventDisableTiming));
-    DQ_CUDA(cudaEventCreateWithFlags(&ctx->gjoin, cudaEventDisableTiming));
-  }
-  DQ_CUDA(cudaEventRecord(ctx->gfork, st));
-  DQ_CUDA(cudaStreamWaitEvent(ctx->gstream, ctx->gfork, 0));
-  peer_gather_decode(ctx, p, lays, std::vector<char>(lays.size(), 0), out, d, ctx->gstream, true);
-  DQ_CUDA(cudaEventRecord(ctx->gjoin, ctx->gstream));
-}
-void early_gather_end(dq_ctx* ctx, cudaStream_t st) { DQ_CUDA(cudaStreamWaitEvent(st, ctx->gjoin, 0)); }
 
 // Fused own-chunk decode in the peer sinks (launch_quant_dec) only up to this many ranks.
 // Measured at d = 2^28 per rank (profiles/r1_multi_gpu.md): N = 2 the gather decode is
@@ -1683,8 +1650,6 @@ void ring_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>& bas
   const uint32_t right = (me + 1) % n;
   PeerMem& pm = ctx->pm;
   std::vector<char> decoded(n, 0);
-  const bool early = early_gather(lays);
-  if (early) early_gather_begin(ctx, p, lays, out, d, st);
   for (uint32_t h = 0; h < n; ++h) {
     const uint32_t ch = (me + 2 * n - 1 - h) % n;  // sink at h = n-1
     CodecArgs a = bases[ch];
@@ -1718,7 +1683,7 @@ void ring_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>& bas
       a.n_outs = static_cast<int>(n);
     }
     const bool dar = h > 0;
-    if (h + 1 == n && n <= kFuseDecodeMaxRanks && !early) {  // the sink also decodes its record into the output
+    if (h + 1 == n && n <= kFuseDecodeMaxRanks) {  // the sink also decodes its record into the output
       a.dec_out = out;
       decoded[ch] = launch_quant_dec(a, 0, true, st, false);
     }
@@ -1729,15 +1694,14 @@ void ring_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>& bas
       else launch_quant_dec(a, 0, true, st);
     });
   }
-  if (early) early_gather_end(ctx, st);
-  else peer_gather_decode(ctx, p, lays, decoded, out, d, st);
+  peer_gather_decode(ctx, p, lays, decoded, out, d, st);
 }
 
 // Every rank decodes the n gather slots of this round's parity into the output, unit by
 // unit as the sinks' stores land (its own slot is complete: its sink ran earlier on st),
 // except the chunks its own sink already decoded (decoded[c], launch_quant_dec).
 void peer_gather_decode(dq_ctx* ctx, const Prepared& p, const std::vector<Layout>& lays,
-                        const std::vector<char>& decoded, float* out, size_t d, cudaStream_t st, bool early) {
+                        const std::vector<char>& decoded, float* out, size_t d, cudaStream_t st) {
   const uint32_t n = ctx->cfg.n_workers, me = static_cast<uint32_t>(ctx->rank);
   PeerMem& pm = ctx->pm;
   GatherArgs g{};
@@ -1753,9 +1717,7 @@ void peer_gather_decode(dq_ctx* ctx, const Prepared& p, const std::vector<Layout
     g.hi[k] = p.lo[c + 1];
     g.n8[k] = lays[c].n8;
     g.n4[k] = lays[c].n4;
-    // the own slot is complete when the decode follows the own sink on st; an early decode
-    // waits for its flags like for the remote slots
-    g.flags[k] = c == me && !early ? nullptr : reinterpret_cast<const uint32_t*>(pm.base + pm.gflag(c));
+    g.flags[k] = c == me ? nullptr : reinterpret_cast<const uint32_t*>(pm.base + pm.gflag(c));
     g.unit[k] = peer_unit(lays[c].nsg);
     max_nsg = std::max(max_nsg, lays[c].nsg);
     gbytes += 1032.0 * lays[c].nsg + lays[c].bytes();
@@ -1769,7 +1731,7 @@ void peer_gather_decode(dq_ctx* ctx, const Prepared& p, const std::vector<Layout
   g.d = d;
   g.n_workers_f = static_cast<float>(n);
   g.uniform_books = ctx->cfg.non_uniform ? 0 : 1;
-  timed(ctx, K_DECODE, gbytes, st, [&] { launch_gather_decode(g, k, max_nsg, st, early ? kEarlyDecodeCtas : 0); });
+  timed(ctx, K_DECODE, gbytes, st, [&] { launch_gather_decode(g, k, max_nsg, st); });
 }
 
 // halving stage of a butterfly reduce event (topology.cpp:46-54): partner bit n >> (stage + 1)
@@ -1797,8 +1759,6 @@ void butterfly_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>
   auto acc_ptr = [&](uint32_t ch) { return ctx->accs.p + static_cast<size_t>(ch) * max_nsg * 256; };
   std::vector<int> held(n, -1);
   std::vector<char> has_acc(n, 0), decoded(n, 0);
-  const bool early = early_gather(lays);
-  if (early) early_gather_begin(ctx, p, lays, out, d, st);
   auto prep = [&](uint32_t ch) {
     CodecArgs a = bases[ch];
     a.unit = peer_unit(lays[ch].nsg);
@@ -1855,7 +1815,7 @@ void butterfly_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>
             a.out_flags[j] = reinterpret_cast<uint32_t*>(pm.peer[q] + pm.gflag(ch));
           }
           a.n_outs = static_cast<int>(n);
-          if (n <= kFuseDecodeMaxRanks && !early) a.dec_out = out;  // and decoded into this rank's output
+          if (n <= kFuseDecodeMaxRanks) a.dec_out = out;  // and decoded into this rank's output
           decoded[ch] = launch_quant_dec(a, src, true, st, false);
           const double ob = decoded[ch] ? 1032.0 * lays[ch].nsg : 0.0;
           timed(ctx, K_DAR, quant_bytes(lays[ch], true) + ob, st, [&] {
@@ -1870,8 +1830,7 @@ void butterfly_peer(dq_ctx* ctx, const Prepared& p, const std::vector<CodecArgs>
       }
     }
   }
-  if (early) early_gather_end(ctx, st);
-  else peer_gather_decode(ctx, p, lays, decoded, out, d, st);
+  peer_gather_decode(ctx, p, lays, decoded, out, d, st);
 }
 
 // NCCL reports errors of enqueued work (a dead peer, a network failure) asynchronously

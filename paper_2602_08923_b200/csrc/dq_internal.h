@@ -251,8 +251,7 @@ void set_force_host_alloc(int on);
 bool launch_alloc_small(const float* F, uint32_t T, double alpha, double budget, uint32_t S, AllocWork w,
                         uint8_t* widths, uint32_t* perm, cudaStream_t st);
 constexpr uint32_t kSmallAllocMaxT = 4096;  // launch_alloc_small applies to T <= this
-// chunks of at most this many super-groups run one super-group per warp and peer unit (and
-// their peer rounds launch the gather decode early, dq_engine.cpp early_gather)
+// chunks of at most this many super-groups run one super-group per warp and peer unit
 constexpr uint32_t kSmallChunkSGs = 148u * 8 * 2;
 // Slow exact path helpers (rare): neighbour flip of `key` (dir -1: largest key below,
 // +1: smallest key above) -> rec; float-threshold counts -> counts[0] = #F>=t48,
