@@ -107,10 +107,24 @@ __host__ __device__ inline uint64_t purpose_prefix(uint64_t seed, uint64_t round
 
 // r % k for the Fisher-Yates draw, k = i+1 <= 64.  Compile-time k lets nvcc
 // strength-reduce; the runtime path handles arbitrary worker counts.
+// K = 3, 5: 2^32 = 1 (mod K), so r = lo + hi (mod K); lo + hi < 2^33 folds once more into
+// 32 bits (its high word is 0 or 1 and the sum cannot overflow again) and the 32-bit
+// remainder is one multiply-high - 5 instructions instead of the 64-bit magic division.
+// K = 6: from r mod 3 and the parity of r (CRT).
 template <int K>
-__device__ __forceinline__ uint32_t mod_const(uint64_t r) {
-  if constexpr ((K & (K - 1)) == 0) return static_cast<uint32_t>(r) & (K - 1);
-  else return static_cast<uint32_t>(r % K);
+__host__ __device__ __forceinline__ uint32_t mod_const(uint64_t r) {
+  if constexpr ((K & (K - 1)) == 0) {
+    return static_cast<uint32_t>(r) & (K - 1);
+  } else if constexpr (K == 3 || K == 5) {
+    const uint64_t s = (r & 0xffffffffull) + (r >> 32);
+    const uint32_t t = static_cast<uint32_t>(s) + static_cast<uint32_t>(s >> 32);
+    return t % K;
+  } else if constexpr (K == 6) {
+    const uint32_t a = mod_const<3>(r);
+    return a + 3u * ((a ^ static_cast<uint32_t>(r)) & 1u);
+  } else {
+    return static_cast<uint32_t>(r % K);
+  }
 }
 
 // ---------------------------------------------------------------- bf16
