@@ -936,6 +936,7 @@ AllocResult allocate_fast_async(dq_ctx* ctx, const dq_config& c, const float* dF
   w.red = red;
   if (!ctx->no_small_alloc && launch_alloc_small(dF, T, kAlpha, budget, S, w, dW, dP, st)) {
     DQ_CUDA(cudaGetLastError());
+    ctx->prof_launches[K_ALLOC_SEARCH] += 1;  // launch count only (asynchronous rounds are not event-timed)
     return r;
   }
   if (red.mean) {  // (not reached: the caller folds the reduction only into small rounds)
@@ -947,6 +948,8 @@ AllocResult allocate_fast_async(dq_ctx* ctx, const dq_config& c, const float* dF
   DQ_CUDA(launch_alloc_search(dF, T, kAlpha, static_cast<uint64_t>(W), budget, S, w, st));
   launch_alloc_assign(dF, T, 0.f, 0.f, true, w, dW, dP, st);
   DQ_CUDA(cudaGetLastError());
+  ctx->prof_launches[K_ALLOC_SEARCH] += kKindLaunches[K_ALLOC_SEARCH];
+  ctx->prof_launches[K_ALLOC_ASSIGN] += kKindLaunches[K_ALLOC_ASSIGN];
   return r;
 }
 
